@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 inner-solve hot path.
+
+Default workload (BASELINE.json configs[1], "config 2"): inexact low-rank ADI
+on the 3-D convection-diffusion pair n=64,000 / m=27,000, r=2, complex128,
+pinned reference heuristic shifts (npairs=12), Jacobi-FGMRES(30) inner solves
+with the paper's dynamic inner tolerance (dynamic_mid_bl), outer tolerance
+1e-8.  One "step" = one full ADI solve to the 1e-8 residual.
+
+  metric  = "wall time to 1e-8 ADI residual" (s, lower is better)
+  value   = device-resident solve, inputs already in HBM
+  e2e     = the public API call run(problem, config, shifts) with host
+            scipy/numpy inputs: uploads, solve and the Z/Y download inside
+  roofline= the dominant kernel class, from a CUDA-event-instrumented pass
+  cpu_baseline = the reference's own CPU path (Jacobi-BiCGstab ADI, restated
+            in oracle/) on the host, rank 0, N=1
+
+`--impl reference` times that CPU path alone (the reference arm).
+`--config c4` runs the inner-solve microbenchmark (SpMM/orthogonalisation GB/s).
+Multi-GPU (torchrun): config 2 is single-GPU in BASELINE.json, so N ranks run
+N independent replicas ("replicas only", weak scaling); value = max over ranks.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+import warnings
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# -- distributed plumbing --------------------------------------------------------
+
+class Dist:
+    def __init__(self, want_gpus):
+        self.rank = int(os.environ.get("RANK", 0))
+        self.world = int(os.environ.get("WORLD_SIZE", 1))
+        self.local = int(os.environ.get("LOCAL_RANK", 0))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x):
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([float(x)], device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# -- clocks during the timed region ------------------------------------------------
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -- workloads ------------------------------------------------------------------------
+
+def build_c2():
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200 import configs as cfgs
+    spec = cfgs.CONFIGS["c2"]
+    A, B, M, C, f, g = cfgs.build_problem("c2")
+    pairs, cyclic = spec.load_shift_pairs()
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
+    cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax,
+                       outer_tolerance=spec.outer_tolerance,
+                       precond_kind_A="jacobi", precond_kind_B="jacobi")
+    seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
+    return spec, prob, cfg, seq, (A, B, M, C, f, g, pairs, cyclic)
+
+
+def c2_config_json(spec, prob, extra=None):
+    out = {"workload": "config 2: ADI to 1e-8, 3-D conv-diff 40^3/30^3, r=2, complex128, "
+                       "Jacobi-FGMRES(30), dynamic_mid_bl",
+           "n": prob.n, "m": prob.m, "r": prob.r, "nnz_A": int(prob.A.nnz),
+           "nnz_B": int(prob.B.nnz), "kmax": spec.kmax, "restart": spec.restart,
+           "flexible": spec.flexible, "strategy": spec.strategy,
+           "shifts": "configs/shifts_c2.json (reference heuristic_shifts, npairs=12)",
+           "seed": spec.seed, "l2": "flushed between timed steps (256 MiB write)",
+           "parallelism": "replicas"}
+    if extra:
+        out.update(extra)
+    return out
+
+
+def cpu_reference_solve(kmax=None):
+    """The reference's own CPU path for config 2 (Jacobi-BiCGstab ADI), restated
+    in oracle/ (the reference cannot travel to the GPU box).  Returns seconds
+    and the outer step count."""
+    from oracle import sylvadi_oracle as orc
+    from paper_2312_02891_b200 import configs as cfgs
+    spec = cfgs.CONFIGS["c2"]
+    A, B, M, C, f, g = cfgs.build_problem("c2")
+    pairs, cyclic = spec.load_shift_pairs()
+    cfg = orc.Config(strategy=spec.strategy, kmax=kmax or spec.kmax,
+                     outer_tolerance=spec.outer_tolerance)
+    bA = orc.Binding("A", A, None, solver="bicgstab")
+    bB = orc.Binding("B", B, None, solver="bicgstab")
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        run = orc.run_adi(A, B, f, g, cfg, pairs, bA, bB, cyclic=cyclic)
+    return time.perf_counter() - t0, run.outer_iterations, bool(run.converged)
+
+
+def _pool_solve(_):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    return cpu_reference_solve()
+
+
+def run_reference_arm(args, dist):
+    """--impl reference: rank 0 times the reference's CPU path; other ranks exit."""
+    if dist.rank != 0:
+        return None
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    workers = max(1, min(args.steps, cores))
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers) as pool:
+        for _ in range(args.warmup):
+            pool.map(_warm_solve, range(workers))
+        t0 = time.perf_counter()
+        results = pool.map(_pool_solve, range(args.steps))
+        wall = time.perf_counter() - t0
+    secs = [r[0] for r in results]
+    value = statistics.mean(secs)
+    spec, prob, _, _, _ = build_c2()
+    line = {
+        "metric": "wall time to 1e-8 ADI residual", "value": value, "unit": "s",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * value, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded reference generators)",
+        "config": c2_config_json(spec, prob, {"outer_steps": results[0][1],
+                                              "converged": all(r[2] for r in results),
+                                              "inner": "Jacobi-BiCGstab (reference path)"}),
+        "cpu_baseline": {"value": value, "unit": "s", "cores": workers, "kind": "port",
+                         "sample": f"{args.steps} full config-2 solves of the reference's "
+                                   f"Jacobi-BiCGstab ADI (oracle/ restatement), one per "
+                                   f"process on {workers} host cores; wall {wall:.1f}s"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def _warm_solve(_):
+    return cpu_reference_solve(kmax=1)
+
+
+def profile_pass(eng):
+    """One instrumented solve: per-kernel-class device time and algorithmic bytes."""
+    from paper_2312_02891_b200 import _lib
+    lib = _lib.load()
+    wss = list(eng.bA._workspaces.values()) + list(eng.bB._workspaces.values())
+    for ws in wss:
+        lib.sad_gmres_profile(ws.handle, 1, None)
+    sol, rep, _ = eng.run()
+    tot = np.zeros(8)
+    for ws in wss:
+        st = np.zeros(8)
+        lib.sad_gmres_profile(ws.handle, 0, st.ctypes.data)
+        tot += st
+    return tot, rep
+
+
+def run_ours_c2(args, dist):
+    import torch
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200 import _lib
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    spec, prob, cfg, seq, raw = build_c2()
+    eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible, device=dev)
+    eng.warm()
+    for _ in range(args.warmup):
+        _, rep, _ = eng.run()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    clocks = Clocks(dev)
+    times, reps = [], []
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.sad_kernel_launches()
+    clocks.start()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, rep, _ = eng.run()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        reps.append(rep)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ck = clocks.stop()
+    launches = lib.sad_kernel_launches() - launches0
+    ms = statistics.mean(times)
+    ms_max = dist.max(ms)
+    rep = reps[-1]
+
+    # instrumented pass for the roofline
+    prof, prep = profile_pass(eng)
+    peak, peak_kind = hbm_peak()
+    spmm_gbs = prof[2] / (prof[0] * 1e-3) / 1e9 if prof[0] > 0 else 0.0
+    orth_gbs = prof[5] / (prof[3] * 1e-3) / 1e9 if prof[3] > 0 else 0.0
+    dominant = "cgs2_orthogonalisation" if prof[3] >= prof[0] else "shifted_spmm"
+    ach, traffic_bytes, launches_dom = ((orth_gbs, prof[5], prof[4]) if dominant.startswith("cgs2")
+                                        else (spmm_gbs, prof[2], prof[1]))
+
+    # e2e through the public API with host inputs
+    e2e_times = []
+    A, B, M, C, f, g, pairs, cyclic = raw
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hprob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
+        sol, erep = pb.run(hprob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
+                           device=dev)
+        Zh, Yh = sol.Z, sol.Y
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e = dist.max(statistics.mean(e2e_times))
+    h2d = (A.indptr.nbytes + A.indices.nbytes + A.data.nbytes
+           + 2 * (B.indptr.nbytes + B.indices.nbytes + B.data.nbytes)
+           + f.nbytes + g.nbytes)
+    d2h = Zh.nbytes + Yh.nbytes
+
+    line = {
+        "metric": "wall time to 1e-8 ADI residual", "value": ms_max / 1000.0, "unit": "s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded reference generators)",
+        "config": c2_config_json(spec, prob, {
+            "outer_steps": rep.outer_iterations, "converged": rep.converged,
+            "final_scaled_residual": rep.final_scaled_residual,
+            "sum_inner_A": rep.sum_inner_A, "sum_inner_B": rep.sum_inner_B,
+            "inner": "Jacobi-FGMRES(30) batched per column, CGS2, device Givens"}),
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": None, "kernel": dominant,
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": traffic_bytes / max(launches_dom, 1),
+                     "measured": "CUDA events on the solve streams, instrumented pass over "
+                                 "one full solve after the timed region"},
+        "kernels": {"spmm": {"ms": prof[0], "launches": int(prof[1]), "gbs": spmm_gbs,
+                             "frac_of_peak": spmm_gbs / peak},
+                    "cgs2": {"ms": prof[3], "steps": int(prof[4]), "gbs": orth_gbs,
+                             "frac_of_peak": orth_gbs / peak},
+                    "cycle_end": {"ms": prof[6], "cycles": int(prof[7])},
+                    "instrumented_solve_ms": prep.wall_ms},
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "clocks": ck,
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        secs, steps_cpu, conv = cpu_reference_solve()
+        line["cpu_baseline"] = {"value": secs, "unit": "s", "cores": 1, "kind": "port",
+                                "sample": f"one full config-2 solve of the reference's "
+                                          f"Jacobi-BiCGstab ADI (oracle/ restatement), "
+                                          f"{steps_cpu} outer steps, converged={conv}"}
+    return line if dist.rank == 0 else None
+
+
+def run_ours_c4(args, dist):
+    """Inner-solve microbenchmark (config 4): 100 fixed GMRES steps, r=8."""
+    import torch
+    from paper_2312_02891_b200 import GpuGmresBinding, _lib
+    from paper_2312_02891_b200 import configs as cfgs
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    n0 = args.c4_n0
+    A, X = cfgs.build_c4(n0=n0, r=8, seed=0)
+    # shift alpha = 0.1 * lambda_max estimate; Gershgorin bound of the stencil
+    lam = -abs(A.diagonal()).max() * 2.0
+    shift = 0.1 * lam
+    steps = args.c4_steps
+    gb = GpuGmresBinding("A", A, None, precond_kind="jacobi", restart=steps, device=dev)
+    rhs = torch.from_numpy(X).cuda()
+    x = torch.empty_like(rhs)
+    res = torch.empty_like(rhs)
+    op = gb.operator(shift)
+    ws = gb.workspace(8, _lib.SAD_F64)
+    for _ in range(args.warmup):
+        ws.fixed(op, rhs, x, res, steps)
+    clocks = Clocks(dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.sad_kernel_launches()
+    clocks.start()
+    tims = np.zeros(4)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, tm = ws.fixed(op, rhs, x, res, steps, timed=True)
+        tims += tm
+    wall = time.perf_counter() - t0
+    ck = clocks.stop()
+    launches = lib.sad_kernel_launches() - l0
+    n, r = A.shape[0], 8
+    blk = n * r * 8
+    spmm_b = A.nnz * 12 + 4 * (n + 1) + 2 * blk + n * 8
+    orth_b = sum((4 * (j + 1) + 6) * blk for j in range(steps))
+    spmm_gbs = args.steps * steps * spmm_b / (tims[0] * 1e-3) / 1e9
+    orth_gbs = args.steps * orth_b / (tims[1] * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+    line = {"metric": "inner SpMM GB/s", "value": spmm_gbs, "unit": "GB/s",
+            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * wall / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"config 4: {n0}^2 conv-diff, r=8, "
+                                                        f"{steps} fixed GMRES steps",
+                                            "n": n, "nnz": int(A.nnz)},
+            "roofline": {"bound": "hbm", "achieved": spmm_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": spmm_gbs / peak, "traffic": None, "kernel": "shifted_spmm",
+                         "peak_kind": peak_kind},
+            "kernels": {"spmm_ms": tims[0], "orth_ms": tims[1], "orth_gbs": orth_gbs,
+                        "orth_frac": orth_gbs / peak, "cycle_end_ms": tims[2],
+                        "init_ms": tims[3]},
+            "gpu_launches": int(launches), "clocks": ck}
+    return line if dist.rank == 0 else None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--c4-n0", type=int, default=4096)
+    ap.add_argument("--c4-steps", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        dist = Dist(0)
+        line = run_reference_arm(args, dist)
+    else:
+        dist = Dist(args.gpus)
+        line = run_ours_c2(args, dist) if args.config == "c2" else run_ours_c4(args, dist)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,114 @@
+"""ctypes binding of libsylvadi_b200.so (the C-ABI in include/sylvadi_b200.h).
+
+The shared library is built in-tree (``python -m paper_2312_02891_b200._build``
+or ``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or no CUDA device is present, every GPU entry point raises.
+"""
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsylvadi_b200.so")
+
+SAD_OK, SAD_EINVAL, SAD_EBREAKDOWN, SAD_ECUDA, SAD_ENCCL, SAD_ENOMEM = range(6)
+SAD_F64, SAD_C128 = 0, 1
+SAD_PRECOND_NONE, SAD_PRECOND_JACOBI = 0, 1
+
+#: every symbol declared in include/sylvadi_b200.h with (restype, argtypes)
+_c = ctypes
+_vp = _c.c_void_p
+_i64 = _c.c_int64
+SIGNATURES = {
+    "sad_version": (_c.c_int, []),
+    "sad_kernel_launches": (_i64, []),
+    "sad_gmres_profile": (_c.c_int, [_vp, _c.c_int, _vp]),
+    "sad_ctx_create": (_c.c_int, [_c.c_int, _c.POINTER(_vp)]),
+    "sad_ctx_destroy": (_c.c_int, [_vp]),
+    "sad_last_error": (_c.c_char_p, [_vp]),
+    "sad_ctx_num_sms": (_c.c_int, [_vp]),
+    "sad_csr_create": (_c.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _c.c_int,
+                                  _c.POINTER(_vp)]),
+    "sad_csr_destroy": (_c.c_int, [_vp]),
+    "sad_csr_nnz": (_i64, [_vp]),
+    "sad_op_create": (_c.c_int, [_vp, _vp, _vp, _c.c_double, _c.c_double, _c.c_int,
+                                 _c.c_int, _c.POINTER(_vp)]),
+    "sad_op_destroy": (_c.c_int, [_vp]),
+    "sad_op_get_dinv": (_c.c_int, [_vp, _vp]),
+    "sad_op_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
+    "sad_op_residual": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),
+    "sad_csr_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _c.c_int, _vp, _vp, _vp]),
+    "sad_gmres_create": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
+                                    _c.POINTER(_vp)]),
+    "sad_gmres_destroy": (_c.c_int, [_vp]),
+    "sad_gmres_bytes": (_i64, [_vp]),
+    "sad_gmres_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp,
+                                   _vp, _vp, _vp]),
+    "sad_gmres_fixed": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_int, _vp, _vp, _vp]),
+    "sad_gram": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),
+    "sad_axpy": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.c_double, _c.c_double,
+                            _vp, _vp, _vp]),
+}
+
+
+class FactorizationBreakdown(RuntimeError):
+    """Zero Jacobi diagonal (the reference's precond.FactorizationBreakdown)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure inside libsylvadi_b200."""
+
+
+_LIB = None
+
+
+def load(path=None):
+    """Load the shared library (once) and attach the ctypes signatures."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise ImportError(
+            f"{p} not found: build it with `python -m paper_2312_02891_b200._build` "
+            "(there is no CPU fallback for the inner-solve path)")
+    lib = ctypes.CDLL(p)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def check(rc, ctx=None):
+    """Map a status code to the reference's exception classes."""
+    if rc == SAD_OK:
+        return
+    lib = load()
+    msg = lib.sad_last_error(ctx).decode() if ctx else f"status {rc}"
+    if rc == SAD_EINVAL:
+        raise ValueError(msg)
+    if rc == SAD_EBREAKDOWN:
+        raise FactorizationBreakdown(msg)
+    if rc == SAD_ENOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+_CTX = {}
+
+
+def context(device=0):
+    """Process-wide context per device (one ctx per device, header contract)."""
+    ctx = _CTX.get(device)
+    if ctx is None:
+        lib = load()
+        h = ctypes.c_void_p()
+        rc = lib.sad_ctx_create(int(device), ctypes.byref(h))
+        if rc != SAD_OK:
+            raise DeviceError(f"sad_ctx_create(device={device}) failed with status {rc}")
+        ctx = h
+        _CTX[device] = ctx
+    return ctx

@@ -1,0 +1,1116 @@
+// sad_capi.cu -- C-ABI of libsylvadi_b200.so (see include/sylvadi_b200.h).
+//
+// Host runtime of the inner-solve hot path: CSR upload (+ explicit transpose),
+// shifted operators with device Jacobi, the batched GMRES/FGMRES driver whose
+// inner loop advances without host synchronisation (device finishers + a
+// host-mapped progress flag polled only to stop issuing work), Gram/axpy block
+// utilities for the device-resident ADI step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/sylvadi_b200.h"
+#include "sad_kernels.cuh"
+
+using namespace sad;
+
+#define SAD_ABI_VERSION 1
+
+struct sad_ctx {
+  int device = 0;
+  int nsm = 148;
+  std::string err;
+  double* scratch = nullptr;     // gram partials
+  unsigned* ticket = nullptr;
+  double2* gram_out = nullptr;
+  double2* gram_host = nullptr;  // pinned
+  int scratch_blocks = 0;
+};
+
+struct DevCsr {
+  int* rowptr = nullptr;
+  int* colidx = nullptr;
+  double* vals = nullptr;
+};
+
+struct sad_csr {
+  sad_ctx* ctx = nullptr;
+  long long nrows = 0, ncols = 0, nnz = 0;
+  DevCsr d, dt;  // matrix and (optional) transpose
+  bool has_t = false;
+  std::vector<int> h_rowptr, h_colidx;   // host copies (transpose/union builds)
+  std::vector<double> h_vals;
+  std::vector<int> ht_rowptr, ht_colidx;
+  std::vector<double> ht_vals;
+};
+
+static std::atomic<unsigned long long> g_op_uid{1};
+static std::atomic<long long> g_launches{0};   // kernels launched by this library
+#define COUNT_LAUNCH(k) g_launches.fetch_add((k), std::memory_order_relaxed)
+
+struct sad_op {
+  sad_ctx* ctx = nullptr;
+  unsigned long long uid = 0;
+  long long n = 0;
+  const int* rowptr = nullptr;
+  const int* colidx = nullptr;
+  const void* vals = nullptr;
+  bool vals_complex = false;
+  bool sigma_identity = false;  // identity mass: shift added in the epilogue
+  double2 sigma_eff = {0.0, 0.0};
+  bool real_ok = true;          // operator (and dinv) real
+  // owned storage for assembled matrices
+  int* own_rowptr = nullptr;
+  int* own_colidx = nullptr;
+  void* own_vals = nullptr;
+  double2* dinv_c = nullptr;
+  double* dinv_r = nullptr;
+  int precond = 0;
+  long long nnz = 0;
+};
+
+struct sad_gmres {
+  sad_ctx* ctx = nullptr;
+  long long n = 0;
+  int R = 1, dtype = 0, m = 1, flexible = 0;
+  size_t esz = 8;
+  void* V = nullptr;
+  void* Z = nullptr;
+  char* state = nullptr;
+  size_t state_bytes = 0;
+  double* part = nullptr;
+  int max_blocks = 0;
+  int pstride = 0;
+  long long* hflag_host = nullptr;
+  long long* hflag_dev = nullptr;
+  GState st{};
+  int64_t bytes = 0;
+  int dot_blocks_per_sm = 1;
+  // profiling (sad_gmres_profile): synchronous stepping with CUDA events
+  int profile = 0;
+  double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+};
+
+// -----------------------------------------------------------------------------
+static int set_err(sad_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return code;
+}
+
+#define CK(ctx, call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return set_err((ctx), SAD_ECUDA, "%s failed: %s (%s:%d)", #call,             \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+  } while (0)
+
+#define CKL(ctx)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return set_err((ctx), SAD_ECUDA, "kernel launch failed: %s (%s:%d)",         \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+  } while (0)
+
+static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" int sad_version(void) { return SAD_ABI_VERSION; }
+extern "C" int64_t sad_kernel_launches(void) { return g_launches.load(); }
+
+extern "C" int sad_ctx_create(int device, sad_ctx** out) {
+  if (!out) return SAD_EINVAL;
+  *out = nullptr;
+  sad_ctx* c = new sad_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete c; return SAD_ECUDA; }
+  int nsm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    delete c;
+    return SAD_ECUDA;
+  }
+  c->nsm = nsm;
+  c->scratch_blocks = nsm * 4;
+  if (cudaMalloc(&c->scratch, (size_t)c->scratch_blocks * 2 * 64 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->ticket, 64) != cudaSuccess ||
+      cudaMalloc(&c->gram_out, 64 * sizeof(double2)) != cudaSuccess ||
+      cudaMallocHost(&c->gram_host, 64 * sizeof(double2)) != cudaSuccess) {
+    delete c;
+    return SAD_ENOMEM;
+  }
+  cudaMemset(c->ticket, 0, 64);
+  *out = c;
+  return SAD_OK;
+}
+
+extern "C" int sad_ctx_destroy(sad_ctx* c) {
+  if (!c) return SAD_OK;
+  cudaFree(c->scratch);
+  cudaFree(c->ticket);
+  cudaFree(c->gram_out);
+  cudaFreeHost(c->gram_host);
+  delete c;
+  return SAD_OK;
+}
+
+extern "C" const char* sad_last_error(const sad_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+extern "C" int sad_ctx_num_sms(const sad_ctx* c) { return c ? c->nsm : 0; }
+
+// -----------------------------------------------------------------------------
+// CSR
+// -----------------------------------------------------------------------------
+static void host_transpose(long long nr, long long nc, const std::vector<int>& rp,
+                           const std::vector<int>& ci, const std::vector<double>& v,
+                           std::vector<int>& trp, std::vector<int>& tci, std::vector<double>& tv) {
+  // counting sort by column; rows visited in increasing order, so each row of the
+  // transpose is sorted by (original) row index -- the same summation order as
+  // scipy's CSC scatter (csc_matvec) for A^T x.
+  trp.assign(nc + 1, 0);
+  for (size_t k = 0; k < ci.size(); ++k) trp[ci[k] + 1]++;
+  for (long long j = 0; j < nc; ++j) trp[j + 1] += trp[j];
+  tci.resize(ci.size());
+  tv.resize(ci.size());
+  std::vector<int> pos(trp.begin(), trp.end() - 1);
+  for (long long i = 0; i < nr; ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      int p = pos[ci[k]]++;
+      tci[p] = (int)i;
+      tv[p] = v[k];
+    }
+}
+
+static int upload_csr(sad_ctx* ctx, DevCsr& d, const std::vector<int>& rp,
+                      const std::vector<int>& ci, const std::vector<double>& v) {
+  CK(ctx, cudaMalloc(&d.rowptr, rp.size() * sizeof(int)));
+  CK(ctx, cudaMalloc(&d.colidx, std::max<size_t>(ci.size(), 1) * sizeof(int)));
+  CK(ctx, cudaMalloc(&d.vals, std::max<size_t>(v.size(), 1) * sizeof(double)));
+  CK(ctx, cudaMemcpy(d.rowptr, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (!ci.empty()) {
+    CK(ctx, cudaMemcpy(d.colidx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(ctx, cudaMemcpy(d.vals, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return SAD_OK;
+}
+
+static void free_csr(DevCsr& d) {
+  cudaFree(d.rowptr);
+  cudaFree(d.colidx);
+  cudaFree(d.vals);
+  d = DevCsr();
+}
+
+extern "C" int sad_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz,
+                              const int32_t* rowptr, const int32_t* colidx, const double* vals,
+                              int build_transpose, sad_csr** out) {
+  if (!ctx || !out) return SAD_EINVAL;
+  *out = nullptr;
+  if (nrows < 0 || ncols < 0 || nnz < 0 || nnz > 2147483647LL || !rowptr)
+    return set_err(ctx, SAD_EINVAL, "bad CSR sizes");
+  if (rowptr[0] != 0 || rowptr[nrows] != nnz)
+    return set_err(ctx, SAD_EINVAL, "row offsets inconsistent with nnz");
+  for (int64_t i = 0; i < nrows; ++i) {
+    if (rowptr[i + 1] < rowptr[i]) return set_err(ctx, SAD_EINVAL, "row offsets not monotone");
+    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      if (colidx[k] < 0 || colidx[k] >= ncols)
+        return set_err(ctx, SAD_EINVAL, "column index out of range in row %lld", (long long)i);
+      if (k > rowptr[i] && colidx[k] <= colidx[k - 1])
+        return set_err(ctx, SAD_EINVAL, "column indices not strictly increasing in row %lld",
+                       (long long)i);
+      if (!std::isfinite(vals[k])) return set_err(ctx, SAD_EINVAL, "non-finite matrix entry");
+    }
+  }
+  sad_csr* c = new sad_csr();
+  c->ctx = ctx;
+  c->nrows = nrows;
+  c->ncols = ncols;
+  c->nnz = nnz;
+  c->h_rowptr.assign(rowptr, rowptr + nrows + 1);
+  c->h_colidx.assign(colidx, colidx + nnz);
+  c->h_vals.assign(vals, vals + nnz);
+  int rc = upload_csr(ctx, c->d, c->h_rowptr, c->h_colidx, c->h_vals);
+  if (rc == SAD_OK && build_transpose) {
+    host_transpose(nrows, ncols, c->h_rowptr, c->h_colidx, c->h_vals, c->ht_rowptr,
+                   c->ht_colidx, c->ht_vals);
+    rc = upload_csr(ctx, c->dt, c->ht_rowptr, c->ht_colidx, c->ht_vals);
+    c->has_t = true;
+  }
+  if (rc != SAD_OK) {
+    free_csr(c->d);
+    free_csr(c->dt);
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return SAD_OK;
+}
+
+extern "C" int sad_csr_destroy(sad_csr* c) {
+  if (!c) return SAD_OK;
+  free_csr(c->d);
+  free_csr(c->dt);
+  delete c;
+  return SAD_OK;
+}
+
+extern "C" int64_t sad_csr_nnz(const sad_csr* c) { return c ? c->nnz : -1; }
+
+// -----------------------------------------------------------------------------
+// shifted operators
+// -----------------------------------------------------------------------------
+static int grid_for(long long work, int per_block, int cap) {
+  long long g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* mass,
+                             double sre, double sim, int adjoint, int precond_kind,
+                             sad_op** out) {
+  if (!ctx || !base || !out) return SAD_EINVAL;
+  *out = nullptr;
+  if (base->nrows != base->ncols) return set_err(ctx, SAD_EINVAL, "shifted operator must be square");
+  if (mass && (mass->nrows != base->nrows || mass->ncols != base->ncols))
+    return set_err(ctx, SAD_EINVAL, "base and mass dimensions disagree");
+  if (adjoint && (!base->has_t || (mass && !mass->has_t)))
+    return set_err(ctx, SAD_EINVAL, "adjoint operator needs matrices created with build_transpose");
+  if (precond_kind != SAD_PRECOND_NONE && precond_kind != SAD_PRECOND_JACOBI)
+    return set_err(ctx, SAD_EINVAL, "unknown preconditioner kind %d", precond_kind);
+  sad_op* op = new sad_op();
+  op->ctx = ctx;
+  op->uid = g_op_uid.fetch_add(1);
+  op->n = base->nrows;
+  op->precond = precond_kind;
+  const double2 sig = adjoint ? make_double2(sre, -sim) : make_double2(sre, sim);
+  op->sigma_eff = sig;
+  const DevCsr& bd = adjoint ? base->dt : base->d;
+  if (!mass) {
+    op->rowptr = bd.rowptr;
+    op->colidx = bd.colidx;
+    op->vals = bd.vals;
+    op->nnz = base->nnz;
+    op->vals_complex = false;
+    op->sigma_identity = true;
+    op->real_ok = (sig.y == 0.0);
+  } else {
+    // assemble base + sigma*mass on the merged pattern (sparse.py:138-155)
+    const std::vector<int>& brp = adjoint ? base->ht_rowptr : base->h_rowptr;
+    const std::vector<int>& bci = adjoint ? base->ht_colidx : base->h_colidx;
+    const std::vector<double>& bv = adjoint ? base->ht_vals : base->h_vals;
+    const std::vector<int>& mrp = adjoint ? mass->ht_rowptr : mass->h_rowptr;
+    const std::vector<int>& mci = adjoint ? mass->ht_colidx : mass->h_colidx;
+    const std::vector<double>& mv = adjoint ? mass->ht_vals : mass->h_vals;
+    const long long n = base->nrows;
+    std::vector<int> rp(n + 1, 0), ci;
+    std::vector<double> vr, vi;
+    ci.reserve(bci.size() + mci.size());
+    const bool cplx = (sig.y != 0.0);
+    vr.reserve(ci.capacity());
+    if (cplx) vi.reserve(ci.capacity());
+    for (long long i = 0; i < n; ++i) {
+      int p = brp[i], q = mrp[i];
+      const int pe = brp[i + 1], qe = mrp[i + 1];
+      while (p < pe || q < qe) {
+        int cb = p < pe ? bci[p] : INT32_MAX;
+        int cm = q < qe ? mci[q] : INT32_MAX;
+        int col = std::min(cb, cm);
+        double a = 0.0, mm = 0.0;
+        if (cb == col) a = bv[p++];
+        if (cm == col) mm = mv[q++];
+        ci.push_back(col);
+        vr.push_back(a + sig.x * mm);
+        if (cplx) vi.push_back(sig.y * mm);
+      }
+      rp[i + 1] = (int)ci.size();
+    }
+    size_t nz = ci.size();
+    CK(ctx, cudaMalloc(&op->own_rowptr, (n + 1) * sizeof(int)));
+    CK(ctx, cudaMalloc(&op->own_colidx, std::max<size_t>(nz, 1) * sizeof(int)));
+    CK(ctx, cudaMemcpy(op->own_rowptr, rp.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    if (nz) CK(ctx, cudaMemcpy(op->own_colidx, ci.data(), nz * sizeof(int), cudaMemcpyHostToDevice));
+    if (cplx) {
+      std::vector<double2> vc(nz);
+      for (size_t k = 0; k < nz; ++k) vc[k] = make_double2(vr[k], vi[k]);
+      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double2)));
+      if (nz) CK(ctx, cudaMemcpy(op->own_vals, vc.data(), nz * sizeof(double2), cudaMemcpyHostToDevice));
+    } else {
+      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double)));
+      if (nz) CK(ctx, cudaMemcpy(op->own_vals, vr.data(), nz * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    op->rowptr = op->own_rowptr;
+    op->colidx = op->own_colidx;
+    op->vals = op->own_vals;
+    op->nnz = (long long)nz;
+    op->vals_complex = cplx;
+    op->sigma_identity = false;
+    op->real_ok = !cplx;
+  }
+  // Jacobi dinv (precond.py:272-276): 1/diag(assembled op); identity when "none"
+  const long long n = op->n;
+  CK(ctx, cudaMalloc(&op->dinv_c, std::max<long long>(n, 1) * sizeof(double2)));
+  CK(ctx, cudaMalloc(&op->dinv_r, std::max<long long>(n, 1) * sizeof(double)));
+  int* d_bd = nullptr;
+  CK(ctx, cudaMalloc(&d_bd, sizeof(int)));
+  CK(ctx, cudaMemset(d_bd, 0, sizeof(int)));
+  const int blocks = grid_for(n, 256, ctx->nsm * 16);
+  if (precond_kind == SAD_PRECOND_JACOBI) {
+    if (op->vals_complex)
+      k_jacobi<double2><<<blocks, 256>>>(n, op->rowptr, op->colidx,
+                                         (const double2*)op->vals, sig, 0, op->dinv_c, d_bd);
+    else
+      k_jacobi<double><<<blocks, 256>>>(n, op->rowptr, op->colidx, (const double*)op->vals,
+                                        sig, op->sigma_identity ? 1 : 0, op->dinv_c, d_bd);
+  } else {
+    std::vector<double2> ones(n, make_double2(1.0, 0.0));
+    CK(ctx, cudaMemcpy(op->dinv_c, ones.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  k_c2r<<<blocks, 256>>>(n, op->dinv_c, op->dinv_r);
+  CKL(ctx);
+  int brk = 0;
+  CK(ctx, cudaMemcpy(&brk, d_bd, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(d_bd);
+  if (brk) {
+    sad_op_destroy(op);
+    return set_err(ctx, SAD_EBREAKDOWN, "zero diagonal entry for Jacobi");
+  }
+  *out = op;
+  return SAD_OK;
+}
+
+extern "C" int sad_op_destroy(sad_op* op) {
+  if (!op) return SAD_OK;
+  cudaFree(op->own_rowptr);
+  cudaFree(op->own_colidx);
+  cudaFree(op->own_vals);
+  cudaFree(op->dinv_c);
+  cudaFree(op->dinv_r);
+  delete op;
+  return SAD_OK;
+}
+
+extern "C" int sad_op_get_dinv(const sad_op* op, double* dinv_host) {
+  if (!op || !dinv_host) return SAD_EINVAL;
+  CK(op->ctx, cudaMemcpy(dinv_host, op->dinv_c, op->n * sizeof(double2), cudaMemcpyDeviceToHost));
+  return SAD_OK;
+}
+
+// -----------------------------------------------------------------------------
+// SpMM dispatch
+// -----------------------------------------------------------------------------
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
+static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
+  k_spmm<XT, VT, R, MODE, PRE, SIGMA><<<grid, kThreads, 0, s>>>(a);
+  COUNT_LAUNCH(1);
+}
+
+template <typename XT, typename VT, int R, int MODE>
+static void launch_spmm_ps(const SpmmArgs<XT>& a, bool pre, bool sigma, int grid, cudaStream_t s) {
+  if (pre) {
+    if (sigma) launch_spmm_t<XT, VT, R, MODE, true, true>(a, grid, s);
+    else launch_spmm_t<XT, VT, R, MODE, true, false>(a, grid, s);
+  } else {
+    if (sigma) launch_spmm_t<XT, VT, R, MODE, false, true>(a, grid, s);
+    else launch_spmm_t<XT, VT, R, MODE, false, false>(a, grid, s);
+  }
+}
+
+template <typename XT, int R, int MODE>
+static void launch_spmm_v(const SpmmArgs<XT>& a, bool vc, bool pre, bool sigma, int grid,
+                          cudaStream_t s);
+template <int R, int MODE>
+struct SpmmV {
+  static void run(const SpmmArgs<double>& a, bool, bool pre, bool sigma, int grid, cudaStream_t s) {
+    launch_spmm_ps<double, double, R, MODE>(a, pre, sigma, grid, s);
+  }
+  static void run(const SpmmArgs<double2>& a, bool vc, bool pre, bool sigma, int grid,
+                  cudaStream_t s) {
+    if (vc) launch_spmm_ps<double2, double2, R, MODE>(a, pre, false, grid, s);
+    else launch_spmm_ps<double2, double, R, MODE>(a, pre, sigma, grid, s);
+  }
+};
+
+template <typename XT, int MODE>
+static int launch_spmm(const SpmmArgs<XT>& a, int R, bool vc, bool pre, bool sigma, int nsm,
+                       cudaStream_t s, int grid_cap = 0) {
+  const int gpw = 32 / R;
+  const int cap = grid_cap > 0 ? grid_cap : nsm * 8;
+  const int grid = grid_for(a.n, kWarps * gpw, cap);
+  switch (R) {
+    case 1: SpmmV<1, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 2: SpmmV<2, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 3: SpmmV<3, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 4: SpmmV<4, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 5: SpmmV<5, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 6: SpmmV<6, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 7: SpmmV<7, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    case 8: SpmmV<8, MODE>::run(a, vc, pre, sigma, grid, s); break;
+    default: return SAD_EINVAL;
+  }
+  return SAD_OK;
+}
+
+static int check_block(sad_ctx* ctx, int r, int dtype) {
+  if (r < 1 || r > 8) return set_err(ctx, SAD_EINVAL, "block width r=%d outside 1..8", r);
+  if (dtype != SAD_F64 && dtype != SAD_C128) return set_err(ctx, SAD_EINVAL, "bad dtype %d", dtype);
+  return SAD_OK;
+}
+
+template <int MODE>
+static int op_spmm(sad_op* op, int r, int dtype, const void* b, const void* x, void* y, void* stream) {
+  sad_ctx* ctx = op->ctx;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  if (dtype == SAD_F64) {
+    if (!op->real_ok) return set_err(ctx, SAD_EINVAL, "complex shift needs a complex128 block");
+    SpmmArgs<double> a{};
+    a.n = op->n; a.rowptr = op->rowptr; a.colidx = op->colidx; a.vals = op->vals;
+    a.x = (const double*)x; a.y = (double*)y; a.b = (const double*)b;
+    a.dinv = op->dinv_r; a.sigma = op->sigma_eff;
+    rc = launch_spmm<double, MODE>(a, r, false, false, op->sigma_identity, ctx->nsm, S_(stream));
+  } else {
+    SpmmArgs<double2> a{};
+    a.n = op->n; a.rowptr = op->rowptr; a.colidx = op->colidx; a.vals = op->vals;
+    a.x = (const double2*)x; a.y = (double2*)y; a.b = (const double2*)b;
+    a.dinv = op->dinv_c; a.sigma = op->sigma_eff;
+    rc = launch_spmm<double2, MODE>(a, r, op->vals_complex, false, op->sigma_identity, ctx->nsm,
+                                    S_(stream));
+  }
+  if (rc) return rc;
+  CKL(ctx);
+  return SAD_OK;
+}
+
+extern "C" int sad_op_apply(sad_op* op, int r, int dtype, const void* x, void* y, void* stream) {
+  if (!op || !x || !y) return SAD_EINVAL;
+  return op_spmm<SPMM_APPLY>(op, r, dtype, nullptr, x, y, stream);
+}
+
+extern "C" int sad_op_residual(sad_op* op, int r, int dtype, const void* b, const void* x, void* y,
+                               void* stream) {
+  if (!op || !b || !x || !y) return SAD_EINVAL;
+  return op_spmm<SPMM_RESID>(op, r, dtype, b, x, y, stream);
+}
+
+extern "C" int sad_csr_apply(sad_csr* csr, int transpose, int r, int dtype, const void* x, void* y,
+                             void* stream) {
+  if (!csr || !x || !y) return SAD_EINVAL;
+  sad_ctx* ctx = csr->ctx;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  if (transpose && !csr->has_t) return set_err(ctx, SAD_EINVAL, "transpose was not built");
+  const DevCsr& d = transpose ? csr->dt : csr->d;
+  const long long rows = transpose ? csr->ncols : csr->nrows;
+  if (dtype == SAD_F64) {
+    SpmmArgs<double> a{};
+    a.n = rows; a.rowptr = d.rowptr; a.colidx = d.colidx; a.vals = d.vals;
+    a.x = (const double*)x; a.y = (double*)y;
+    rc = launch_spmm<double, SPMM_APPLY>(a, r, false, false, false, ctx->nsm, S_(stream));
+  } else {
+    SpmmArgs<double2> a{};
+    a.n = rows; a.rowptr = d.rowptr; a.colidx = d.colidx; a.vals = d.vals;
+    a.x = (const double2*)x; a.y = (double2*)y;
+    rc = launch_spmm<double2, SPMM_APPLY>(a, r, false, false, false, ctx->nsm, S_(stream));
+  }
+  if (rc) return rc;
+  CKL(ctx);
+  return SAD_OK;
+}
+
+// -----------------------------------------------------------------------------
+// GMRES workspace
+// -----------------------------------------------------------------------------
+template <typename T>
+static T* carve(char*& p, size_t count) {
+  size_t off = (reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15);
+  T* r = reinterpret_cast<T*>(off);
+  p = reinterpret_cast<char*>(off + count * sizeof(T));
+  return r;
+}
+
+static size_t dot_smem(int J, int R, size_t esz) { return (size_t)J * kWarps * R * esz + kWarps * R * 8; }
+static size_t upd_smem(int J, int R, size_t esz) { return (size_t)J * R * esz; }
+
+template <typename XT, int R>
+static int set_smem_attrs(size_t dsm, size_t usm) {
+  cudaError_t e = cudaSuccess;
+  e = cudaFuncSetAttribute(k_dot<XT, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_dot<XT, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_update<XT, R, UPD_ORTH1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_update<XT, R, UPD_ORTH2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_update<XT, R, UPD_X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_update<XT, R, UPD_XF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+  return e == cudaSuccess ? 0 : 1;
+}
+
+template <typename XT>
+static int set_smem_all(int R, size_t dsm, size_t usm) {
+  switch (R) {
+    case 1: return set_smem_attrs<XT, 1>(dsm, usm);
+    case 2: return set_smem_attrs<XT, 2>(dsm, usm);
+    case 3: return set_smem_attrs<XT, 3>(dsm, usm);
+    case 4: return set_smem_attrs<XT, 4>(dsm, usm);
+    case 5: return set_smem_attrs<XT, 5>(dsm, usm);
+    case 6: return set_smem_attrs<XT, 6>(dsm, usm);
+    case 7: return set_smem_attrs<XT, 7>(dsm, usm);
+    case 8: return set_smem_attrs<XT, 8>(dsm, usm);
+  }
+  return 1;
+}
+
+extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int restart, int flexible,
+                                sad_gmres** out) {
+  if (!ctx || !out) return SAD_EINVAL;
+  *out = nullptr;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  if (n < 1) return set_err(ctx, SAD_EINVAL, "n must be >= 1");
+  if (restart < 1 || restart > 400) return set_err(ctx, SAD_EINVAL, "restart %d outside 1..400", restart);
+  sad_gmres* ws = new sad_gmres();
+  ws->ctx = ctx;
+  ws->n = n;
+  ws->R = r;
+  ws->dtype = dtype;
+  ws->m = restart;
+  ws->flexible = flexible ? 1 : 0;
+  ws->esz = dtype == SAD_F64 ? 8 : 16;
+  const int m = restart;
+  const size_t blk = (size_t)n * r * ws->esz;
+  size_t dsm = dot_smem(m + 1, r, ws->esz), usm = upd_smem(m + 1, r, ws->esz);
+  if (dsm > 220 * 1024) {
+    delete ws;
+    return set_err(ctx, SAD_EINVAL, "restart %d too long for the shared-memory dot at r=%d", m, r);
+  }
+  int bad = dtype == SAD_F64 ? set_smem_all<double>(r, dsm, usm) : set_smem_all<double2>(r, dsm, usm);
+  if (bad) {
+    delete ws;
+    return set_err(ctx, SAD_ECUDA, "cudaFuncSetAttribute failed");
+  }
+  ws->dot_blocks_per_sm = std::max(1, std::min(8, (int)((200 * 1024) / dsm)));
+  if (cudaMalloc(&ws->V, blk * (m + 1)) != cudaSuccess) {
+    delete ws;
+    return set_err(ctx, SAD_ENOMEM, "basis allocation of %zu bytes failed", blk * (m + 1));
+  }
+  if (ws->flexible && cudaMalloc(&ws->Z, blk * m) != cudaSuccess) {
+    cudaFree(ws->V);
+    delete ws;
+    return set_err(ctx, SAD_ENOMEM, "FGMRES Z allocation failed");
+  }
+  ws->max_blocks = ctx->nsm * 8;
+  ws->pstride = 2 * (m + 1) * r + r + 8;
+  size_t sb = 0;
+  sb += 16 * 8;                              // j, any_active, jx, ticket, seqs
+  sb += 4 * r * sizeof(int) + r * 8 + 64;    // active, done, kdim, iters
+  sb += (size_t)(m + 1) * r * 8;             // S
+  sb += 2 * (size_t)(m + 1) * r * 16;        // h, h2
+  sb += (size_t)r * m * (m + 1) * 16;        // H
+  sb += (size_t)r * m * 8 + (size_t)r * m * 16;  // cs, sn
+  sb += (size_t)r * (m + 1) * 16;            // g
+  sb += (size_t)m * r * 16;                  // ycoef
+  sb += 2 * r * 8;                           // wpre2, beta
+  sb += 64 * 16;                             // alignment slack
+  ws->state_bytes = sb;
+  if (cudaMalloc(&ws->state, sb) != cudaSuccess ||
+      cudaMalloc(&ws->part, (size_t)ws->max_blocks * ws->pstride * sizeof(double)) != cudaSuccess ||
+      cudaHostAlloc(&ws->hflag_host, 8 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&ws->hflag_dev, ws->hflag_host, 0) != cudaSuccess) {
+    sad_gmres_destroy(ws);
+    return set_err(ctx, SAD_ENOMEM, "workspace allocation failed");
+  }
+  cudaMemset(ws->state, 0, sb);
+  char* p = ws->state;
+  GState& st = ws->st;
+  st.j = carve<int>(p, 1);
+  st.any_active = carve<int>(p, 1);
+  st.jx = carve<int>(p, 1);
+  st.ticket = carve<unsigned>(p, 1);
+  st.stepseq = carve<unsigned long long>(p, 1);
+  st.cycleseq = carve<unsigned long long>(p, 1);
+  st.active = carve<int>(p, r);
+  st.done = carve<int>(p, r);
+  st.kdim = carve<int>(p, r);
+  st.iters = carve<long long>(p, r);
+  st.S = carve<double>(p, (size_t)(m + 1) * r);
+  st.h = carve<double2>(p, (size_t)(m + 1) * r);
+  st.h2 = carve<double2>(p, (size_t)(m + 1) * r);
+  st.H = carve<double2>(p, (size_t)r * m * (m + 1));
+  st.cs = carve<double>(p, (size_t)r * m);
+  st.sn = carve<double2>(p, (size_t)r * m);
+  st.g = carve<double2>(p, (size_t)r * (m + 1));
+  st.ycoef = carve<double2>(p, (size_t)m * r);
+  st.wpre2 = carve<double>(p, r);
+  st.beta = carve<double>(p, r);
+  if ((size_t)(p - ws->state) > sb) {
+    sad_gmres_destroy(ws);
+    return set_err(ctx, SAD_EINVAL, "internal: state carve overflow");
+  }
+  st.part = ws->part;
+  st.hflag = ws->hflag_dev;
+  st.m = m;
+  st.R = r;
+  st.pstride = ws->pstride;
+  ws->bytes = (int64_t)(blk * (m + 1) + (ws->flexible ? blk * m : 0) + sb +
+                        (size_t)ws->max_blocks * ws->pstride * 8);
+  *out = ws;
+  return SAD_OK;
+}
+
+extern "C" int sad_gmres_destroy(sad_gmres* ws) {
+  if (!ws) return SAD_OK;
+  for (int i = 0; i < 3; ++i)
+    if (ws->ev[i]) cudaEventDestroy(ws->ev[i]);
+  cudaFree(ws->V);
+  cudaFree(ws->Z);
+  cudaFree(ws->state);
+  cudaFree(ws->part);
+  if (ws->hflag_host) cudaFreeHost(ws->hflag_host);
+  delete ws;
+  return SAD_OK;
+}
+
+extern "C" int64_t sad_gmres_bytes(const sad_gmres* ws) { return ws ? ws->bytes : -1; }
+
+// ---- per-step launches ------------------------------------------------------
+template <typename XT, int R>
+struct Orth {
+  static void dot(const OrthArgs& a, bool pass1, int grid, size_t smem, cudaStream_t s) {
+    COUNT_LAUNCH(1);
+    if (pass1) k_dot<XT, R, true><<<grid, kThreads, smem, s>>>(a);
+    else k_dot<XT, R, false><<<grid, kThreads, smem, s>>>(a);
+  }
+  static void upd(const OrthArgs& a, int mode, int grid, size_t smem, cudaStream_t s) {
+    COUNT_LAUNCH(1);
+    switch (mode) {
+      case UPD_ORTH1: k_update<XT, R, UPD_ORTH1><<<grid, kThreads, smem, s>>>(a); break;
+      case UPD_ORTH2: k_update<XT, R, UPD_ORTH2><<<grid, kThreads, smem, s>>>(a); break;
+      case UPD_X: k_update<XT, R, UPD_X><<<grid, kThreads, smem, s>>>(a); break;
+      case UPD_XF: k_update<XT, R, UPD_XF><<<grid, kThreads, smem, s>>>(a); break;
+    }
+  }
+};
+
+template <typename XT>
+static void orth_dot(int R, const OrthArgs& a, bool pass1, int grid, size_t smem, cudaStream_t s) {
+  switch (R) {
+    case 1: Orth<XT, 1>::dot(a, pass1, grid, smem, s); break;
+    case 2: Orth<XT, 2>::dot(a, pass1, grid, smem, s); break;
+    case 3: Orth<XT, 3>::dot(a, pass1, grid, smem, s); break;
+    case 4: Orth<XT, 4>::dot(a, pass1, grid, smem, s); break;
+    case 5: Orth<XT, 5>::dot(a, pass1, grid, smem, s); break;
+    case 6: Orth<XT, 6>::dot(a, pass1, grid, smem, s); break;
+    case 7: Orth<XT, 7>::dot(a, pass1, grid, smem, s); break;
+    case 8: Orth<XT, 8>::dot(a, pass1, grid, smem, s); break;
+  }
+}
+
+template <typename XT>
+static void orth_upd(int R, const OrthArgs& a, int mode, int grid, size_t smem, cudaStream_t s) {
+  switch (R) {
+    case 1: Orth<XT, 1>::upd(a, mode, grid, smem, s); break;
+    case 2: Orth<XT, 2>::upd(a, mode, grid, smem, s); break;
+    case 3: Orth<XT, 3>::upd(a, mode, grid, smem, s); break;
+    case 4: Orth<XT, 4>::upd(a, mode, grid, smem, s); break;
+    case 5: Orth<XT, 5>::upd(a, mode, grid, smem, s); break;
+    case 6: Orth<XT, 6>::upd(a, mode, grid, smem, s); break;
+    case 7: Orth<XT, 7>::upd(a, mode, grid, smem, s); break;
+    case 8: Orth<XT, 8>::upd(a, mode, grid, smem, s); break;
+  }
+}
+
+struct Launcher {
+  sad_gmres* ws;
+  sad_op* op;
+  cudaStream_t s;
+  const void* rhs;
+  void* x;
+  int grid_spmm, grid_dot, grid_upd;
+  size_t dsm, usm;
+
+  template <typename XT>
+  SpmmArgs<XT> spmm_args(int mode) const {
+    SpmmArgs<XT> a{};
+    a.n = ws->n;
+    a.rowptr = op->rowptr;
+    a.colidx = op->colidx;
+    a.vals = op->vals;
+    a.sigma = op->sigma_eff;
+    a.stride = ws->n * ws->R;
+    a.st = ws->st;
+    a.dinv = reinterpret_cast<const XT*>(sizeof(XT) == 8 ? (const void*)op->dinv_r
+                                                         : (const void*)op->dinv_c);
+    if (mode == SPMM_ARNOLDI) {
+      a.x = reinterpret_cast<const XT*>(ws->V);
+      a.zout = reinterpret_cast<XT*>(ws->Z);
+    } else {  // residual into V_0
+      a.x = reinterpret_cast<const XT*>(x);
+      a.b = reinterpret_cast<const XT*>(rhs);
+      a.y = reinterpret_cast<XT*>(ws->V);
+    }
+    return a;
+  }
+
+  OrthArgs orth_args() const {
+    OrthArgs a{};
+    a.n = ws->n;
+    a.V = ws->V;
+    a.Z = ws->Z;
+    a.x = x;
+    a.dinv = ws->dtype == SAD_F64 ? (const void*)op->dinv_r : (const void*)op->dinv_c;
+    a.stride = ws->n * ws->R;
+    a.st = ws->st;
+    return a;
+  }
+
+  template <typename XT>
+  void arnoldi_t(int which) const {
+    const bool pre = op->precond == SAD_PRECOND_JACOBI;
+    const int R = ws->R;
+    const OrthArgs oa = orth_args();
+    switch (which) {
+      case 0: {
+        auto a = spmm_args<XT>(SPMM_ARNOLDI);
+        launch_spmm<XT, SPMM_ARNOLDI>(a, R, op->vals_complex, pre, op->sigma_identity,
+                                      ws->ctx->nsm, s, grid_spmm);
+        break;
+      }
+      case 1: orth_dot<XT>(R, oa, true, grid_dot, dsm, s); break;
+      case 2: orth_upd<XT>(R, oa, UPD_ORTH1, grid_upd, usm, s); break;
+      case 3: orth_dot<XT>(R, oa, false, grid_dot, dsm, s); break;
+      case 4: orth_upd<XT>(R, oa, UPD_ORTH2, grid_upd, usm, s); break;
+    }
+  }
+  void arnoldi(int which) const {
+    if (ws->dtype == SAD_F64) arnoldi_t<double>(which);
+    else arnoldi_t<double2>(which);
+  }
+
+  template <typename XT>
+  void cycle_end_t() const {
+    k_trisolve<<<1, 32, 0, s>>>(ws->st, ws->flexible);
+    COUNT_LAUNCH(1);
+    const OrthArgs oa = orth_args();
+    orth_upd<XT>(ws->R, oa, ws->flexible ? UPD_XF : UPD_X, grid_upd, usm, s);
+    residual_t<XT>();
+  }
+  template <typename XT>
+  void residual_t() const {
+    auto a = spmm_args<XT>(SPMM_RESID_CYCLE);
+    launch_spmm<XT, SPMM_RESID_CYCLE>(a, ws->R, op->vals_complex, false, op->sigma_identity,
+                                      ws->ctx->nsm, s, grid_spmm);
+  }
+  void cycle_end() const {
+    if (ws->dtype == SAD_F64) cycle_end_t<double>();
+    else cycle_end_t<double2>();
+  }
+  void residual() const {
+    if (ws->dtype == SAD_F64) residual_t<double>();
+    else residual_t<double2>();
+  }
+};
+
+static int prepare(sad_gmres* ws, sad_op* op, const void* rhs, void* x, cudaStream_t s,
+                   Launcher& L) {
+  sad_ctx* ctx = ws->ctx;
+  if (!op || !rhs || !x) return set_err(ctx, SAD_EINVAL, "null argument");
+  if (op->n != ws->n) return set_err(ctx, SAD_EINVAL, "operator size %lld != workspace size %lld",
+                                     op->n, ws->n);
+  if (ws->dtype == SAD_F64 && !op->real_ok)
+    return set_err(ctx, SAD_EINVAL, "complex shift needs a complex128 workspace");
+  L.ws = ws;
+  L.op = op;
+  L.s = s;
+  L.rhs = rhs;
+  L.x = x;
+  const int R = ws->R;
+  const int gpw = 32 / R;
+  const int U = (R <= 2) ? 8 : 4;
+  const long long tiles = (ws->n + (long long)gpw * U - 1) / ((long long)gpw * U);
+  L.grid_spmm = grid_for(ws->n, kWarps * gpw, ws->max_blocks);
+  L.grid_dot = grid_for(tiles, kWarps, std::min(ws->max_blocks, ctx->nsm * ws->dot_blocks_per_sm));
+  L.grid_upd = grid_for(tiles, kWarps, std::min(ws->max_blocks, ctx->nsm * 8));
+  L.dsm = dot_smem(ws->m + 1, R, ws->esz);
+  L.usm = upd_smem(ws->m + 1, R, ws->esz);
+  return SAD_OK;
+}
+
+static int read_results(sad_gmres* ws, void* res, cudaStream_t s, int64_t* iters, double* resn,
+                        uint8_t* conv, double tol) {
+  sad_ctx* ctx = ws->ctx;
+  const int R = ws->R;
+  if (res) CK(ctx, cudaMemcpyAsync(res, ws->V, (size_t)ws->n * R * ws->esz, cudaMemcpyDeviceToDevice, s));
+  std::vector<long long> it(R);
+  std::vector<double> be(R);
+  CK(ctx, cudaMemcpyAsync(it.data(), ws->st.iters, R * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(ctx, cudaMemcpyAsync(be.data(), ws->st.beta, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(ctx, cudaStreamSynchronize(s));
+  for (int c = 0; c < R; ++c) {
+    if (iters) iters[c] = it[c];
+    if (resn) resn[c] = be[c];
+    if (conv) conv[c] = be[c] <= tol ? 1 : 0;
+  }
+  return SAD_OK;
+}
+
+// Spin until `pred()` holds, reading host-mapped flags written by the device.
+// Falls back to a stream query so a faulted/finished stream cannot hang us.
+template <typename P>
+static int spin_until(sad_ctx* ctx, cudaStream_t s, P pred) {
+  unsigned long it = 0;
+  while (!pred()) {
+    if ((++it & 1023) == 0) {
+      cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) {
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        if (pred()) break;
+        return set_err(ctx, SAD_ECUDA, "device progress flag not observed after stream drained");
+      }
+      if (q != cudaErrorNotReady)
+        return set_err(ctx, SAD_ECUDA, "stream failed: %s", cudaGetErrorString(q));
+      if ((it & ((1u << 16) - 1)) == 0) std::this_thread::yield();
+    }
+  }
+  return SAD_OK;
+}
+
+// Algorithmic bytes of one shifted SpMM application:
+// nnz*(4 + value bytes) + 4(n+1) + read x + write y (+ dinv gather when PRE, + Z write).
+static double spmm_bytes(const sad_gmres* ws, const sad_op* op, bool arnoldi) {
+  const double n = (double)ws->n, blk = n * ws->R * ws->esz;
+  const long long nnz = op->nnz;
+  double b = (double)nnz * (4.0 + (op->vals_complex ? 16.0 : 8.0)) + 4.0 * (n + 1) + 2.0 * blk;
+  if (arnoldi && op->precond == SAD_PRECOND_JACOBI) b += n * ws->esz;
+  if (arnoldi && ws->flexible) b += blk;
+  return b;
+}
+
+extern "C" int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host) {
+  if (!ws) return SAD_EINVAL;
+  sad_ctx* ctx = ws->ctx;
+  if (stats_host)
+    for (int i = 0; i < 8; ++i) stats_host[i] = ws->prof[i];
+  if (enable) {
+    for (int i = 0; i < 8; ++i) ws->prof[i] = 0.0;
+    for (int i = 0; i < 3; ++i)
+      if (!ws->ev[i]) CK(ctx, cudaEventCreate(&ws->ev[i]));
+  }
+  ws->profile = enable ? 1 : 0;
+  return SAD_OK;
+}
+
+extern "C" int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs, void* x, void* res,
+                               double tol_col, int maxit, void* stream, int64_t* iters_host,
+                               double* resnorm_host, uint8_t* conv_host) {
+  if (!ws) return SAD_EINVAL;
+  sad_ctx* ctx = ws->ctx;
+  if (!(tol_col > 0.0)) return set_err(ctx, SAD_EINVAL, "abs_tolerance must be positive");
+  if (maxit < 0) return set_err(ctx, SAD_EINVAL, "maxit must be >= 0");
+  cudaStream_t s = S_(stream);
+  Launcher L;
+  int rc = prepare(ws, op, rhs, x, s, L);
+  if (rc) return rc;
+  ws->st.tol = tol_col;
+  ws->st.maxit = maxit;
+  ws->st.fixed = 0;
+  volatile long long* hf = ws->hflag_host;
+  for (int i = 0; i < 8; ++i) hf[i] = -1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  k_init<<<1, 32, 0, s>>>(ws->st);
+  COUNT_LAUNCH(1);
+  CK(ctx, cudaMemsetAsync(x, 0, (size_t)ws->n * ws->R * ws->esz, s));
+  L.residual();
+  CKL(ctx);
+  long long cycles = 1;
+  rc = spin_until(ctx, s, [&] { return hf[2] >= cycles; });
+  if (rc) return rc;
+  int any = (int)hf[3];
+  const int LAG = 3;
+  const double N = (double)ws->n * ws->R * ws->esz;   // bytes of one n x r block
+  while (any) {
+    const long long base = hf[0] < 0 ? 0 : hf[0];
+    for (int step = 0; step < ws->m; ++step) {
+      if (ws->profile) {
+        // synchronous stepping: exact per-kernel-class device times
+        if (step > 0 && hf[1] == 0) break;
+        CK(ctx, cudaEventRecord(ws->ev[0], s));
+        L.arnoldi(0);
+        CK(ctx, cudaEventRecord(ws->ev[1], s));
+        for (int k = 1; k < 5; ++k) L.arnoldi(k);
+        CK(ctx, cudaEventRecord(ws->ev[2], s));
+        CK(ctx, cudaEventSynchronize(ws->ev[2]));
+        float t1 = 0.f, t2 = 0.f;
+        cudaEventElapsedTime(&t1, ws->ev[0], ws->ev[1]);
+        cudaEventElapsedTime(&t2, ws->ev[1], ws->ev[2]);
+        const double J = step + 1;
+        ws->prof[0] += t1;
+        ws->prof[1] += 1;
+        ws->prof[2] += spmm_bytes(ws, op, true);
+        ws->prof[3] += t2;
+        ws->prof[4] += 1;
+        ws->prof[5] += (4.0 * J + 6.0) * N;
+        continue;
+      }
+      bool stop = false;
+      rc = spin_until(ctx, s, [&] {
+        long long done = hf[0] - base;
+        long long act = hf[1];
+        if (done >= 1 && act == 0) { stop = true; return true; }
+        return step - done <= LAG;
+      });
+      if (rc) return rc;
+      if (stop) break;
+      for (int k = 0; k < 5; ++k) L.arnoldi(k);
+    }
+    if (ws->profile) CK(ctx, cudaEventRecord(ws->ev[0], s));
+    L.cycle_end();
+    CKL(ctx);
+    ++cycles;
+    rc = spin_until(ctx, s, [&] { return hf[2] >= cycles; });
+    if (rc) return rc;
+    if (ws->profile) {
+      CK(ctx, cudaEventRecord(ws->ev[1], s));
+      CK(ctx, cudaEventSynchronize(ws->ev[1]));
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ws->ev[0], ws->ev[1]);
+      ws->prof[6] += t;
+      ws->prof[7] += 1;
+    }
+    any = (int)hf[3];
+  }
+  return read_results(ws, res, s, iters_host, resnorm_host, conv_host, tol_col);
+}
+
+extern "C" int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs, void* x, void* res,
+                               int steps, void* stream, double* resnorm_host, double* timing_ms) {
+  if (!ws) return SAD_EINVAL;
+  sad_ctx* ctx = ws->ctx;
+  if (steps < 1 || steps > ws->m)
+    return set_err(ctx, SAD_EINVAL, "steps %d outside 1..restart(%d)", steps, ws->m);
+  cudaStream_t s = S_(stream);
+  Launcher L;
+  int rc = prepare(ws, op, rhs, x, s, L);
+  if (rc) return rc;
+  ws->st.tol = 0.0;
+  ws->st.maxit = steps;
+  ws->st.fixed = 1;
+  k_init<<<1, 32, 0, s>>>(ws->st);
+  COUNT_LAUNCH(1);
+  CK(ctx, cudaMemsetAsync(x, 0, (size_t)ws->n * ws->R * ws->esz, s));
+  const bool timed = timing_ms != nullptr;
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    if (!timed) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+  };
+  mark();
+  L.residual();
+  mark();
+  for (int step = 0; step < steps; ++step) {
+    L.arnoldi(0);
+    mark();
+    for (int k = 1; k < 5; ++k) L.arnoldi(k);
+    mark();
+  }
+  L.cycle_end();
+  mark();
+  CKL(ctx);
+  CK(ctx, cudaStreamSynchronize(s));
+  if (timed) {
+    for (int i = 0; i < 4; ++i) timing_ms[i] = 0.0;
+    auto el = [&](int a, int b) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[a], ev[b]);
+      return (double)t;
+    };
+    timing_ms[3] += el(0, 1);
+    for (int step = 0; step < steps; ++step) {
+      timing_ms[0] += el(1 + 2 * step, 2 + 2 * step);
+      timing_ms[1] += el(2 + 2 * step, 3 + 2 * step);
+    }
+    timing_ms[2] += el(1 + 2 * steps, 2 + 2 * steps);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  return read_results(ws, res, s, nullptr, resnorm_host, nullptr, 0.0);
+}
+
+// -----------------------------------------------------------------------------
+// block utilities
+// -----------------------------------------------------------------------------
+template <typename XT>
+static void gram_launch(int R, long long n, const void* x, const void* y, double* part,
+                        unsigned* ticket, double2* out, int grid, cudaStream_t s) {
+  const XT* X = (const XT*)x;
+  const XT* Y = (const XT*)y;
+  switch (R) {
+    case 1: k_gram<XT, 1><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    default: break;
+    case 2: k_gram<XT, 2><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    case 3: k_gram<XT, 3><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    case 4: k_gram<XT, 4><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    case 5: k_gram<XT, 5><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    case 6: k_gram<XT, 6><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    case 7: k_gram<XT, 7><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+    case 8: k_gram<XT, 8><<<grid, kThreads, 0, s>>>(n, X, Y, part, ticket, out); break;
+  }
+}
+
+extern "C" int sad_gram(sad_ctx* ctx, int64_t n, int r, int dtype, const void* x, const void* y,
+                        double* gram_host, void* stream) {
+  if (!ctx || !x || !y || !gram_host) return SAD_EINVAL;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  cudaStream_t s = S_(stream);
+  const int grid = grid_for(n, kThreads, ctx->scratch_blocks);
+  COUNT_LAUNCH(1);
+  if (dtype == SAD_F64)
+    gram_launch<double>(r, n, x, y, ctx->scratch, ctx->ticket, ctx->gram_out, grid, s);
+  else
+    gram_launch<double2>(r, n, x, y, ctx->scratch, ctx->ticket, ctx->gram_out, grid, s);
+  CKL(ctx);
+  CK(ctx, cudaMemcpyAsync(ctx->gram_host, ctx->gram_out, r * r * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  CK(ctx, cudaStreamSynchronize(s));
+  std::memcpy(gram_host, ctx->gram_host, r * r * sizeof(double2));
+  return SAD_OK;
+}
+
+extern "C" int sad_axpy(sad_ctx* ctx, int64_t n, int r, int dtype, double are, double aim,
+                        const void* x, void* y, void* stream) {
+  if (!ctx || !x || !y) return SAD_EINVAL;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  if (dtype == SAD_F64 && aim != 0.0) return set_err(ctx, SAD_EINVAL, "complex coefficient on a real block");
+  const long long count = n * r;
+  const int grid = grid_for(count, 256, ctx->nsm * 16);
+  COUNT_LAUNCH(1);
+  if (dtype == SAD_F64)
+    k_axpy<double><<<grid, 256, 0, S_(stream)>>>(count, make_double2(are, aim), (const double*)x, (double*)y);
+  else
+    k_axpy<double2><<<grid, 256, 0, S_(stream)>>>(count, make_double2(are, aim), (const double2*)x,
+                                                  (double2*)y);
+  CKL(ctx);
+  return SAD_OK;
+}

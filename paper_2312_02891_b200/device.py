@@ -1,0 +1,251 @@
+"""Device objects: CSR matrices, shifted operators, Krylov workspaces, blocks.
+
+Thin RAII wrappers over the C-ABI handles.  Device memory for vector blocks
+is torch tensors (plumbing only); the arithmetic runs in libsylvadi_b200.so.
+"""
+
+import ctypes
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+
+_KIND = {"none": _lib.SAD_PRECOND_NONE, "jacobi": _lib.SAD_PRECOND_JACOBI}
+
+
+def as_csr(mat):
+    """scipy CSR (canonical) from a scipy matrix, a reference SparseMatrix
+    (anything with ``.scipy()``) or a dense array."""
+    if hasattr(mat, "scipy"):
+        mat = mat.scipy()
+    if sp.issparse(mat):
+        csr = sp.csr_matrix(mat)
+    else:
+        arr = np.asarray(mat)
+        if arr.ndim != 2:
+            raise ValueError("expected a 2-d matrix")
+        csr = sp.csr_matrix(arr)
+    if not (csr.has_sorted_indices and csr.has_canonical_format):
+        csr = csr.copy()
+        csr.sum_duplicates()
+        csr.sort_indices()
+    if np.iscomplexobj(csr.data):
+        raise ValueError("coefficient matrices must be real (sparse.py:33-35)")
+    return csr
+
+
+def torch_dtype(dtype):
+    import torch
+    return torch.float64 if dtype == _lib.SAD_F64 else torch.complex128
+
+
+def current_stream_handle(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class DeviceMatrix:
+    """Real CSR matrix resident on the device (optionally with its transpose)."""
+
+    def __init__(self, mat, transpose=False, device=0):
+        csr = as_csr(mat)
+        self.shape = csr.shape
+        self.nnz = int(csr.nnz)
+        self.device = device
+        self.has_transpose = bool(transpose)
+        self._ctx = _lib.context(device)
+        lib = _lib.load()
+        rp = np.ascontiguousarray(csr.indptr, dtype=np.int32)
+        ci = np.ascontiguousarray(csr.indices, dtype=np.int32)
+        va = np.ascontiguousarray(csr.data, dtype=np.float64)
+        h = ctypes.c_void_p()
+        rc = lib.sad_csr_create(self._ctx, csr.shape[0], csr.shape[1], self.nnz,
+                                rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+                                1 if transpose else 0, ctypes.byref(h))
+        _lib.check(rc, self._ctx)
+        self.handle = h
+        self.diagonal = csr.diagonal()
+
+    @property
+    def nrows(self):
+        return self.shape[0]
+
+    def apply(self, x, y=None, transpose=False, stream=None):
+        """y = A x (or A^T x) for an (n, r) torch block."""
+        import torch
+        dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
+        rows = self.shape[1] if transpose else self.shape[0]
+        if y is None:
+            y = torch.empty((rows, x.shape[1]), dtype=x.dtype, device=x.device)
+        rc = _lib.load().sad_csr_apply(self.handle, 1 if transpose else 0, x.shape[1], dtype,
+                                       x.data_ptr(), y.data_ptr(),
+                                       current_stream_handle(stream))
+        _lib.check(rc, self._ctx)
+        return y
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.load().sad_csr_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class DeviceOperator:
+    """``base + shift*mass`` (or its conjugate transpose) with device Jacobi
+    (ShiftedOperator, sparse.py:158-206 + precond.py:272-276)."""
+
+    def __init__(self, base, mass, shift, adjoint=False, precond_kind="jacobi"):
+        if precond_kind not in _KIND:
+            raise ValueError(f"preconditioner {precond_kind!r} is not available on the "
+                             "GPU path (supported: none, jacobi)")
+        self.base, self.mass = base, mass
+        self.shift = complex(shift)
+        self.adjoint = bool(adjoint)
+        self.n = base.shape[0]
+        self._ctx = base._ctx
+        h = ctypes.c_void_p()
+        rc = _lib.load().sad_op_create(self._ctx, base.handle,
+                                       None if mass is None else mass.handle,
+                                       self.shift.real, self.shift.imag,
+                                       1 if adjoint else 0, _KIND[precond_kind],
+                                       ctypes.byref(h))
+        _lib.check(rc, self._ctx)
+        self.handle = h
+        self.is_real = (self.shift.imag == 0.0)
+
+    def dinv(self):
+        out = np.empty(self.n, dtype=np.complex128)
+        _lib.check(_lib.load().sad_op_get_dinv(self.handle, out.ctypes.data), self._ctx)
+        return out
+
+    def apply(self, x, y=None, stream=None):
+        import torch
+        dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
+        if y is None:
+            y = torch.empty_like(x)
+        rc = _lib.load().sad_op_apply(self.handle, x.shape[1], dtype, x.data_ptr(),
+                                      y.data_ptr(), current_stream_handle(stream))
+        _lib.check(rc, self._ctx)
+        return y
+
+    def residual(self, b, x, y=None, stream=None):
+        import torch
+        dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
+        if y is None:
+            y = torch.empty_like(x)
+        rc = _lib.load().sad_op_residual(self.handle, x.shape[1], dtype, b.data_ptr(),
+                                         x.data_ptr(), y.data_ptr(),
+                                         current_stream_handle(stream))
+        _lib.check(rc, self._ctx)
+        return y
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.load().sad_op_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class GmresWorkspace:
+    """(restart+1) basis blocks (+ restart Z blocks for FGMRES) on the device."""
+
+    def __init__(self, n, r, dtype, restart, flexible, device=0):
+        self.n, self.r, self.dtype = n, r, dtype
+        self.restart, self.flexible = restart, bool(flexible)
+        self._ctx = _lib.context(device)
+        h = ctypes.c_void_p()
+        rc = _lib.load().sad_gmres_create(self._ctx, n, r, dtype, restart,
+                                          1 if flexible else 0, ctypes.byref(h))
+        _lib.check(rc, self._ctx)
+        self.handle = h
+
+    @property
+    def nbytes(self):
+        return int(_lib.load().sad_gmres_bytes(self.handle))
+
+    def solve(self, op, rhs, x, res, tol_col, maxit, stream=None):
+        """Returns (iterations int64[r], residual norms float64[r], converged bool[r])."""
+        r = self.r
+        iters = np.zeros(r, dtype=np.int64)
+        norms = np.zeros(r, dtype=np.float64)
+        conv = np.zeros(r, dtype=np.uint8)
+        rc = _lib.load().sad_gmres_solve(
+            self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
+            None if res is None else res.data_ptr(), float(tol_col), int(maxit),
+            current_stream_handle(stream), iters.ctypes.data, norms.ctypes.data,
+            conv.ctypes.data)
+        _lib.check(rc, self._ctx)
+        return iters, norms, conv.astype(bool)
+
+    def fixed(self, op, rhs, x, res, steps, stream=None, timed=False):
+        norms = np.zeros(self.r, dtype=np.float64)
+        timing = np.zeros(4, dtype=np.float64)
+        rc = _lib.load().sad_gmres_fixed(
+            self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
+            None if res is None else res.data_ptr(), int(steps),
+            current_stream_handle(stream), norms.ctypes.data,
+            timing.ctypes.data if timed else None)
+        _lib.check(rc, self._ctx)
+        return norms, timing
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.load().sad_gmres_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def gram(x, y=None, device=0, stream=None):
+    """X^H Y (r x r complex numpy) of two device blocks."""
+    import torch
+    y = x if y is None else y
+    r = x.shape[1]
+    dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
+    out = np.zeros(r * r, dtype=np.complex128)
+    ctx = _lib.context(device)
+    rc = _lib.load().sad_gram(ctx, x.shape[0], r, dtype, x.data_ptr(), y.data_ptr(),
+                              out.ctypes.data, current_stream_handle(stream))
+    _lib.check(rc, ctx)
+    return out.reshape(r, r)
+
+
+def axpy(a, x, y, device=0, stream=None):
+    """y += a x for device blocks (complex a only for complex blocks)."""
+    import torch
+    a = complex(a)
+    dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
+    ctx = _lib.context(device)
+    rc = _lib.load().sad_axpy(ctx, x.shape[0], x.shape[1], dtype, a.real, a.imag,
+                              x.data_ptr(), y.data_ptr(), current_stream_handle(stream))
+    _lib.check(rc, ctx)
+    return y
+
+
+def sigma_max_from_gram(G):
+    """Largest singular value of a block from its Gram matrix X^H X."""
+    if G.size == 0:
+        return 0.0
+    ev = np.linalg.eigvalsh(0.5 * (G + G.conj().T))
+    return float(np.sqrt(max(ev[-1], 0.0)))
+
+
+def product_norm_from_grams(Gw, Gt):
+    """||w t^*||_2 from Gw = w^H w and Gt = t^H t: sqrt(lambda_max(Gw^1/2 Gt Gw^1/2))."""
+    Gw = 0.5 * (Gw + Gw.conj().T)
+    Gt = 0.5 * (Gt + Gt.conj().T)
+    lam, Q = np.linalg.eigh(Gw)
+    half = (Q * np.sqrt(np.clip(lam, 0.0, None))[None, :]) @ Q.conj().T
+    K = half @ Gt @ half
+    ev = np.linalg.eigvalsh(0.5 * (K + K.conj().T))
+    return float(np.sqrt(max(ev[-1], 0.0)))

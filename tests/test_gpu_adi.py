@@ -1,0 +1,89 @@
+"""ADI-level parity on the GPU: the device-resident driver against the CPU
+oracle on identical seeded inputs and pinned shifts (BASELINE north_star bars:
+same outer step count, per-step inner iteration counts within +-2, final
+relative residual below the outer tolerance, ||Z G Y^* - X_ref||_F/||X_ref||_F
+<= 1e-8)."""
+
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import sylvadi_oracle as orc
+from paper_2312_02891_b200 import configs as cfgs
+
+from conftest import GOLD, read_steps_csv
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _gpu_run(name, bindings_mode=False, **kw):
+    import paper_2312_02891_b200 as pb
+    spec = cfgs.CONFIGS[name]
+    A, B, M, C, f, g = cfgs.build_problem(name)
+    pairs, cyclic = spec.load_shift_pairs()
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
+    cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax,
+                       outer_tolerance=spec.outer_tolerance,
+                       precond_kind_A="jacobi", precond_kind_B="jacobi")
+    seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
+    bindings = None
+    if bindings_mode:
+        bindings = pb.make_gpu_bindings(prob, cfg, restart=spec.restart, flexible=spec.flexible)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return pb.run_with_state(prob, cfg, seq, bindings=bindings, restart=spec.restart,
+                                 flexible=spec.flexible, **kw)
+
+
+def _check_against_golden(rep, name):
+    gold = read_steps_csv(os.path.join(GOLD, f"oracle_{name}_gmres.csv"))
+    assert rep.converged
+    assert rep.outer_iterations == len(gold)
+    assert rep.final_scaled_residual < 1e-8
+    worst = 0
+    for rec, gd in zip(rep.records, gold):
+        worst = max(worst, abs(rec.inner_it_A - gd["inner_it_A"]),
+                    abs(rec.inner_it_B - gd["inner_it_B"]))
+        assert abs(rec.delta_A - gd["delta_A"]) <= 1e-6 * gd["delta_A"] + 1e-300
+    assert worst <= 2, worst
+    return worst
+
+
+def test_c1_device_driver_matches_oracle():
+    sol, rep, state = _gpu_run("c1")
+    _check_against_golden(rep, "c1")
+    # X parity in factored form against the oracle's own run (same algorithm)
+    spec = cfgs.CONFIGS["c1"]
+    A, B, M, C, f, g = cfgs.build_problem("c1")
+    pairs, cyclic = spec.load_shift_pairs()
+    ocfg = orc.Config(strategy=spec.strategy, kmax=spec.kmax)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = orc.run_adi(A, B, f, g, ocfg, pairs,
+                          orc.Binding("A", A, None, restart=spec.restart),
+                          orc.Binding("B", B, None, restart=spec.restart), cyclic=cyclic)
+    gd = np.repeat(np.asarray(sol.gammas), sol.r)
+    gr = np.repeat(np.asarray(ref.gammas), sol.r)
+    err = orc.factored_relative_difference(sol.Z, gd, sol.Y, ref.Z, gr, ref.Y)
+    assert err <= 1e-8, err
+
+
+def test_c1_dropin_bindings_host_loop():
+    """GpuGmresBinding behind the reference-style host loop (bindings=...)."""
+    sol, rep, state = _gpu_run("c1", bindings_mode=True)
+    _check_against_golden(rep, "c1")
+
+
+def test_c1_serial_and_concurrent_sides_agree():
+    _, rep1, _ = _gpu_run("c1", concurrent=False)
+    _, rep2, _ = _gpu_run("c1", concurrent=True)
+    assert [r.inner_it_A for r in rep1.records] == [r.inner_it_A for r in rep2.records]
+    assert [r.scaled_res for r in rep1.records] == [r.scaled_res for r in rep2.records]
+
+
+def test_c2_device_driver_matches_oracle():
+    sol, rep, state = _gpu_run("c2")
+    _check_against_golden(rep, "c2")
