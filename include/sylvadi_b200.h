@@ -40,6 +40,11 @@ enum sad_status {
 };
 
 enum sad_dtype { SAD_F64 = 0, SAD_C128 = 1 };
+/* GMRES engines: one cooperative persistent kernel per solve (default), or the
+ * multi-kernel CGS2 pipeline (one launch per phase, host-polled). */
+enum sad_engine { SAD_ENGINE_MULTI = 0, SAD_ENGINE_PERSISTENT = 1 };
+/* sad_gmres_set_option keys */
+enum sad_option { SAD_OPT_ENGINE = 0, SAD_OPT_MAX_SMS = 1, SAD_OPT_MIN_ELEMS_PER_THREAD = 2 };
 enum sad_precond { SAD_PRECOND_NONE = 0, SAD_PRECOND_JACOBI = 1 };
 
 typedef struct sad_ctx sad_ctx;
@@ -107,6 +112,10 @@ int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int restart,
 int sad_gmres_destroy(sad_gmres* ws);
 /* Device bytes held by the workspace. */
 int64_t sad_gmres_bytes(const sad_gmres* ws);
+/* Engine / grid options (see enum sad_option).  SAD_OPT_MAX_SMS caps the SMs a
+ * persistent solve occupies so that the A- and B-side solves can be resident
+ * at the same time on two streams (0 = all SMs). */
+int sad_gmres_set_option(sad_gmres* ws, int key, int value);
 
 /*
  * Solve Op X = RHS column by column (batched in lock-step) to the per-column
@@ -129,21 +138,25 @@ int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
 
 /*
  * Same solve, but a fixed number of Arnoldi steps (no stopping test inside the
- * cycle; config 4 "100 fixed block-GMRES iterations").  Per-kernel device time
- * is accumulated into timing_ms_host[4] = {spmm, orth, givens+small, residual}
- * when timing_ms_host != NULL (CUDA events on `stream`).
+ * cycle; config 4 "100 fixed block-GMRES iterations").  When timing_ms_host is
+ * not NULL it receives (CUDA events on `stream`):
+ *   multi-kernel engine: {spmm_ms, orth_ms, cycle_end_ms, initial_residual_ms}
+ *   persistent engine:   {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes}
  */
 int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
                     void* res_dev, int steps, void* stream,
                     double* resnorm_host, double* timing_ms_host);
 
 /*
- * Profiling of sad_gmres_solve: enable=1 resets the counters and switches the
- * solver to synchronous stepping with CUDA events on the solve stream;
- * enable=0 switches it off.  stats_host[8] (may be NULL) receives the counters
- * accumulated so far: {spmm_ms, spmm_launches, spmm_algorithmic_bytes,
- * orth_ms (CGS2: 2 dots + 2 updates + Givens), arnoldi_steps, orth_bytes,
- * cycle_end_ms, cycles}.
+ * Profiling of sad_gmres_solve: enable=1 resets the counters; enable=0 stops.
+ * stats_host[8] (may be NULL) receives the counters accumulated so far.
+ * Multi-kernel engine (synchronous stepping with CUDA events):
+ *   {spmm_ms, spmm_launches, spmm_algorithmic_bytes, orth_ms, arnoldi_steps,
+ *    orth_bytes, cycle_end_ms, cycles}
+ * Persistent engine (CUDA events around each cooperative launch, phase times
+ * from %globaltimer in block 0):
+ *   {kernel_ms, launches, algorithmic_bytes, phaseA_ms (SpMM + basis dots),
+ *    arnoldi_steps, phaseC_ms (basis update), cycle_end_ms, cycles}
  */
 int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host);
 

@@ -375,10 +375,16 @@ def givens(f, g):
     return af / nrm, alpha * np.conj(g) / nrm, alpha * nrm
 
 
-def _gmres_column(op, dinv, b, tol, m, maxit, flexible):
+def _gmres_column(op, dinv, b, tol, m, maxit, flexible, orth="cgs2"):
     """One column of Jacobi-right-preconditioned GMRES(m) from x0 = 0.
 
     Iteration = one Arnoldi step (u = D^-1 v_j, w = Op u, CGS2, Givens).
+    ``orth="dcgs2"`` replaces the second Gram-Schmidt pass by its Gram-matrix
+    form (the device engine's choice): with G = V^H V kept up to date one
+    column late (G[:, j] = V^H v_j, formed in the same sweep as h1 = V^H w),
+    h2 = h1 - G h1 equals V^H (w - V h1) in exact arithmetic, so
+    w <- w - V (h1 + h2) in ONE update sweep (two basis sweeps per step
+    instead of four; the delayed re-orthogonalisation of Swirydowicz et al.).
     A cycle ends when |g_{j+1}| <= tol, j+1 == m, a lucky breakdown
     (h_{j+1,j} <= GMRES_LUCKY*||w_pre||) or the iteration cap; then
     x += D^-1 V y (GMRES) / Z y (FGMRES) and the TRUE residual b - Op x is
@@ -396,6 +402,7 @@ def _gmres_column(op, dinv, b, tol, m, maxit, flexible):
         return x, 0, r
     while True:
         V = np.zeros((m + 1, n), dtype=np.complex128)
+        Gm = np.zeros((m + 1, m + 1), dtype=np.complex128) if orth == "dcgs2" else None
         Z = np.zeros((m, n), dtype=np.complex128) if flexible else None
         H = np.zeros((m + 1, m), dtype=np.complex128)
         cs = np.zeros(m)
@@ -410,11 +417,19 @@ def _gmres_column(op, dinv, b, tol, m, maxit, flexible):
                 Z[j] = u
             w = op.apply(u[:, None])[:, 0]
             wpre = np.linalg.norm(w)
-            h = V[:j + 1].conj() @ w
-            w = w - V[:j + 1].T @ h
-            h2 = V[:j + 1].conj() @ w
-            w = w - V[:j + 1].T @ h2
-            h = h + h2
+            if orth == "dcgs2":
+                gcol = V[:j + 1].conj() @ V[j]
+                Gm[:j + 1, j] = gcol
+                Gm[j, :j + 1] = np.conj(gcol)
+                h1 = V[:j + 1].conj() @ w
+                h = h1 + (h1 - Gm[:j + 1, :j + 1] @ h1)
+                w = w - V[:j + 1].T @ h
+            else:
+                h = V[:j + 1].conj() @ w
+                w = w - V[:j + 1].T @ h
+                h2 = V[:j + 1].conj() @ w
+                w = w - V[:j + 1].T @ h2
+                h = h + h2
             hn = np.linalg.norm(w)
             col = np.zeros(m + 1, dtype=np.complex128)
             col[:j + 1] = h
@@ -458,7 +473,7 @@ def _back_substitute(R, g):
 
 
 def gmres(op, rhs, abs_tolerance, max_iterations=1000, dinv=None,
-          restart=50, flexible=False):
+          restart=50, flexible=False, orth="cgs2"):
     """Batched-by-column GMRES with the reference's result contract
     (krylov.py:41-70, per-column target abs_tolerance/r, krylov.py:164)."""
     rhs = _check_request(op, rhs, abs_tolerance)
@@ -470,7 +485,7 @@ def gmres(op, rhs, abs_tolerance, max_iterations=1000, dinv=None,
     iters = np.zeros(r, dtype=np.int64)
     for c in range(r):
         xc, it, _ = _gmres_column(op, dinv, rhs[:, c], tol_col, restart,
-                                  max_iterations, flexible)
+                                  max_iterations, flexible, orth)
         x[:, c] = xc
         iters[c] = it
     return _finalize(op, rhs, x, iters, tol_col)
@@ -486,7 +501,7 @@ class Binding:
     """
 
     def __init__(self, side, base, mass, solver="gmres", max_iterations=1000,
-                 restart=50, precond="jacobi"):
+                 restart=50, precond="jacobi", orth="cgs2"):
         self.side = side
         self.base = base
         self.mass = mass
@@ -494,6 +509,7 @@ class Binding:
         self.max_iterations = max_iterations
         self.restart = restart
         self.precond = precond
+        self.orth = orth
         self._ops = {}
 
     def _op(self, shift):
@@ -511,7 +527,8 @@ class Binding:
         if self.solver == "bicgstab":
             return bicgstab(op, rhs, delta, self.max_iterations, dinv)
         return gmres(op, rhs, delta, self.max_iterations, dinv,
-                     restart=self.restart, flexible=(self.solver == "fgmres"))
+                     restart=self.restart, flexible=(self.solver == "fgmres"),
+                     orth=self.orth)
 
 
 class StepRec:

@@ -3,6 +3,7 @@
     python -m paper_2312_02891_b200._build [--force]
 """
 
+import glob
 import os
 import shutil
 import subprocess
@@ -11,8 +12,8 @@ import sys
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SRC_DIR = os.path.join(_HERE, "csrc")
 SOURCES = [os.path.join(SRC_DIR, "sad_capi.cu")]
-DEPS = SOURCES + [os.path.join(SRC_DIR, "sad_kernels.cuh"),
-                  os.path.join(os.path.dirname(_HERE), "include", "sylvadi_b200.h")]
+DEPS = SOURCES + sorted(glob.glob(os.path.join(SRC_DIR, "*.cuh"))) + [
+    os.path.join(os.path.dirname(_HERE), "include", "sylvadi_b200.h")]
 OUT = os.path.join(_HERE, "libsylvadi_b200.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",

@@ -14,6 +14,8 @@ LIB_PATH = os.path.join(_HERE, "libsylvadi_b200.so")
 SAD_OK, SAD_EINVAL, SAD_EBREAKDOWN, SAD_ECUDA, SAD_ENCCL, SAD_ENOMEM = range(6)
 SAD_F64, SAD_C128 = 0, 1
 SAD_PRECOND_NONE, SAD_PRECOND_JACOBI = 0, 1
+SAD_ENGINE_MULTI, SAD_ENGINE_PERSISTENT = 0, 1
+SAD_OPT_ENGINE, SAD_OPT_MAX_SMS, SAD_OPT_MIN_ELEMS_PER_THREAD = 0, 1, 2
 
 #: every symbol declared in include/sylvadi_b200.h with (restype, argtypes)
 _c = ctypes
@@ -42,6 +44,7 @@ SIGNATURES = {
                                     _c.POINTER(_vp)]),
     "sad_gmres_destroy": (_c.c_int, [_vp]),
     "sad_gmres_bytes": (_i64, [_vp]),
+    "sad_gmres_set_option": (_c.c_int, [_vp, _c.c_int, _c.c_int]),
     "sad_gmres_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp,
                                    _vp, _vp, _vp]),
     "sad_gmres_fixed": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_int, _vp, _vp, _vp]),

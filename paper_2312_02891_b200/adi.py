@@ -414,7 +414,8 @@ def run(problem, config, shift_sequence, bindings=None, **kw):
 
 
 def run_with_state(problem, config, shift_sequence, bindings=None, *, restart=50,
-                   flexible=False, device=0, concurrent=True, keep_on_device=False):
+                   flexible=False, device=0, concurrent=True, keep_on_device=False,
+                   engine="persistent"):
     """adi.py:553-607.  ``bindings=None`` runs the device-resident driver with
     GpuGmresBinding(restart, flexible) on both sides; otherwise the host loop
     drives the given bindings."""
@@ -425,7 +426,8 @@ def run_with_state(problem, config, shift_sequence, bindings=None, *, restart=50
     if bindings is not None:
         return _run_host(problem, config, shift_sequence, bindings)
     return _run_device(problem, config, shift_sequence, restart=restart, flexible=flexible,
-                       device=device, concurrent=concurrent, keep_on_device=keep_on_device)
+                       device=device, concurrent=concurrent, keep_on_device=keep_on_device,
+                       engine=engine)
 
 
 def _adopt_config(cfg):
@@ -511,7 +513,7 @@ class DeviceAdi:
     (the bench times repeated runs with the inputs already in HBM)."""
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
-                 device=0, concurrent=True):
+                 device=0, concurrent=True, engine="persistent"):
         import torch
         if not isinstance(problem, SylvesterProblem):
             problem = SylvesterProblem.from_reference(problem)
@@ -531,12 +533,20 @@ class DeviceAdi:
         self.tdtype = torch.complex128 if complex_run else torch.float64
         kind_a = config.precond_kind_A
         kind_b = config.precond_kind_B
+        # concurrent A/B persistent solves: each side may occupy half of the SMs
+        # (proportional to its size) so both cooperative grids are co-resident
+        nsm = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        na, nb = problem.n, problem.m
+        sm_a = max(1, min(nsm - 1, int(round(nsm * na / (na + nb))))) if concurrent else 0
+        sm_b = max(1, nsm - sm_a) if concurrent else 0
         self.bA = GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
                                   max_iterations=config.max_inner_iterations, restart=restart,
-                                  flexible=flexible, device=device)
+                                  flexible=flexible, device=device, engine=engine,
+                                  max_sms=sm_a)
         self.bB = GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
                                   max_iterations=config.max_inner_iterations, restart=restart,
-                                  flexible=flexible, device=device)
+                                  flexible=flexible, device=device, engine=engine,
+                                  max_sms=sm_b)
         self.Md = self.bA.mass      # M (for M z)
         self.Cd = self.bB.mass      # C with transpose (for C^T y)
         self.f = torch.from_numpy(np.ascontiguousarray(problem.f)).to(self.dev, self.tdtype)
@@ -653,9 +663,9 @@ def _seq_len(seq):
 
 
 def _run_device(problem, config, shifts, restart, flexible, device, concurrent,
-                keep_on_device):
+                keep_on_device, engine="persistent"):
     eng = DeviceAdi(problem, config, shifts, restart=restart, flexible=flexible,
-                    device=device, concurrent=concurrent)
+                    device=device, concurrent=concurrent, engine=engine)
     sol, rep, state = eng.run()
     if not keep_on_device:
         state.Z, state.Y = sol.Z, sol.Y

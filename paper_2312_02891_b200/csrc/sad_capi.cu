@@ -21,6 +21,7 @@
 
 #include "../../include/sylvadi_b200.h"
 #include "sad_kernels.cuh"
+#include "sad_persistent.cuh"
 
 using namespace sad;
 
@@ -96,6 +97,12 @@ struct sad_gmres {
   GState st{};
   int64_t bytes = 0;
   int dot_blocks_per_sm = 1;
+  // persistent engine
+  int engine = SAD_ENGINE_PERSISTENT;
+  int max_sms = 0;              // 0 = all SMs
+  int min_elems_per_thread = 2;
+  PState pst{};
+  double* stats_dev = nullptr;
   // profiling (sad_gmres_profile): synchronous stepping with CUDA events
   int profile = 0;
   double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -619,7 +626,7 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
     return set_err(ctx, SAD_ENOMEM, "FGMRES Z allocation failed");
   }
   ws->max_blocks = ctx->nsm * 8;
-  ws->pstride = 2 * (m + 1) * r + r + 8;
+  ws->pstride = 2 * (2 * (m + 1) * r + r) + 8;
   size_t sb = 0;
   sb += 16 * 8;                              // j, any_active, jx, ticket, seqs
   sb += 4 * r * sizeof(int) + r * 8 + 64;    // active, done, kdim, iters
@@ -630,6 +637,10 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
   sb += (size_t)r * (m + 1) * 16;            // g
   sb += (size_t)m * r * 16;                  // ycoef
   sb += 2 * r * 8;                           // wpre2, beta
+  sb += (size_t)r * (m + 1) * (m + 1) * 16;  // G (persistent engine)
+  sb += 2 * (size_t)(m + 1) * r * 16;        // hc, coef
+  sb += (size_t)(2 * (m + 1) + 1) * r * 16;  // red
+  sb += 4 * 16 + 8 * 8;                      // barrier, err, stats
   sb += 64 * 16;                             // alignment slack
   ws->state_bytes = sb;
   if (cudaMalloc(&ws->state, sb) != cudaSuccess ||
@@ -662,6 +673,16 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
   st.ycoef = carve<double2>(p, (size_t)m * r);
   st.wpre2 = carve<double>(p, r);
   st.beta = carve<double>(p, r);
+  PState& ps = ws->pst;
+  ps.G = carve<double2>(p, (size_t)r * (m + 1) * (m + 1));
+  ps.hc = carve<double2>(p, (size_t)(m + 1) * r);
+  ps.coef = carve<double2>(p, (size_t)(m + 1) * r);
+  ps.red = carve<double2>(p, (size_t)(2 * (m + 1) + 1) * r);
+  ps.bar_count = carve<unsigned>(p, 1);
+  ps.bar_gen = carve<unsigned>(p, 1);
+  ps.err = carve<int>(p, 1);
+  ps.stats = carve<double>(p, 8);
+  ws->stats_dev = ps.stats;
   if ((size_t)(p - ws->state) > sb) {
     sad_gmres_destroy(ws);
     return set_err(ctx, SAD_EINVAL, "internal: state carve overflow");
@@ -919,6 +940,156 @@ extern "C" int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host) 
   return SAD_OK;
 }
 
+// ---- persistent (cooperative) engine ------------------------------------------
+template <typename XT, typename VT, int R, bool SIGMA, bool FLEX>
+static cudaError_t coop_launch_t(PArgs<XT> a, sad_gmres* ws, cudaStream_t s, size_t smem) {
+  auto kern = k_gmres_persistent<XT, VT, R, true, SIGMA, FLEX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int nb = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (nb < 1) return cudaErrorInvalidConfiguration;
+  const int nsm = ws->ctx->nsm;
+  const int sms = ws->max_sms > 0 ? std::min(ws->max_sms, nsm) : nsm;
+  const long long elems = a.n * R;
+  const long long per_block = (long long)kThreads * std::max(1, ws->min_elems_per_thread);
+  long long grid = (elems + per_block - 1) / per_block;
+  grid = std::max(1LL, std::min(grid, (long long)nb * sms));
+  grid = std::min(grid, (long long)ws->max_blocks);
+  a.rows_per_block = (a.n + grid - 1) / grid;
+  void* args[] = {(void*)&a};
+  e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
+  COUNT_LAUNCH(1);
+  return e;
+}
+
+template <typename XT, typename VT, bool SIGMA, bool FLEX>
+static cudaError_t coop_R(int R, const PArgs<XT>& a, sad_gmres* ws, cudaStream_t s, size_t smem) {
+  switch (R) {
+    case 1: return coop_launch_t<XT, VT, 1, SIGMA, FLEX>(a, ws, s, smem);
+    case 2: return coop_launch_t<XT, VT, 2, SIGMA, FLEX>(a, ws, s, smem);
+    case 3: return coop_launch_t<XT, VT, 3, SIGMA, FLEX>(a, ws, s, smem);
+    case 4: return coop_launch_t<XT, VT, 4, SIGMA, FLEX>(a, ws, s, smem);
+    case 5: return coop_launch_t<XT, VT, 5, SIGMA, FLEX>(a, ws, s, smem);
+    case 6: return coop_launch_t<XT, VT, 6, SIGMA, FLEX>(a, ws, s, smem);
+    case 7: return coop_launch_t<XT, VT, 7, SIGMA, FLEX>(a, ws, s, smem);
+    case 8: return coop_launch_t<XT, VT, 8, SIGMA, FLEX>(a, ws, s, smem);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename XT, typename VT, bool SIGMA>
+static cudaError_t coop_flex(bool flex, int R, const PArgs<XT>& a, sad_gmres* ws, cudaStream_t s,
+                             size_t smem) {
+  return flex ? coop_R<XT, VT, SIGMA, true>(R, a, ws, s, smem)
+              : coop_R<XT, VT, SIGMA, false>(R, a, ws, s, smem);
+}
+
+static cudaError_t coop_dispatch_d(const PArgs<double>& a, sad_gmres* ws, sad_op* op,
+                                   cudaStream_t s, size_t smem) {
+  return op->sigma_identity ? coop_flex<double, double, true>(ws->flexible, ws->R, a, ws, s, smem)
+                            : coop_flex<double, double, false>(ws->flexible, ws->R, a, ws, s, smem);
+}
+static cudaError_t coop_dispatch_z(const PArgs<double2>& a, sad_gmres* ws, sad_op* op,
+                                   cudaStream_t s, size_t smem) {
+  if (op->vals_complex) return coop_flex<double2, double2, false>(ws->flexible, ws->R, a, ws, s, smem);
+  return op->sigma_identity ? coop_flex<double2, double, true>(ws->flexible, ws->R, a, ws, s, smem)
+                            : coop_flex<double2, double, false>(ws->flexible, ws->R, a, ws, s, smem);
+}
+
+template <typename XT>
+static PArgs<XT> make_pargs(sad_gmres* ws, sad_op* op, const void* rhs, void* x) {
+  PArgs<XT> a{};
+  a.n = ws->n;
+  a.rowptr = op->rowptr;
+  a.colidx = op->colidx;
+  a.vals = op->vals;
+  a.dinv = reinterpret_cast<const XT*>(sizeof(XT) == 8 ? (const void*)op->dinv_r
+                                                       : (const void*)op->dinv_c);
+  a.sigma = op->sigma_eff;
+  a.b = reinterpret_cast<const XT*>(rhs);
+  a.x = reinterpret_cast<XT*>(x);
+  a.V = reinterpret_cast<XT*>(ws->V);
+  a.Z = reinterpret_cast<XT*>(ws->Z);
+  a.stride = ws->n * ws->R;
+  a.st = ws->pst;
+  return a;
+}
+
+static double spmm_bytes(const sad_gmres* ws, const sad_op* op, bool arnoldi);
+
+static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, cudaStream_t s,
+                          double tol, int maxit, int fixed) {
+  sad_ctx* ctx = ws->ctx;
+  if (!op || !rhs || !x) return set_err(ctx, SAD_EINVAL, "null argument");
+  if (op->n != ws->n)
+    return set_err(ctx, SAD_EINVAL, "operator size %lld != workspace size %lld", op->n, ws->n);
+  if (ws->dtype == SAD_F64 && !op->real_ok)
+    return set_err(ctx, SAD_EINVAL, "complex shift needs a complex128 workspace");
+  ws->st.tol = tol;
+  ws->st.maxit = maxit;
+  ws->st.fixed = fixed;
+  ws->pst.g = ws->st;
+  ws->pst.spmm_bytes_arn = spmm_bytes(ws, op, true);
+  ws->pst.spmm_bytes_res = spmm_bytes(ws, op, false) + (double)ws->n * ws->R * ws->esz;
+  CK(ctx, cudaMemsetAsync(ws->pst.bar_count, 0, sizeof(unsigned), s));
+  CK(ctx, cudaMemsetAsync(ws->pst.err, 0, sizeof(int), s));
+  if (ws->profile) {
+    CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 8 * sizeof(double), s));
+    CK(ctx, cudaEventRecord(ws->ev[0], s));
+  }
+  const size_t smem = (size_t)2 * (ws->m + 1) * kWarps * ws->R * ws->esz;
+  cudaError_t e;
+  if (ws->dtype == SAD_F64) e = coop_dispatch_d(make_pargs<double>(ws, op, rhs, x), ws, op, s, smem);
+  else e = coop_dispatch_z(make_pargs<double2>(ws, op, rhs, x), ws, op, s, smem);
+  if (e != cudaSuccess)
+    return set_err(ctx, SAD_ECUDA, "cooperative GMRES launch failed: %s", cudaGetErrorString(e));
+  if (ws->profile) CK(ctx, cudaEventRecord(ws->ev[1], s));
+  return SAD_OK;
+}
+
+static int persistent_collect(sad_gmres* ws, cudaStream_t s) {
+  sad_ctx* ctx = ws->ctx;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(ctx, SAD_ECUDA, "persistent GMRES failed: %s", cudaGetErrorString(e));
+  if (ws->profile) {
+    float ms = 0.f;
+    CK(ctx, cudaEventElapsedTime(&ms, ws->ev[0], ws->ev[1]));
+    double st[8];
+    CK(ctx, cudaMemcpy(st, ws->stats_dev, sizeof(st), cudaMemcpyDeviceToHost));
+    ws->prof[0] += ms;
+    ws->prof[1] += 1;
+    ws->prof[2] += st[0];
+    ws->prof[3] += st[3] * 1e-6;
+    ws->prof[4] += st[1];
+    ws->prof[5] += st[4] * 1e-6;
+    ws->prof[6] += (st[5] + st[6]) * 1e-6;
+    ws->prof[7] += st[2];
+  }
+  return SAD_OK;
+}
+
+extern "C" int sad_gmres_set_option(sad_gmres* ws, int key, int value) {
+  if (!ws) return SAD_EINVAL;
+  switch (key) {
+    case SAD_OPT_ENGINE:
+      if (value != SAD_ENGINE_MULTI && value != SAD_ENGINE_PERSISTENT)
+        return set_err(ws->ctx, SAD_EINVAL, "unknown engine %d", value);
+      ws->engine = value;
+      return SAD_OK;
+    case SAD_OPT_MAX_SMS:
+      if (value < 0) return set_err(ws->ctx, SAD_EINVAL, "max_sms must be >= 0");
+      ws->max_sms = value;
+      return SAD_OK;
+    case SAD_OPT_MIN_ELEMS_PER_THREAD:
+      if (value < 1) return set_err(ws->ctx, SAD_EINVAL, "min elements per thread must be >= 1");
+      ws->min_elems_per_thread = value;
+      return SAD_OK;
+  }
+  return set_err(ws->ctx, SAD_EINVAL, "unknown option %d", key);
+}
+
 extern "C" int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs, void* x, void* res,
                                double tol_col, int maxit, void* stream, int64_t* iters_host,
                                double* resnorm_host, uint8_t* conv_host) {
@@ -927,6 +1098,13 @@ extern "C" int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs, void*
   if (!(tol_col > 0.0)) return set_err(ctx, SAD_EINVAL, "abs_tolerance must be positive");
   if (maxit < 0) return set_err(ctx, SAD_EINVAL, "maxit must be >= 0");
   cudaStream_t s = S_(stream);
+  if (ws->engine == SAD_ENGINE_PERSISTENT) {
+    int rc = persistent_run(ws, op, rhs, x, s, tol_col, maxit, 0);
+    if (rc) return rc;
+    rc = persistent_collect(ws, s);
+    if (rc) return rc;
+    return read_results(ws, res, s, iters_host, resnorm_host, conv_host, tol_col);
+  }
   Launcher L;
   int rc = prepare(ws, op, rhs, x, s, L);
   if (rc) return rc;
@@ -1008,6 +1186,34 @@ extern "C" int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs, void*
   if (steps < 1 || steps > ws->m)
     return set_err(ctx, SAD_EINVAL, "steps %d outside 1..restart(%d)", steps, ws->m);
   cudaStream_t s = S_(stream);
+  if (ws->engine == SAD_ENGINE_PERSISTENT) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing_ms) {
+      CK(ctx, cudaEventCreate(&e0));
+      CK(ctx, cudaEventCreate(&e1));
+      CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 8 * sizeof(double), s));
+      CK(ctx, cudaEventRecord(e0, s));
+    }
+    int rc = persistent_run(ws, op, rhs, x, s, 0.0, steps, 1);
+    if (rc) return rc;
+    if (timing_ms) CK(ctx, cudaEventRecord(e1, s));
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_err(ctx, SAD_ECUDA, "persistent GMRES failed: %s", cudaGetErrorString(e));
+    if (timing_ms) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double st[8];
+      CK(ctx, cudaMemcpy(st, ws->stats_dev, sizeof(st), cudaMemcpyDeviceToHost));
+      // {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes}
+      timing_ms[0] = ms;
+      timing_ms[1] = st[3] * 1e-6;
+      timing_ms[2] = st[4] * 1e-6;
+      timing_ms[3] = st[0];
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    return read_results(ws, res, s, nullptr, resnorm_host, nullptr, 0.0);
+  }
   Launcher L;
   int rc = prepare(ws, op, rhs, x, s, L);
   if (rc) return rc;

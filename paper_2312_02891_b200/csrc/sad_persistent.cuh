@@ -1,0 +1,620 @@
+// sad_persistent.cuh -- the whole GMRES/FGMRES solve as ONE cooperative kernel.
+//
+// Every block owns a contiguous slab of rows.  One Arnoldi step is two
+// streaming phases separated by grid-wide "reduce barriers":
+//
+//   phase A  w = Op(D^-1 v_j)  (fused shifted SpMM, own rows)
+//            h_raw = V^H w  and the delayed Gram column g_raw = V^H v_j
+//            (ONE sweep over the basis), ||w||^2
+//   -- barrier; the last block reduces the partials in block order and forms
+//      G[:, j], h1 = S h_raw, h2 = h1 - G h1, c = h1 + h2, coef = S c --
+//   phase C  w <- w - sum_i V_i coef_i  (ONE sweep), ||w||^2
+//   -- barrier; the last block does the Hessenberg column, Givens rotation,
+//      stopping test (and, at a cycle end, the triangular solve) --
+//
+// so the basis is streamed twice per step (CGS2 streams it four times) and the
+// host is not involved until the solve is over.  At a cycle end the blocks
+// update x (phase X), recompute the TRUE residual b - Op x into V_0 (phase R)
+// and the last block decides per column whether to restart.
+//
+// Reductions are deterministic (fixed block order, fixed trees).  Mutable
+// shared data is read after a barrier whose release is followed by
+// __threadfence() (invalidates L1), or with ld.cg.
+#pragma once
+
+#include "sad_kernels.cuh"
+
+namespace sad {
+
+struct PState {
+  GState g;              // j, any_active, active, done, kdim, iters, S, H, cs, sn, g, ycoef, ...
+  double2* G;            // [R][(m+1)*(m+1)] Gram of the raw-scaled basis
+  double2* hc;           // [(m+1)*R] Hessenberg column before rotation
+  double2* coef;         // [(m+1)*R] phase-C coefficients
+  double2* red;          // [(2(m+1)+1)*R] reduced partials
+  unsigned* bar_count;
+  unsigned* bar_gen;
+  int* err;              // barrier timeout flag
+  double* stats;         // [8] bytes_alg, steps, cycles, t_A, t_C, t_X, t_R (ns, block 0)
+  double spmm_bytes_arn; // algorithmic bytes of one Arnoldi SpMM
+  double spmm_bytes_res; // algorithmic bytes of one residual SpMM
+};
+
+template <typename XT>
+struct PArgs {
+  long long n;
+  const int* rowptr;
+  const int* colidx;
+  const void* vals;
+  const XT* dinv;
+  double2 sigma;
+  const XT* b;
+  XT* x;
+  XT* V;
+  XT* Z;
+  long long stride;      // n*R elements per basis block
+  long long rows_per_block;
+  PState st;
+};
+
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+__device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
+__device__ __forceinline__ double ldcg1(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ int ldcgi(const int* p) { return __ldcg(p); }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Arrive at the grid barrier.  Returns true in exactly one block (the last to
+// arrive), which must then do the reduction and call release().
+__device__ __forceinline__ bool bar_arrive(const PState& st, unsigned& gen_seen) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gen_seen = ld_volatile_u32(st.bar_gen);
+    __threadfence();
+    unsigned t = atomicAdd(st.bar_count, 1u);
+    s_last = (t == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  bool last = s_last != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+__device__ __forceinline__ void bar_release(const PState& st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *st.bar_count = 0u;
+    __threadfence();
+    atomicAdd(st.bar_gen, 1u);
+  }
+  __syncthreads();
+}
+
+// Non-last blocks wait for the release; spin with a 20 s safety timeout
+// (a hang would otherwise wedge the GPU).
+__device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0 = gtimer();
+    unsigned spins = 0;
+    while (ld_volatile_u32(st.bar_gen) == gen_seen) {
+      if (++spins > 64) __nanosleep(64);
+      if ((spins & 1023u) == 0 && gtimer() - t0 > 20000000000ull) {
+        atomicExch(st.err, 1);
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+  __threadfence();
+}
+
+// Deterministic reduction of per-block partials: out[o] = sum_b part[b][o],
+// o < nout (complex), using all threads of the (last) block.
+__device__ void reduce_partials(const double* part, int pstride, int nblocks, int nout,
+                                double2* out) {
+  __shared__ double2 s_red[kThreads];
+  int teams = nout >= kThreads ? 1 : kThreads / nout;
+  for (int base = 0; base < nout; base += kThreads / teams) {
+    const int t = threadIdx.x;
+    const int o = base + t / teams;
+    const int lane_in = t % teams;
+    double2 acc = make_double2(0.0, 0.0);
+    if (o < nout && t / teams < kThreads / teams) {
+      int b = lane_in;
+      for (; b + 3 * teams < nblocks; b += 4 * teams) {
+        const double* p0 = part + (size_t)b * pstride + 2 * o;
+        const double* p1 = p0 + (size_t)teams * pstride;
+        const double* p2 = p1 + (size_t)teams * pstride;
+        const double* p3 = p2 + (size_t)teams * pstride;
+        double a0 = __ldcg(p0), a1 = __ldcg(p0 + 1), b0 = __ldcg(p1), b1 = __ldcg(p1 + 1);
+        double c0 = __ldcg(p2), c1 = __ldcg(p2 + 1), d0 = __ldcg(p3), d1 = __ldcg(p3 + 1);
+        acc.x += a0; acc.y += a1;
+        acc.x += b0; acc.y += b1;
+        acc.x += c0; acc.y += c1;
+        acc.x += d0; acc.y += d1;
+      }
+      for (; b < nblocks; b += teams) {
+        const double* p0 = part + (size_t)b * pstride + 2 * o;
+        acc.x += __ldcg(p0);
+        acc.y += __ldcg(p0 + 1);
+      }
+    }
+    s_red[t] = acc;
+    __syncthreads();
+    if (lane_in == 0 && o < nout && t / teams < kThreads / teams) {
+      double2 sum = s_red[t];
+      for (int q = 1; q < teams; ++q) sum = add(sum, s_red[t + q]);
+      out[o] = sum;
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// row kernels shared by the phases
+// ----------------------------------------------------------------------------
+template <typename XT, typename VT, bool PRE, bool SIGMA, int R>
+__device__ __forceinline__ XT spmm_row(const PArgs<XT>& a, const XT* x, long long row,
+                                       int c, XT& xi_out) {
+  const VT* vals = reinterpret_cast<const VT*>(a.vals);
+  const int k0 = __ldg(a.rowptr + row), k1 = __ldg(a.rowptr + row + 1);
+  XT acc = zero<XT>();
+  int k = k0;
+  for (; k + 1 < k1; k += 2) {
+    const int c0 = __ldg(a.colidx + k), c1 = __ldg(a.colidx + k + 1);
+    const VT v0 = __ldg(vals + k), v1 = __ldg(vals + k + 1);
+    XT x0 = x[(long long)c0 * R + c];
+    XT x1 = x[(long long)c1 * R + c];
+    if (PRE) {
+      x0 = mul(__ldg(a.dinv + c0), x0);
+      x1 = mul(__ldg(a.dinv + c1), x1);
+    }
+    acc = fma_(v0, x0, acc);
+    acc = fma_(v1, x1, acc);
+  }
+  if (k < k1) {
+    const int c0 = __ldg(a.colidx + k);
+    const VT v0 = __ldg(vals + k);
+    XT x0 = x[(long long)c0 * R + c];
+    if (PRE) x0 = mul(__ldg(a.dinv + c0), x0);
+    acc = fma_(v0, x0, acc);
+  }
+  XT xi = x[row * R + c];
+  xi_out = xi;
+  if (SIGMA) {
+    XT xs = PRE ? mul(__ldg(a.dinv + row), xi) : xi;
+    acc = fma_(from_c<XT>(a.sigma), xs, acc);
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------
+// the persistent solve kernel
+// ----------------------------------------------------------------------------
+template <typename XT, typename VT, int R, bool PRE, bool SIGMA, bool FLEX>
+__global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
+  constexpr int GPW = 32 / R;
+  constexpr int UA = (R <= 2) ? 8 : 4;   // rows per lane per phase-A tile
+  constexpr int UC = (R <= 2) ? 8 : 4;   // rows per lane per phase-C tile
+  extern __shared__ double smem_p[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / R, c = lane - grp * R;
+  const bool lane_ok = grp < GPW;
+  PState& st = a.st;
+  GState& gs = st.g;
+  const int m = gs.m;
+  const long long n = a.n;
+  const long long r0 = (long long)blockIdx.x * a.rows_per_block;
+  const long long r1 = min(n, r0 + a.rows_per_block);
+  // rows owned by this lane: r0 + warp*GPW + grp + q*kWarps*GPW
+  const long long row_step = (long long)kWarps * GPW;
+  const long long row_first = r0 + warp * GPW + grp;
+  const int pstride = gs.pstride;
+  double* mypart = gs.part + (size_t)blockIdx.x * pstride;
+  unsigned gen = 0;
+  const bool timing = (blockIdx.x == 0 && threadIdx.x == 0);
+  unsigned long long tphase = 0;
+
+  XT* s_acc = reinterpret_cast<XT*>(smem_p);  // [2(m+1)][kWarps][R] (phase A)
+  __shared__ double s_w2[kWarps][8];
+  __shared__ int s_any;
+
+  // ---- init: x = 0, V_0 = b, ||b||^2 -> restart decision --------------------
+  {
+    if (blockIdx.x == 0 && threadIdx.x < R) {
+      gs.iters[threadIdx.x] = 0;
+      gs.done[threadIdx.x] = 0;
+      gs.active[threadIdx.x] = 0;
+      gs.kdim[threadIdx.x] = 0;
+    }
+    double n2 = 0.0;
+    if (lane_ok)
+      for (long long row = row_first; row < r1; row += row_step) {
+        XT bv = a.b[row * R + c];
+        a.V[row * R + c] = bv;
+        a.x[row * R + c] = zero<XT>();
+        n2 += abs2(bv);
+      }
+    n2 = group_reduce<R>(n2, grp);
+    if (grp == 0 && lane_ok) s_w2[warp][c] = n2;
+    __syncthreads();
+    if (threadIdx.x < R) {
+      double t = 0.0;
+      for (int w = 0; w < kWarps; ++w) t += s_w2[w][threadIdx.x];
+      mypart[2 * threadIdx.x] = t;
+      mypart[2 * threadIdx.x + 1] = 0.0;
+    }
+    if (bar_arrive(st, gen)) {
+      reduce_partials(gs.part, pstride, gridDim.x, R, st.red);
+      __syncthreads();
+      __shared__ double s_n2[8];
+      if (threadIdx.x < R) s_n2[threadIdx.x] = st.red[threadIdx.x].x;
+      __syncthreads();
+      // fin_cycle without the host flag protocol
+      if (threadIdx.x < R) {
+        int cc = threadIdx.x;
+        double beta = sqrt(s_n2[cc]);
+        gs.beta[cc] = beta;
+        bool d = beta <= gs.tol || gs.iters[cc] >= gs.maxit;
+        gs.done[cc] = d;
+        gs.active[cc] = !d;
+        gs.kdim[cc] = 0;
+        gs.S[cc] = d ? 0.0 : 1.0 / beta;
+        gs.g[cc * (m + 1)] = make_double2(beta, 0.0);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int any = 0;
+        for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
+        *gs.any_active = any;
+        *gs.j = 0;
+        st.stats[2] += 1.0;
+      }
+      bar_release(st);
+    } else {
+      bar_wait(st, gen);
+    }
+  }
+
+  // ---- cycles ---------------------------------------------------------------
+  while (true) {
+    if (threadIdx.x == 0) s_any = ldcgi(gs.any_active);
+    __syncthreads();
+    if (!s_any) break;
+    // ---------------- Arnoldi steps ----------------
+    while (true) {
+      const int j = ldcgi(gs.j);
+      const int J = j + 1;
+      if (timing) tphase = gtimer();
+      // ======== phase A: SpMM + h_raw + delayed Gram column ========
+      {
+        const XT* vj = a.V + (long long)j * a.stride;
+        XT* w = a.V + (long long)J * a.stride;
+        const double sj = lane_ok ? ldcg1(gs.S + j * R + c) : 0.0;
+        for (int o = threadIdx.x; o < 2 * J * kWarps * R; o += kThreads) s_acc[o] = zero<XT>();
+        double w2 = 0.0;
+        __syncthreads();
+        for (long long base = r0 + (long long)warp * GPW * UA; base < r1;
+             base += (long long)kWarps * GPW * UA) {
+          // warp-uniform loop: the shuffles below need every lane present
+          XT wv[UA], xv[UA];
+          long long idx[UA];
+#pragma unroll
+          for (int u = 0; u < UA; ++u) {
+            const long long row = base + u * GPW + grp;
+            const bool ok = lane_ok && row < r1;
+            idx[u] = ok ? row * R + c : -1;
+            wv[u] = zero<XT>();
+            xv[u] = zero<XT>();
+            if (ok) {
+              XT xi;
+              XT acc = spmm_row<XT, VT, PRE, SIGMA, R>(a, vj, row, c, xi);
+              wv[u] = sscal(sj, acc);
+              xv[u] = xi;
+              w[idx[u]] = wv[u];
+              if (FLEX) {
+                XT zi = PRE ? mul(__ldg(a.dinv + row), xi) : xi;
+                a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
+              }
+              w2 += abs2(wv[u]);
+            }
+          }
+          for (int i = 0; i < J; ++i) {
+            const XT* vi = a.V + (long long)i * a.stride;
+            XT ph = zero<XT>(), pg = zero<XT>();
+#pragma unroll
+            for (int u = 0; u < UA; ++u) {
+              if (idx[u] >= 0) {
+                const XT v = vi[idx[u]];
+                ph = cfma(v, wv[u], ph);
+                pg = cfma(v, xv[u], pg);
+              }
+            }
+            ph = group_reduce<R>(ph, grp);
+            pg = group_reduce<R>(pg, grp);
+            if (grp == 0 && lane_ok) {
+              XT* s0 = s_acc + ((size_t)i * kWarps + warp) * R + c;
+              *s0 = add(*s0, ph);
+              XT* s1 = s_acc + ((size_t)(J + i) * kWarps + warp) * R + c;
+              *s1 = add(*s1, pg);
+            }
+          }
+        }
+        w2 = group_reduce<R>(w2, grp);
+        if (grp == 0 && lane_ok) s_w2[warp][c] = w2;
+        __syncthreads();
+        for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) {
+          const int ii = o / R, cc = o - ii * R;
+          XT t = zero<XT>();
+          for (int wq = 0; wq < kWarps; ++wq) t = add(t, s_acc[((size_t)ii * kWarps + wq) * R + cc]);
+          const double2 tc = to_c(t);
+          mypart[2 * o] = tc.x;
+          mypart[2 * o + 1] = tc.y;
+        }
+        if (threadIdx.x < R) {
+          double t = 0.0;
+          for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
+          mypart[2 * (2 * J * R + threadIdx.x)] = t;
+          mypart[2 * (2 * J * R + threadIdx.x) + 1] = 0.0;
+        }
+        if (bar_arrive(st, gen)) {
+          const int nout = 2 * J * R + R;
+          reduce_partials(gs.part, pstride, gridDim.x, nout, st.red);
+          __syncthreads();
+          // G column j and h1 (scaled)
+          for (int o = threadIdx.x; o < J * R; o += kThreads) {
+            const int ii = o / R, cc = o - ii * R;
+            const double si = gs.S[ii * R + cc], sjj = gs.S[j * R + cc];
+            double2 graw = st.red[J * R + o];
+            double2 gij = (si == 0.0 || sjj == 0.0) ? make_double2(0.0, 0.0)
+                                                    : make_double2(si * sjj * graw.x, si * sjj * graw.y);
+            double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1);
+            Gc[(size_t)ii * (m + 1) + j] = gij;          // G[i][j]
+            Gc[(size_t)j * (m + 1) + ii] = cconj(gij);   // G[j][i]
+            double2 hr = st.red[o];
+            st.coef[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * hr.x, si * hr.y);  // h1
+          }
+          if (threadIdx.x < R) gs.wpre2[threadIdx.x] = st.red[2 * J * R + threadIdx.x].x;
+          __syncthreads();
+          // c = h1 + (h1 - G h1) = 2 h1 - G h1 ; coef = S c
+          for (int o = threadIdx.x; o < J * R; o += kThreads) {
+            const int ii = o / R, cc = o - ii * R;
+            const double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1);
+            double2 gh = make_double2(0.0, 0.0);
+            for (int l = 0; l < J; ++l) gh = add(gh, mul(Gc[l], st.coef[l * R + cc]));
+            double2 h1 = st.coef[o];
+            double2 cv = make_double2(2.0 * h1.x - gh.x, 2.0 * h1.y - gh.y);
+            if (!gs.active[cc]) cv = make_double2(0.0, 0.0);
+            st.hc[o] = cv;
+          }
+          __syncthreads();
+          for (int o = threadIdx.x; o < J * R; o += kThreads) {
+            const int ii = o / R, cc = o - ii * R;
+            const double si = gs.S[ii * R + cc];
+            double2 cv = st.hc[o];
+            st.coef[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * cv.x, si * cv.y);
+          }
+          bar_release(st);
+        } else {
+          bar_wait(st, gen);
+        }
+      }
+      if (timing) { unsigned long long t = gtimer(); st.stats[3] += (double)(t - tphase); tphase = t; }
+      // ======== phase C: w -= V coef, ||w||^2 -> Givens ========
+      {
+        XT* w = a.V + (long long)J * a.stride;
+        XT* s_coef = reinterpret_cast<XT*>(smem_p);
+        for (int o = threadIdx.x; o < J * R; o += kThreads) s_coef[o] = from_c<XT>(ldcg2(st.coef + o));
+        __syncthreads();
+        double n2 = 0.0;
+        for (long long base = r0 + (long long)warp * GPW * UC; base < r1;
+             base += (long long)kWarps * GPW * UC) {
+          XT acc[UC];
+          long long idx[UC];
+#pragma unroll
+          for (int u = 0; u < UC; ++u) {
+            const long long row = base + u * GPW + grp;
+            idx[u] = (lane_ok && row < r1) ? row * R + c : -1;
+            acc[u] = zero<XT>();
+          }
+#pragma unroll 2
+          for (int i = 0; i < J; ++i) {
+            const XT* vi = a.V + (long long)i * a.stride;
+            const XT cf = s_coef[i * R + c];
+#pragma unroll
+            for (int u = 0; u < UC; ++u)
+              if (idx[u] >= 0) acc[u] = fma_(vi[idx[u]], cf, acc[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < UC; ++u) {
+            if (idx[u] < 0) continue;
+            const XT wv = sub(w[idx[u]], acc[u]);
+            w[idx[u]] = wv;
+            n2 += abs2(wv);
+          }
+        }
+        n2 = group_reduce<R>(n2, grp);
+        if (grp == 0 && lane_ok) s_w2[warp][c] = n2;
+        __syncthreads();
+        if (threadIdx.x < R) {
+          double t = 0.0;
+          for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
+          mypart[2 * threadIdx.x] = t;
+          mypart[2 * threadIdx.x + 1] = 0.0;
+        }
+        if (bar_arrive(st, gen)) {
+          reduce_partials(gs.part, pstride, gridDim.x, R, st.red);
+          __syncthreads();
+          if (threadIdx.x < R) {
+            const int cc = threadIdx.x;
+            if (gs.active[cc]) {
+              const double hn = sqrt(st.red[cc].x);
+              double2* col = gs.H + ((size_t)cc * m + j) * (m + 1);
+              for (int ii = 0; ii <= j; ++ii) col[ii] = st.hc[ii * R + cc];
+              double* csv = gs.cs + (size_t)cc * m;
+              double2* snv = gs.sn + (size_t)cc * m;
+              for (int ii = 0; ii < j; ++ii) {
+                double2 x0 = col[ii], x1 = col[ii + 1];
+                const double ci = csv[ii];
+                const double2 si = snv[ii];
+                col[ii] = add(scal(ci, x0), mul(si, x1));
+                col[ii + 1] = sub(scal(ci, x1), mul(cconj(si), x0));
+              }
+              double cj; double2 sjv, rj;
+              givens(col[j], make_double2(hn, 0.0), cj, sjv, rj);
+              csv[j] = cj; snv[j] = sjv;
+              col[j] = rj;
+              col[j + 1] = make_double2(0.0, 0.0);
+              double2* gv = gs.g + (size_t)cc * (m + 1);
+              const double2 gj = gv[j];
+              const double2 gn = mul(cconj(sjv), gj);
+              gv[j + 1] = make_double2(-gn.x, -gn.y);
+              gv[j] = scal(cj, gj);
+              const long long it = ++gs.iters[cc];
+              gs.kdim[cc] = j + 1;
+              const double est = cabs_(gv[j + 1]);
+              gs.S[(j + 1) * R + cc] = hn > 0.0 ? 1.0 / hn : 0.0;
+              bool end = (j + 1 == m) || it >= gs.maxit;
+              if (!gs.fixed) end = end || est <= gs.tol || hn <= kLucky * sqrt(gs.wpre2[cc]);
+              if (end) gs.active[cc] = 0;
+            } else {
+              gs.S[(j + 1) * R + cc] = 0.0;
+            }
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            int any = 0;
+            for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
+            *gs.any_active = any;
+            *gs.j = j + 1;
+            st.stats[1] += 1.0;
+            st.stats[0] += st.spmm_bytes_arn + (2.0 * J + 2.0) * (double)a.stride * sizeof(XT);
+          }
+          __syncthreads();
+          if (*gs.any_active == 0) {
+            // cycle end: back substitution (as k_trisolve)
+            if (threadIdx.x < R) {
+              const int cc = threadIdx.x;
+              const int k = gs.kdim[cc];
+              const double2* Hc = gs.H + (size_t)cc * m * (m + 1);
+              const double2* gv = gs.g + (size_t)cc * (m + 1);
+              for (int ii = k - 1; ii >= 0; --ii) {
+                double2 acc = gv[ii];
+                for (int l = ii + 1; l < k; ++l)
+                  acc = sub(acc, mul(Hc[(size_t)l * (m + 1) + ii], gs.ycoef[l * R + cc]));
+                gs.ycoef[ii * R + cc] = cdiv(acc, Hc[(size_t)ii * (m + 1) + ii]);
+              }
+              for (int ii = 0; ii < k; ++ii) {
+                if (!FLEX) {
+                  const double s = gs.S[ii * R + cc];
+                  const double2 y = gs.ycoef[ii * R + cc];
+                  gs.ycoef[ii * R + cc] = s == 0.0 ? make_double2(0.0, 0.0) : make_double2(s * y.x, s * y.y);
+                }
+              }
+              for (int ii = k; ii < m; ++ii) gs.ycoef[ii * R + cc] = make_double2(0.0, 0.0);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+              int jx = 0;
+              for (int cc = 0; cc < R; ++cc) jx = max(jx, gs.kdim[cc]);
+              *gs.jx = jx;
+            }
+          }
+          bar_release(st);
+        } else {
+          bar_wait(st, gen);
+        }
+      }
+      if (timing) { unsigned long long t = gtimer(); st.stats[4] += (double)(t - tphase); tphase = t; }
+      if (threadIdx.x == 0) s_any = ldcgi(gs.any_active);
+      __syncthreads();
+      if (!s_any) break;
+    }
+    // ---------------- cycle end ----------------
+    // phase X: x += D^-1 sum_i V_i ycoef_i   (FGMRES: sum_i Z_i ycoef_i)
+    {
+      const int jx = ldcgi(gs.jx);
+      XT* s_coef = reinterpret_cast<XT*>(smem_p);
+      for (int o = threadIdx.x; o < jx * R; o += kThreads) s_coef[o] = from_c<XT>(ldcg2(gs.ycoef + o));
+      __syncthreads();
+      const XT* B = FLEX ? a.Z : a.V;
+      if (lane_ok && jx > 0)
+        for (long long row = row_first; row < r1; row += row_step) {
+          XT acc = zero<XT>();
+          const XT* bp = B + row * R + c;
+          for (int i = 0; i < jx; ++i) acc = fma_(bp[(long long)i * a.stride], s_coef[i * R + c], acc);
+          XT xv = a.x[row * R + c];
+          xv = FLEX ? add(xv, acc) : fma_(__ldg(a.dinv + row), acc, xv);
+          a.x[row * R + c] = xv;
+        }
+      if (bar_arrive(st, gen)) {
+        if (threadIdx.x == 0)
+          st.stats[0] += (double)(jx + 2) * (double)a.stride * sizeof(XT) +
+                         (FLEX ? 0.0 : (double)n * sizeof(XT));
+        bar_release(st);
+      } else {
+        bar_wait(st, gen);
+      }
+    }
+    if (timing) { unsigned long long t = gtimer(); st.stats[5] += (double)(t - tphase); tphase = t; }
+    // phase R: V_0 = b - Op x, ||.||^2 -> restart decision
+    {
+      double n2 = 0.0;
+      if (lane_ok)
+        for (long long row = row_first; row < r1; row += row_step) {
+          XT xi;
+          XT acc = spmm_row<XT, VT, false, SIGMA, R>(a, a.x, row, c, xi);
+          XT rv = sub(a.b[row * R + c], acc);
+          a.V[row * R + c] = rv;
+          n2 += abs2(rv);
+        }
+      n2 = group_reduce<R>(n2, grp);
+      if (grp == 0 && lane_ok) s_w2[warp][c] = n2;
+      __syncthreads();
+      if (threadIdx.x < R) {
+        double t = 0.0;
+        for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
+        mypart[2 * threadIdx.x] = t;
+        mypart[2 * threadIdx.x + 1] = 0.0;
+      }
+      if (bar_arrive(st, gen)) {
+        reduce_partials(gs.part, pstride, gridDim.x, R, st.red);
+        __syncthreads();
+        if (threadIdx.x < R) {
+          const int cc = threadIdx.x;
+          const double beta = sqrt(st.red[cc].x);
+          gs.beta[cc] = beta;
+          const bool d = gs.done[cc] || beta <= gs.tol || gs.iters[cc] >= gs.maxit;
+          gs.done[cc] = d;
+          gs.active[cc] = !d;
+          gs.kdim[cc] = 0;
+          gs.S[cc] = d ? 0.0 : 1.0 / beta;
+          gs.g[cc * (m + 1)] = make_double2(beta, 0.0);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int any = 0;
+          for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
+          *gs.any_active = any;
+          *gs.j = 0;
+          st.stats[2] += 1.0;
+          st.stats[0] += st.spmm_bytes_res;
+        }
+        bar_release(st);
+      } else {
+        bar_wait(st, gen);
+      }
+    }
+    if (timing) { unsigned long long t = gtimer(); st.stats[6] += (double)(t - tphase); tphase = t; }
+  }
+}
+
+}  // namespace sad

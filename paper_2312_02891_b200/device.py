@@ -154,10 +154,19 @@ class DeviceOperator:
             self.handle = None
 
 
-class GmresWorkspace:
-    """(restart+1) basis blocks (+ restart Z blocks for FGMRES) on the device."""
+ENGINES = {"multi": _lib.SAD_ENGINE_MULTI, "persistent": _lib.SAD_ENGINE_PERSISTENT}
 
-    def __init__(self, n, r, dtype, restart, flexible, device=0):
+
+class GmresWorkspace:
+    """(restart+1) basis blocks (+ restart Z blocks for FGMRES) on the device.
+
+    engine "persistent" (default): the whole solve is one cooperative kernel
+    with delayed-Gram CGS2 (two basis sweeps per step); "multi": one launch per
+    phase with classical CGS2 (four sweeps), host-polled between cycles.
+    ``max_sms`` caps the SMs a persistent solve occupies (0 = all)."""
+
+    def __init__(self, n, r, dtype, restart, flexible, device=0, engine="persistent",
+                 max_sms=0):
         self.n, self.r, self.dtype = n, r, dtype
         self.restart, self.flexible = restart, bool(flexible)
         self._ctx = _lib.context(device)
@@ -166,6 +175,21 @@ class GmresWorkspace:
                                           1 if flexible else 0, ctypes.byref(h))
         _lib.check(rc, self._ctx)
         self.handle = h
+        self.set_option(_lib.SAD_OPT_ENGINE, ENGINES[engine])
+        self.engine = engine
+        if max_sms:
+            self.set_option(_lib.SAD_OPT_MAX_SMS, int(max_sms))
+
+    def set_option(self, key, value):
+        _lib.check(_lib.load().sad_gmres_set_option(self.handle, int(key), int(value)),
+                   self._ctx)
+
+    def profile(self, enable):
+        """Enable/disable profiling; returns the 8 counters accumulated so far."""
+        out = np.zeros(8, dtype=np.float64)
+        _lib.check(_lib.load().sad_gmres_profile(self.handle, 1 if enable else 0,
+                                                 out.ctypes.data), self._ctx)
+        return out
 
     @property
     def nbytes(self):

@@ -91,7 +91,7 @@ class GpuGmresBinding:
 
     def __init__(self, side, base, mass, mode="iterative", precond_kind="jacobi",
                  droptol=0.1, max_iterations=1000, *, restart=50, flexible=False,
-                 device=0):
+                 device=0, engine="persistent", max_sms=0):
         if side not in ("A", "B"):
             raise ValueError("side must be 'A' or 'B'")
         if mode != "iterative":
@@ -109,6 +109,8 @@ class GpuGmresBinding:
         self.restart = int(restart)
         self.flexible = bool(flexible)
         self.device = device
+        self.engine = engine
+        self.max_sms = int(max_sms)
         adjoint = (side == "B")
         self.base = base if isinstance(base, DeviceMatrix) else DeviceMatrix(base, adjoint, device)
         self.mass = (None if mass is None else
@@ -139,7 +141,8 @@ class GpuGmresBinding:
         key = (r, dtype)
         ws = self._workspaces.get(key)
         if ws is None:
-            ws = GmresWorkspace(self.n, r, dtype, self.restart, self.flexible, self.device)
+            ws = GmresWorkspace(self.n, r, dtype, self.restart, self.flexible, self.device,
+                                engine=self.engine, max_sms=self.max_sms)
             self._workspaces[key] = ws
         return ws
 
@@ -215,7 +218,8 @@ class SolverBindings:
     B: object
 
 
-def make_gpu_bindings(problem, config, restart=50, flexible=False, device=0):
+def make_gpu_bindings(problem, config, restart=50, flexible=False, device=0,
+                      engine="persistent"):
     """GPU counterpart of make_bindings (adi.py:497-505)."""
     kind_a = getattr(config, "precond_kind_A", "jacobi")
     kind_b = getattr(config, "precond_kind_B", "jacobi")
@@ -223,7 +227,7 @@ def make_gpu_bindings(problem, config, restart=50, flexible=False, device=0):
     return SolverBindings(
         A=GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
                           max_iterations=maxit, restart=restart, flexible=flexible,
-                          device=device),
+                          device=device, engine=engine),
         B=GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
                           max_iterations=maxit, restart=restart, flexible=flexible,
-                          device=device))
+                          device=device, engine=engine))

@@ -77,9 +77,15 @@ def test_c1_dropin_bindings_host_loop():
     _check_against_golden(rep, "c1")
 
 
-def test_c1_serial_and_concurrent_sides_agree():
-    _, rep1, _ = _gpu_run("c1", concurrent=False)
-    _, rep2, _ = _gpu_run("c1", concurrent=True)
+def test_c1_multi_kernel_engine_matches_oracle():
+    sol, rep, state = _gpu_run("c1", engine="multi")
+    _check_against_golden(rep, "c1")
+
+
+@pytest.mark.parametrize("engine", ["persistent", "multi"])
+def test_c1_serial_and_concurrent_sides_agree(engine):
+    _, rep1, _ = _gpu_run("c1", concurrent=False, engine=engine)
+    _, rep2, _ = _gpu_run("c1", concurrent=True, engine=engine)
     assert [r.inner_it_A for r in rep1.records] == [r.inner_it_A for r in rep2.records]
     assert [r.scaled_res for r in rep1.records] == [r.scaled_res for r in rep2.records]
 

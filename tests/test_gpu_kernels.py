@@ -131,22 +131,27 @@ def test_gram_and_axpy(rng, r):
 
 # -- GMRES solves against the oracle ---------------------------------------------------
 
+ENGINES = [("persistent", "dcgs2"), ("multi", "cgs2")]
+
+
 def _solve_both(mat, adjoint, shift, rhs, delta, restart, flexible=False, maxit=1000,
-                precond="jacobi"):
+                precond="jacobi", engine="persistent"):
     from paper_2312_02891_b200 import GpuGmresBinding
     side = "B" if adjoint else "A"
+    orth = dict(ENGINES)[engine]
     gb = GpuGmresBinding(side, mat, None, precond_kind=precond, max_iterations=maxit,
-                         restart=restart, flexible=flexible)
+                         restart=restart, flexible=flexible, engine=engine)
     got = gb.solve(shift, rhs, delta)
     ob = orc.Binding(side, mat, None, solver="fgmres" if flexible else "gmres",
-                     max_iterations=maxit, restart=restart, precond=precond)
+                     max_iterations=maxit, restart=restart, precond=precond, orth=orth)
     want = ob.solve(shift, rhs, delta)
     return got, want
 
 
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
 @pytest.mark.parametrize("flexible", [False, True])
 @pytest.mark.parametrize("side", ["A", "B"])
-def test_gmres_c1_matches_oracle(side, flexible):
+def test_gmres_c1_matches_oracle(side, flexible, engine):
     A, B, _, _, f, g = cfgs.build_problem("c1")
     pairs, _ = cfgs.CONFIGS["c1"].load_shift_pairs()
     mat, rhs = (A, f) if side == "A" else (B, g)
@@ -154,7 +159,8 @@ def test_gmres_c1_matches_oracle(side, flexible):
         shift = beta if side == "A" else alpha
         for rel in (1e-3, 1e-8, 1e-11):
             delta = rel * np.linalg.norm(rhs)
-            got, want = _solve_both(mat, side == "B", shift, rhs, delta, 50, flexible)
+            got, want = _solve_both(mat, side == "B", shift, rhs, delta, 50, flexible,
+                                    engine=engine)
             assert np.all(np.abs(got.iterations - want.iterations) <= 2), \
                 (shift, rel, got.iterations, want.iterations)
             assert np.array_equal(got.converged, want.converged)
@@ -163,22 +169,24 @@ def test_gmres_c1_matches_oracle(side, flexible):
             assert dx <= max(10.0 * rel, 1e-9)
 
 
-@pytest.mark.parametrize("r", [2, 3, 8])
-def test_gmres_block_columns_independent(rng, r):
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
+@pytest.mark.parametrize("r", [2, 3, 5, 8])
+def test_gmres_block_columns_independent(rng, r, engine):
     """Lock-step batching keeps per-column semantics."""
     A, _, _, _, _, _ = cfgs.build_problem("c1")
     rhs = rng.standard_normal((A.shape[0], r)) * np.logspace(0, 3, r)[None, :]
     delta = 1e-7 * np.linalg.norm(rhs)
-    got, want = _solve_both(A, False, -700.0 + 50.0j, rhs, delta, 20)
+    got, want = _solve_both(A, False, -700.0 + 50.0j, rhs, delta, 20, engine=engine)
     assert np.all(np.abs(got.iterations - want.iterations) <= 2)
     assert np.array_equal(got.converged, want.converged)
 
 
-def test_gmres_known_answers(rng):
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
+def test_gmres_known_answers(rng, engine):
     from paper_2312_02891_b200 import GpuGmresBinding
     # identity: <= 1 iteration (test_krylov.py:15-20)
     b = rng.standard_normal((6, 1))
-    gb = GpuGmresBinding("A", sp.eye(6, format="csr"), None, restart=5)
+    gb = GpuGmresBinding("A", sp.eye(6, format="csr"), None, restart=5, engine=engine)
     res = gb.solve(0.0, b, 1e-12)
     assert res.total_iterations <= 1 and np.max(np.abs(res.solution - b)) < 1e-12
     # loose tolerance: 0 iterations, zero solution (test_krylov.py:27-33)
@@ -188,7 +196,7 @@ def test_gmres_known_answers(rng):
     # achieved norms are independent recomputes (test_krylov.py:45-54)
     d = rng.standard_normal((12, 12)) + 12 * np.eye(12)
     b = rng.standard_normal((12, 3))
-    gb = GpuGmresBinding("A", sp.csr_matrix(d), None, restart=10)
+    gb = GpuGmresBinding("A", sp.csr_matrix(d), None, restart=10, engine=engine)
     res = gb.solve(0.0, b, 1e-8)
     for c in range(3):
         check = np.linalg.norm(b[:, c] - d @ res.solution[:, c])
@@ -202,34 +210,39 @@ def test_gmres_known_answers(rng):
         gb.solve(0.0, np.full((12, 1), np.inf), 1e-8)
 
 
-def test_gmres_maxit_nonconvergence_flagged():
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
+def test_gmres_maxit_nonconvergence_flagged(engine):
     A, _, _, _, f, _ = cfgs.build_problem("c1")
-    got, want = _solve_both(A, False, -600.0, f, 1e-14, 5, maxit=7)
+    got, want = _solve_both(A, False, -600.0, f, 1e-14, 5, maxit=7, engine=engine)
     assert got.iterations[0] == 7 == want.iterations[0]
     assert not got.converged[0]
 
 
-def test_gmres_c2_complex_matches_oracle():
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
+def test_gmres_c2_complex_matches_oracle(engine):
     A, B, _, _, f, g = cfgs.build_problem("c2")
     pairs, _ = cfgs.CONFIGS["c2"].load_shift_pairs()
     alpha, beta = pairs[0]
     for mat, adjoint, shift, rhs in ((A, False, beta, f), (B, True, alpha, g)):
         delta = 1e-9 * np.linalg.norm(rhs)
-        got, want = _solve_both(mat, adjoint, shift, rhs, delta, 30, flexible=True)
+        got, want = _solve_both(mat, adjoint, shift, rhs, delta, 30, flexible=True,
+                                engine=engine)
         assert np.all(np.abs(got.iterations - want.iterations) <= 2)
         assert np.all(got.converged)
 
 
-def test_gmres_fixed_steps_residual_identity(rng):
-    """Fixed-step mode (config 4 path): after m steps, the recomputed true
-    residual equals the GMRES least-squares residual |g_m| (Arnoldi identity)."""
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
+def test_gmres_fixed_steps_match_oracle(rng, engine):
+    """Fixed-step mode (config 4 path): the true residual after 40 steps
+    matches the oracle's (same Krylov space, same least-squares solution)."""
     from paper_2312_02891_b200 import GpuGmresBinding
     A = cfgs.convdiff_fd(2, 128, (100.0, 100.0))
     rhs = rng.standard_normal((A.shape[0], 8))
-    gb = GpuGmresBinding("A", A, None, restart=40)
+    gb = GpuGmresBinding("A", A, None, restart=40, engine=engine)
     out = gb.solve_device(-5000.0, torch.from_numpy(rhs).cuda(), 1.0, fixed_steps=40)
     assert np.all(out.iterations == 40)
-    ob = orc.Binding("A", A, None, solver="gmres", restart=40, max_iterations=40)
+    ob = orc.Binding("A", A, None, solver="gmres", restart=40, max_iterations=40,
+                     orth=dict(ENGINES)[engine])
     want = ob.solve(-5000.0, rhs, 1e-300 * 8)
     rel = np.abs(out.achieved_residual_norms - want.achieved_residual_norms) / want.achieved_residual_norms
     assert np.all(rel < 1e-6), rel
