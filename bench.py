@@ -343,7 +343,8 @@ def run_ours_c2(args, dist):
 
 
 def run_ours_c4(args, dist):
-    """Inner-solve microbenchmark (config 4): 100 fixed GMRES steps, r=8."""
+    """Inner-solve microbenchmark (config 4): shifted SpMM GB/s on the r=8 block
+    (metric), plus 100 fixed GMRES steps through the persistent engine."""
     import torch
     from paper_2312_02891_b200 import GpuGmresBinding, _lib
     from paper_2312_02891_b200 import configs as cfgs
@@ -352,51 +353,65 @@ def run_ours_c4(args, dist):
     lib = _lib.load()
     n0 = args.c4_n0
     A, X = cfgs.build_c4(n0=n0, r=8, seed=0)
-    # shift alpha = 0.1 * lambda_max estimate; Gershgorin bound of the stencil
-    lam = -abs(A.diagonal()).max() * 2.0
-    shift = 0.1 * lam
+    # alpha = 0.1 * lambda_max estimate (Gershgorin bound of the stencil, negative)
+    shift = 0.1 * (-abs(A.diagonal()).max() * 2.0)
     steps = args.c4_steps
     gb = GpuGmresBinding("A", A, None, precond_kind="jacobi", restart=steps, device=dev)
     rhs = torch.from_numpy(X).cuda()
     x = torch.empty_like(rhs)
     res = torch.empty_like(rhs)
     op = gb.operator(shift)
-    ws = gb.workspace(8, _lib.SAD_F64)
+    n, r = A.shape[0], 8
+    blk = n * r * 8
+    spmm_b = A.nnz * 12 + 4 * (n + 1) + 2 * blk
+    # --- shifted SpMM (the metric): K timed launches, L2 flushed in between ---
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    y = torch.empty_like(rhs)
     for _ in range(args.warmup):
-        ws.fixed(op, rhs, x, res, steps)
+        op.apply(rhs, y)
     clocks = Clocks(dev)
     dist.barrier()
     torch.cuda.synchronize()
     l0 = lib.sad_kernel_launches()
     clocks.start()
-    tims = np.zeros(4)
-    t0 = time.perf_counter()
+    ms = []
     for _ in range(args.steps):
-        _, tm = ws.fixed(op, rhs, x, res, steps, timed=True)
-        tims += tm
-    wall = time.perf_counter() - t0
-    ck = clocks.stop()
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        op.apply(rhs, y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    dist.barrier()
     launches = lib.sad_kernel_launches() - l0
-    n, r = A.shape[0], 8
-    blk = n * r * 8
-    spmm_b = A.nnz * 12 + 4 * (n + 1) + 2 * blk + n * 8
-    orth_b = sum((4 * (j + 1) + 6) * blk for j in range(steps))
-    spmm_gbs = args.steps * steps * spmm_b / (tims[0] * 1e-3) / 1e9
-    orth_gbs = args.steps * orth_b / (tims[1] * 1e-3) / 1e9
+    spmm_ms = statistics.mean(ms)
+    spmm_gbs = spmm_b / (spmm_ms * 1e-3) / 1e9
+    value = spmm_gbs * dist.world
+    # --- the inner solve: 100 fixed GMRES steps, one persistent launch ---
+    ws = gb.workspace(8, _lib.SAD_F64)
+    ws.fixed(op, rhs, x, res, steps)
+    _, tm = ws.fixed(op, rhs, x, res, steps, timed=True)
+    ck = clocks.stop()
     peak, peak_kind = hbm_peak()
-    line = {"metric": "inner SpMM GB/s", "value": spmm_gbs, "unit": "GB/s",
+    solve_gbs = tm[3] / (tm[0] * 1e-3) / 1e9
+    line = {"metric": "inner SpMM GB/s", "value": value, "unit": "GB/s",
             "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * wall / args.steps, "higher_is_better": True,
+            "ms_per_step": spmm_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"config 4: {n0}^2 conv-diff, r=8, "
-                                                        f"{steps} fixed GMRES steps",
-                                            "n": n, "nnz": int(A.nnz)},
+                                                        f"shifted SpMM + {steps} fixed GMRES steps",
+                                            "n": n, "nnz": int(A.nnz),
+                                            "l2": "flushed between timed SpMMs"},
             "roofline": {"bound": "hbm", "achieved": spmm_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": spmm_gbs / peak, "traffic": None, "kernel": "shifted_spmm",
-                         "peak_kind": peak_kind},
-            "kernels": {"spmm_ms": tims[0], "orth_ms": tims[1], "orth_gbs": orth_gbs,
-                        "orth_frac": orth_gbs / peak, "cycle_end_ms": tims[2],
-                        "init_ms": tims[3]},
+                         "frac": spmm_gbs / peak, "traffic": None, "kernel": "k_spmm",
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": spmm_b},
+            "inner_solve": {"kernel": "k_gmres_persistent", "steps": steps,
+                            "kernel_ms": tm[0], "phaseA_ms": tm[1], "phaseC_ms": tm[2],
+                            "algorithmic_bytes": tm[3], "gbs": solve_gbs,
+                            "frac": solve_gbs / peak,
+                            "iterations_per_s": steps * r / (tm[0] * 1e-3)},
             "gpu_launches": int(launches), "clocks": ck}
     return line if dist.rank == 0 else None
 

@@ -202,8 +202,9 @@ __device__ __forceinline__ XT spmm_row(const PArgs<XT>& a, const XT* x, long lon
 template <typename XT, typename VT, int R, bool PRE, bool SIGMA, bool FLEX>
 __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   constexpr int GPW = 32 / R;
-  constexpr int UA = (R <= 2) ? 8 : 4;   // rows per lane per phase-A tile
-  constexpr int UC = (R <= 2) ? 8 : 4;   // rows per lane per phase-C tile
+  constexpr int UA = (R <= 4) ? 4 : 2;   // rows per lane per phase-A tile
+  constexpr int UC = 2;                  // rows per lane per phase-C tile
+  constexpr int IB = 4;                  // basis blocks per phase-A round
   extern __shared__ double smem_p[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / R, c = lane - grp * R;
@@ -302,49 +303,64 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         for (int o = threadIdx.x; o < 2 * J * kWarps * R; o += kThreads) s_acc[o] = zero<XT>();
         double w2 = 0.0;
         __syncthreads();
-        for (long long base = r0 + (long long)warp * GPW * UA; base < r1;
-             base += (long long)kWarps * GPW * UA) {
+        // rows of a block-tile are dealt to the warps GPW at a time (u-major), so
+        // every warp gets work even when the block owns few rows; for fixed u a
+        // warp reads GPW consecutive rows = 32 consecutive elements (coalesced)
+        for (long long base = r0; base < r1; base += (long long)kWarps * GPW * UA) {
           // warp-uniform loop: the shuffles below need every lane present
           XT wv[UA], xv[UA];
           long long idx[UA];
 #pragma unroll
           for (int u = 0; u < UA; ++u) {
-            const long long row = base + u * GPW + grp;
-            const bool ok = lane_ok && row < r1;
-            idx[u] = ok ? row * R + c : -1;
-            wv[u] = zero<XT>();
-            xv[u] = zero<XT>();
-            if (ok) {
-              XT xi;
-              XT acc = spmm_row<XT, VT, PRE, SIGMA, R>(a, vj, row, c, xi);
-              wv[u] = sscal(sj, acc);
-              xv[u] = xi;
+            const long long row = base + ((long long)u * kWarps + warp) * GPW + grp;
+            idx[u] = (lane_ok && row < r1) ? row * R + c : -1;
+          }
+          spmm_rows<XT, VT, PRE, SIGMA, R, UA>(a.rowptr, a.colidx,
+                                               reinterpret_cast<const VT*>(a.vals), a.dinv,
+                                               a.sigma, vj, idx, c, wv, xv);
+#pragma unroll
+          for (int u = 0; u < UA; ++u) {
+            if (idx[u] >= 0) {
+              wv[u] = sscal(sj, wv[u]);
               w[idx[u]] = wv[u];
               if (FLEX) {
-                XT zi = PRE ? mul(__ldg(a.dinv + row), xi) : xi;
+                XT zi = PRE ? mul(__ldg(a.dinv + idx[u] / R), xv[u]) : xv[u];
                 a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
               }
               w2 += abs2(wv[u]);
             }
           }
-          for (int i = 0; i < J; ++i) {
-            const XT* vi = a.V + (long long)i * a.stride;
-            XT ph = zero<XT>(), pg = zero<XT>();
+          for (int i0 = 0; i0 < J; i0 += IB) {
+            // IB basis blocks per round: IB*UA independent loads in flight
+            XT ph[IB], pg[IB];
 #pragma unroll
-            for (int u = 0; u < UA; ++u) {
-              if (idx[u] >= 0) {
-                const XT v = vi[idx[u]];
-                ph = cfma(v, wv[u], ph);
-                pg = cfma(v, xv[u], pg);
+            for (int ib = 0; ib < IB; ++ib) { ph[ib] = zero<XT>(); pg[ib] = zero<XT>(); }
+#pragma unroll
+            for (int ib = 0; ib < IB; ++ib) {
+              if (i0 + ib < J) {
+                const XT* vi = a.V + (long long)(i0 + ib) * a.stride;
+#pragma unroll
+                for (int u = 0; u < UA; ++u) {
+                  if (idx[u] >= 0) {
+                    const XT v = vi[idx[u]];
+                    ph[ib] = cfma(v, wv[u], ph[ib]);
+                    pg[ib] = cfma(v, xv[u], pg[ib]);
+                  }
+                }
               }
             }
-            ph = group_reduce<R>(ph, grp);
-            pg = group_reduce<R>(pg, grp);
-            if (grp == 0 && lane_ok) {
-              XT* s0 = s_acc + ((size_t)i * kWarps + warp) * R + c;
-              *s0 = add(*s0, ph);
-              XT* s1 = s_acc + ((size_t)(J + i) * kWarps + warp) * R + c;
-              *s1 = add(*s1, pg);
+#pragma unroll
+            for (int ib = 0; ib < IB; ++ib) {
+              if (i0 + ib < J) {
+                const XT h = group_reduce<R>(ph[ib], grp);
+                const XT gq = group_reduce<R>(pg[ib], grp);
+                if (grp == 0 && lane_ok) {
+                  XT* s0 = s_acc + ((size_t)(i0 + ib) * kWarps + warp) * R + c;
+                  *s0 = add(*s0, h);
+                  XT* s1 = s_acc + ((size_t)(J + i0 + ib) * kWarps + warp) * R + c;
+                  *s1 = add(*s1, gq);
+                }
+              }
             }
           }
         }
@@ -415,17 +431,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         for (int o = threadIdx.x; o < J * R; o += kThreads) s_coef[o] = from_c<XT>(ldcg2(st.coef + o));
         __syncthreads();
         double n2 = 0.0;
-        for (long long base = r0 + (long long)warp * GPW * UC; base < r1;
-             base += (long long)kWarps * GPW * UC) {
+        for (long long base = r0; base < r1; base += (long long)kWarps * GPW * UC) {
           XT acc[UC];
           long long idx[UC];
 #pragma unroll
           for (int u = 0; u < UC; ++u) {
-            const long long row = base + u * GPW + grp;
+            const long long row = base + ((long long)u * kWarps + warp) * GPW + grp;
             idx[u] = (lane_ok && row < r1) ? row * R + c : -1;
             acc[u] = zero<XT>();
           }
-#pragma unroll 2
+#pragma unroll 8
           for (int i = 0; i < J; ++i) {
             const XT* vi = a.V + (long long)i * a.stride;
             const XT cf = s_coef[i * R + c];
@@ -568,14 +583,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
     // phase R: V_0 = b - Op x, ||.||^2 -> restart decision
     {
       double n2 = 0.0;
-      if (lane_ok)
-        for (long long row = row_first; row < r1; row += row_step) {
-          XT xi;
-          XT acc = spmm_row<XT, VT, false, SIGMA, R>(a, a.x, row, c, xi);
-          XT rv = sub(a.b[row * R + c], acc);
-          a.V[row * R + c] = rv;
+      for (long long base = r0; base < r1; base += (long long)kWarps * GPW * UA) {
+        long long idx[UA];
+        XT acc[UA], xi[UA];
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          const long long row = base + ((long long)u * kWarps + warp) * GPW + grp;
+          idx[u] = (lane_ok && row < r1) ? row * R + c : -1;
+        }
+        spmm_rows<XT, VT, false, SIGMA, R, UA>(a.rowptr, a.colidx,
+                                               reinterpret_cast<const VT*>(a.vals), a.dinv,
+                                               a.sigma, a.x, idx, c, acc, xi);
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          if (idx[u] < 0) continue;
+          const XT rv = sub(a.b[idx[u]], acc[u]);
+          a.V[idx[u]] = rv;
           n2 += abs2(rv);
         }
+      }
       n2 = group_reduce<R>(n2, grp);
       if (grp == 0 && lane_ok) s_w2[warp][c] = n2;
       __syncthreads();
