@@ -626,6 +626,8 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
     return set_err(ctx, SAD_ENOMEM, "FGMRES Z allocation failed");
   }
   ws->max_blocks = ctx->nsm * 8;
+  // [max_blocks][pstride] doubles for the multi engine; the persistent engine
+  // uses the same buffer output-major: [(2(m+1)+1) r][max_blocks] complex
   ws->pstride = 2 * (2 * (m + 1) * r + r) + 8;
   size_t sb = 0;
   sb += 16 * 8;                              // j, any_active, jx, ticket, seqs
@@ -958,6 +960,7 @@ static cudaError_t coop_launch_t(PArgs<XT> a, sad_gmres* ws, cudaStream_t s, siz
   grid = std::max(1LL, std::min(grid, (long long)nb * sms));
   grid = std::min(grid, (long long)ws->max_blocks);
   a.rows_per_block = (a.n + grid - 1) / grid;
+  a.pT = ws->max_blocks;
   void* args[] = {(void*)&a};
   e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
   COUNT_LAUNCH(1);

@@ -54,6 +54,7 @@ struct PArgs {
   XT* Z;
   long long stride;      // n*R elements per basis block
   long long rows_per_block;
+  int pT;                // block stride of the output-major partials
   PState st;
 };
 
@@ -116,84 +117,29 @@ __device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
   __threadfence();
 }
 
-// Deterministic reduction of per-block partials: out[o] = sum_b part[b][o],
-// o < nout (complex), using all threads of the (last) block.
-__device__ void reduce_partials(const double* part, int pstride, int nblocks, int nout,
-                                double2* out) {
-  __shared__ double2 s_red[kThreads];
-  int teams = nout >= kThreads ? 1 : kThreads / nout;
-  for (int base = 0; base < nout; base += kThreads / teams) {
-    const int t = threadIdx.x;
-    const int o = base + t / teams;
-    const int lane_in = t % teams;
+// Deterministic reduction of per-block partials stored OUTPUT-MAJOR:
+// partT[o * pT + b] (complex).  One warp per output: lane l sums blocks
+// l, l+32, ... (coalesced, independent loads), then a fixed shuffle tree.
+__device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int nout,
+                                  double2* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = warp; o < nout; o += kWarps) {
+    const double2* p = partT + (size_t)o * pT;
     double2 acc = make_double2(0.0, 0.0);
-    if (o < nout && t / teams < kThreads / teams) {
-      int b = lane_in;
-      for (; b + 3 * teams < nblocks; b += 4 * teams) {
-        const double* p0 = part + (size_t)b * pstride + 2 * o;
-        const double* p1 = p0 + (size_t)teams * pstride;
-        const double* p2 = p1 + (size_t)teams * pstride;
-        const double* p3 = p2 + (size_t)teams * pstride;
-        double a0 = __ldcg(p0), a1 = __ldcg(p0 + 1), b0 = __ldcg(p1), b1 = __ldcg(p1 + 1);
-        double c0 = __ldcg(p2), c1 = __ldcg(p2 + 1), d0 = __ldcg(p3), d1 = __ldcg(p3 + 1);
-        acc.x += a0; acc.y += a1;
-        acc.x += b0; acc.y += b1;
-        acc.x += c0; acc.y += c1;
-        acc.x += d0; acc.y += d1;
-      }
-      for (; b < nblocks; b += teams) {
-        const double* p0 = part + (size_t)b * pstride + 2 * o;
-        acc.x += __ldcg(p0);
-        acc.y += __ldcg(p0 + 1);
-      }
+    int b = lane;
+    for (; b + 96 < nblocks; b += 128) {
+      const double2 v0 = __ldcg(p + b), v1 = __ldcg(p + b + 32);
+      const double2 v2 = __ldcg(p + b + 64), v3 = __ldcg(p + b + 96);
+      acc = add(acc, v0);
+      acc = add(acc, v1);
+      acc = add(acc, v2);
+      acc = add(acc, v3);
     }
-    s_red[t] = acc;
-    __syncthreads();
-    if (lane_in == 0 && o < nout && t / teams < kThreads / teams) {
-      double2 sum = s_red[t];
-      for (int q = 1; q < teams; ++q) sum = add(sum, s_red[t + q]);
-      out[o] = sum;
-    }
-    __syncthreads();
+    for (; b < nblocks; b += 32) acc = add(acc, __ldcg(p + b));
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc = add(acc, shfl_down(acc, s));
+    if (lane == 0) out[o] = acc;
   }
-}
-
-// ----------------------------------------------------------------------------
-// row kernels shared by the phases
-// ----------------------------------------------------------------------------
-template <typename XT, typename VT, bool PRE, bool SIGMA, int R>
-__device__ __forceinline__ XT spmm_row(const PArgs<XT>& a, const XT* x, long long row,
-                                       int c, XT& xi_out) {
-  const VT* vals = reinterpret_cast<const VT*>(a.vals);
-  const int k0 = __ldg(a.rowptr + row), k1 = __ldg(a.rowptr + row + 1);
-  XT acc = zero<XT>();
-  int k = k0;
-  for (; k + 1 < k1; k += 2) {
-    const int c0 = __ldg(a.colidx + k), c1 = __ldg(a.colidx + k + 1);
-    const VT v0 = __ldg(vals + k), v1 = __ldg(vals + k + 1);
-    XT x0 = x[(long long)c0 * R + c];
-    XT x1 = x[(long long)c1 * R + c];
-    if (PRE) {
-      x0 = mul(__ldg(a.dinv + c0), x0);
-      x1 = mul(__ldg(a.dinv + c1), x1);
-    }
-    acc = fma_(v0, x0, acc);
-    acc = fma_(v1, x1, acc);
-  }
-  if (k < k1) {
-    const int c0 = __ldg(a.colidx + k);
-    const VT v0 = __ldg(vals + k);
-    XT x0 = x[(long long)c0 * R + c];
-    if (PRE) x0 = mul(__ldg(a.dinv + c0), x0);
-    acc = fma_(v0, x0, acc);
-  }
-  XT xi = x[row * R + c];
-  xi_out = xi;
-  if (SIGMA) {
-    XT xs = PRE ? mul(__ldg(a.dinv + row), xi) : xi;
-    acc = fma_(from_c<XT>(a.sigma), xs, acc);
-  }
-  return acc;
 }
 
 // ----------------------------------------------------------------------------
@@ -202,7 +148,7 @@ __device__ __forceinline__ XT spmm_row(const PArgs<XT>& a, const XT* x, long lon
 template <typename XT, typename VT, int R, bool PRE, bool SIGMA, bool FLEX>
 __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   constexpr int GPW = 32 / R;
-  constexpr int UA = (R <= 4) ? 4 : 2;   // rows per lane per phase-A tile
+  constexpr int UA = sizeof(XT) == 8 ? 8 : 4;   // rows per lane per phase-A tile
   constexpr int UC = 2;                  // rows per lane per phase-C tile
   constexpr int IB = 4;                  // basis blocks per phase-A round
   extern __shared__ double smem_p[];
@@ -218,8 +164,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   // rows owned by this lane: r0 + warp*GPW + grp + q*kWarps*GPW
   const long long row_step = (long long)kWarps * GPW;
   const long long row_first = r0 + warp * GPW + grp;
-  const int pstride = gs.pstride;
-  double* mypart = gs.part + (size_t)blockIdx.x * pstride;
+  const int pT = a.pT;
+  double2* partT = reinterpret_cast<double2*>(gs.part);
+  auto put = [&](int o, double2 v) { partT[(size_t)o * pT + blockIdx.x] = v; };
   unsigned gen = 0;
   const bool timing = (blockIdx.x == 0 && threadIdx.x == 0);
   unsigned long long tphase = 0;
@@ -250,11 +197,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
     if (threadIdx.x < R) {
       double t = 0.0;
       for (int w = 0; w < kWarps; ++w) t += s_w2[w][threadIdx.x];
-      mypart[2 * threadIdx.x] = t;
-      mypart[2 * threadIdx.x + 1] = 0.0;
+      put(threadIdx.x, make_double2(t, 0.0));
     }
     if (bar_arrive(st, gen)) {
-      reduce_partials(gs.part, pstride, gridDim.x, R, st.red);
+      reduce_partials_T(partT, pT, gridDim.x, R, st.red);
       __syncthreads();
       __shared__ double s_n2[8];
       if (threadIdx.x < R) s_n2[threadIdx.x] = st.red[threadIdx.x].x;
@@ -371,19 +317,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           const int ii = o / R, cc = o - ii * R;
           XT t = zero<XT>();
           for (int wq = 0; wq < kWarps; ++wq) t = add(t, s_acc[((size_t)ii * kWarps + wq) * R + cc]);
-          const double2 tc = to_c(t);
-          mypart[2 * o] = tc.x;
-          mypart[2 * o + 1] = tc.y;
+          put(o, to_c(t));
         }
         if (threadIdx.x < R) {
           double t = 0.0;
           for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
-          mypart[2 * (2 * J * R + threadIdx.x)] = t;
-          mypart[2 * (2 * J * R + threadIdx.x) + 1] = 0.0;
+          put(2 * J * R + threadIdx.x, make_double2(t, 0.0));
         }
         if (bar_arrive(st, gen)) {
           const int nout = 2 * J * R + R;
-          reduce_partials(gs.part, pstride, gridDim.x, nout, st.red);
+          reduce_partials_T(partT, pT, gridDim.x, nout, st.red);
           __syncthreads();
           // G column j and h1 (scaled)
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
@@ -462,11 +405,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         if (threadIdx.x < R) {
           double t = 0.0;
           for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
-          mypart[2 * threadIdx.x] = t;
-          mypart[2 * threadIdx.x + 1] = 0.0;
+          put(threadIdx.x, make_double2(t, 0.0));
         }
         if (bar_arrive(st, gen)) {
-          reduce_partials(gs.part, pstride, gridDim.x, R, st.red);
+          reduce_partials_T(partT, pT, gridDim.x, R, st.red);
           __syncthreads();
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
@@ -608,11 +550,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
       if (threadIdx.x < R) {
         double t = 0.0;
         for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
-        mypart[2 * threadIdx.x] = t;
-        mypart[2 * threadIdx.x + 1] = 0.0;
+        put(threadIdx.x, make_double2(t, 0.0));
       }
       if (bar_arrive(st, gen)) {
-        reduce_partials(gs.part, pstride, gridDim.x, R, st.red);
+        reduce_partials_T(partT, pT, gridDim.x, R, st.red);
         __syncthreads();
         if (threadIdx.x < R) {
           const int cc = threadIdx.x;
