@@ -1042,7 +1042,10 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 8 * sizeof(double), s));
     CK(ctx, cudaEventRecord(ws->ev[0], s));
   }
-  const size_t smem = (size_t)2 * (ws->m + 1) * kWarps * ws->R * ws->esz;
+  const size_t m1 = ws->m + 1;
+  const size_t smem = std::max({(size_t)2 * m1 * kWarps * ws->R * ws->esz,       // phase-A sums
+                                (size_t)ws->R * (m1 * 16 + ws->m * 24),          // Givens staging
+                                (size_t)kWarps * ws->m * 16});                   // back substitution
   cudaError_t e;
   if (ws->dtype == SAD_F64) e = coop_dispatch_d(make_pargs<double>(ws, op, rhs, x), ws, op, s, smem);
   else e = coop_dispatch_z(make_pargs<double2>(ws, op, rhs, x), ws, op, s, smem);

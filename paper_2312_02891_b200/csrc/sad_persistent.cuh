@@ -18,8 +18,8 @@
 // and the last block decides per column whether to restart.
 //
 // Reductions are deterministic (fixed block order, fixed trees).  Mutable
-// shared data is read after a barrier whose release is followed by
-// __threadfence() (invalidates L1), or with ld.cg.
+// shared data is read after a barrier (acquire by thread 0 + bar.sync), or
+// with ld.cg.
 #pragma once
 
 #include "sad_kernels.cuh"
@@ -71,30 +71,48 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Grid barrier with a reduction slot.  Only thread 0 of a block talks to the
+// global counters, with release/acquire semantics at gpu scope; bar.sync makes
+// the rest of the block's writes cumulative with thread 0's release, and the
+// acquire (which invalidates the SM's L1) orders every later load of the block.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.add.release.gpu.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Arrive at the grid barrier.  Returns true in exactly one block (the last to
-// arrive), which must then do the reduction and call release().
+// arrive), which must then do the reduction and call bar_release().
 __device__ __forceinline__ bool bar_arrive(const PState& st, unsigned& gen_seen) {
   __shared__ unsigned s_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    gen_seen = ld_volatile_u32(st.bar_gen);
-    __threadfence();
-    unsigned t = atomicAdd(st.bar_count, 1u);
+    gen_seen = ld_relaxed(st.bar_gen);
+    const unsigned t = atom_add_acq_rel(st.bar_count, 1u);
     s_last = (t == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
-  bool last = s_last != 0;
-  if (last) __threadfence();
-  return last;
+  return s_last != 0;
 }
 
 __device__ __forceinline__ void bar_release(const PState& st) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    *st.bar_count = 0u;
-    __threadfence();
-    atomicAdd(st.bar_gen, 1u);
+    *reinterpret_cast<volatile unsigned*>(st.bar_count) = 0u;
+    red_add_release(st.bar_gen, 1u);
   }
   __syncthreads();
 }
@@ -103,18 +121,21 @@ __device__ __forceinline__ void bar_release(const PState& st) {
 // (a hang would otherwise wedge the GPU).
 __device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
   if (threadIdx.x == 0) {
-    unsigned long long t0 = gtimer();
+    unsigned long long t0 = 0;
     unsigned spins = 0;
-    while (ld_volatile_u32(st.bar_gen) == gen_seen) {
-      if (++spins > 64) __nanosleep(64);
-      if ((spins & 1023u) == 0 && gtimer() - t0 > 20000000000ull) {
-        atomicExch(st.err, 1);
-        __trap();
+    while (ld_acquire(st.bar_gen) == gen_seen) {
+      if (++spins > 32) __nanosleep(32);
+      if ((spins & 4095u) == 0) {
+        const unsigned long long t = gtimer();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 20000000000ull) {
+          atomicExch(st.err, 1);
+          __trap();
+        }
       }
     }
   }
   __syncthreads();
-  __threadfence();
 }
 
 // Deterministic reduction of per-block partials stored OUTPUT-MAJOR:
@@ -409,25 +430,39 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         }
         if (bar_arrive(st, gen)) {
           reduce_partials_T(partT, pT, gridDim.x, R, st.red);
+          // stage the Hessenberg column and the previous rotations in smem
+          double2* s_col = reinterpret_cast<double2*>(smem_p);        // [R][m+1]
+          double2* s_sn = s_col + (size_t)R * (m + 1);                 // [R][m]
+          double* s_cs = reinterpret_cast<double*>(s_sn + (size_t)R * m);  // [R][m]
+          for (int o = threadIdx.x; o < (j + 1) * R; o += kThreads) {
+            const int ii = o / R, cc = o - ii * R;
+            s_col[cc * (m + 1) + ii] = st.hc[o];
+          }
+          for (int o = threadIdx.x; o < j * R; o += kThreads) {
+            const int cc = o / j, ii = o - cc * j;
+            s_sn[cc * m + ii] = gs.sn[(size_t)cc * m + ii];
+            s_cs[cc * m + ii] = gs.cs[(size_t)cc * m + ii];
+          }
           __syncthreads();
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
             if (gs.active[cc]) {
               const double hn = sqrt(st.red[cc].x);
-              double2* col = gs.H + ((size_t)cc * m + j) * (m + 1);
-              for (int ii = 0; ii <= j; ++ii) col[ii] = st.hc[ii * R + cc];
-              double* csv = gs.cs + (size_t)cc * m;
-              double2* snv = gs.sn + (size_t)cc * m;
+              double2* col = s_col + (size_t)cc * (m + 1);
+              const double* csv = s_cs + (size_t)cc * m;
+              const double2* snv = s_sn + (size_t)cc * m;
+              double2 x0 = col[0];
               for (int ii = 0; ii < j; ++ii) {
-                double2 x0 = col[ii], x1 = col[ii + 1];
+                const double2 x1 = col[ii + 1];
                 const double ci = csv[ii];
                 const double2 si = snv[ii];
                 col[ii] = add(scal(ci, x0), mul(si, x1));
-                col[ii + 1] = sub(scal(ci, x1), mul(cconj(si), x0));
+                x0 = sub(scal(ci, x1), mul(cconj(si), x0));
               }
               double cj; double2 sjv, rj;
-              givens(col[j], make_double2(hn, 0.0), cj, sjv, rj);
-              csv[j] = cj; snv[j] = sjv;
+              givens(x0, make_double2(hn, 0.0), cj, sjv, rj);
+              gs.cs[(size_t)cc * m + j] = cj;
+              gs.sn[(size_t)cc * m + j] = sjv;
               col[j] = rj;
               col[j + 1] = make_double2(0.0, 0.0);
               double2* gv = gs.g + (size_t)cc * (m + 1);
@@ -447,6 +482,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             }
           }
           __syncthreads();
+          // write the rotated column back (only columns that were active)
+          for (int o = threadIdx.x; o < (j + 2) * R; o += kThreads) {
+            const int cc = o / (j + 2), ii = o - cc * (j + 2);
+            if (gs.kdim[cc] == j + 1)
+              gs.H[((size_t)cc * m + j) * (m + 1) + ii] = s_col[cc * (m + 1) + ii];
+          }
+          __syncthreads();
           if (threadIdx.x == 0) {
             int any = 0;
             for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
@@ -457,26 +499,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           }
           __syncthreads();
           if (*gs.any_active == 0) {
-            // cycle end: back substitution (as k_trisolve)
-            if (threadIdx.x < R) {
-              const int cc = threadIdx.x;
+            // cycle end: back substitution, one warp per column (lanes split the
+            // inner products; fixed shuffle tree)
+            for (int cc = warp; cc < R; cc += kWarps) {
               const int k = gs.kdim[cc];
               const double2* Hc = gs.H + (size_t)cc * m * (m + 1);
               const double2* gv = gs.g + (size_t)cc * (m + 1);
+              double2* yv = reinterpret_cast<double2*>(smem_p) + (size_t)warp * m;
               for (int ii = k - 1; ii >= 0; --ii) {
-                double2 acc = gv[ii];
-                for (int l = ii + 1; l < k; ++l)
-                  acc = sub(acc, mul(Hc[(size_t)l * (m + 1) + ii], gs.ycoef[l * R + cc]));
-                gs.ycoef[ii * R + cc] = cdiv(acc, Hc[(size_t)ii * (m + 1) + ii]);
+                double2 part = make_double2(0.0, 0.0);
+                for (int l = ii + 1 + lane; l < k; l += 32)
+                  part = add(part, mul(Hc[(size_t)l * (m + 1) + ii], yv[l]));
+#pragma unroll
+                for (int sh = 16; sh > 0; sh >>= 1) part = add(part, shfl_down(part, sh));
+                if (lane == 0) yv[ii] = cdiv(sub(gv[ii], part), Hc[(size_t)ii * (m + 1) + ii]);
+                __syncwarp();
               }
-              for (int ii = 0; ii < k; ++ii) {
-                if (!FLEX) {
-                  const double s = gs.S[ii * R + cc];
-                  const double2 y = gs.ycoef[ii * R + cc];
-                  gs.ycoef[ii * R + cc] = s == 0.0 ? make_double2(0.0, 0.0) : make_double2(s * y.x, s * y.y);
+              for (int ii = lane; ii < m; ii += 32) {
+                double2 y = ii < k ? yv[ii] : make_double2(0.0, 0.0);
+                if (!FLEX && ii < k) {
+                  const double sc = gs.S[ii * R + cc];
+                  y = sc == 0.0 ? make_double2(0.0, 0.0) : make_double2(sc * y.x, sc * y.y);
                 }
+                gs.ycoef[ii * R + cc] = y;
               }
-              for (int ii = k; ii < m; ++ii) gs.ycoef[ii * R + cc] = make_double2(0.0, 0.0);
+              __syncwarp();
             }
             __syncthreads();
             if (threadIdx.x == 0) {
