@@ -235,7 +235,7 @@ def profile_pass(eng):
     for ws in wss:
         ws.profile(True)
     sol, rep, _ = eng.run()
-    tot = np.zeros(8)
+    tot = np.zeros(12)
     for ws in wss:
         tot += ws.profile(False)
     return tot, rep

@@ -149,14 +149,16 @@ int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
 
 /*
  * Profiling of sad_gmres_solve: enable=1 resets the counters; enable=0 stops.
- * stats_host[8] (may be NULL) receives the counters accumulated so far.
+ * stats_host[12] (may be NULL) receives the counters accumulated so far.
  * Multi-kernel engine (synchronous stepping with CUDA events):
  *   {spmm_ms, spmm_launches, spmm_algorithmic_bytes, orth_ms, arnoldi_steps,
  *    orth_bytes, cycle_end_ms, cycles}
  * Persistent engine (CUDA events around each cooperative launch, phase times
  * from %globaltimer in block 0):
  *   {kernel_ms, launches, algorithmic_bytes, phaseA_ms (SpMM + basis dots),
- *    arnoldi_steps, phaseC_ms (basis update), cycle_end_ms, cycles}
+ *    arnoldi_steps, phaseC_ms (basis update), cycle_end_ms, cycles,
+ *    workA_ms, workC_ms (block 0 before the barrier), finA_ms, finC_ms (the
+ *    reducing block's serial section)}
  */
 int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host);
 

@@ -105,7 +105,9 @@ struct sad_gmres {
   double* stats_dev = nullptr;
   // profiling (sad_gmres_profile): synchronous stepping with CUDA events
   int profile = 0;
+  int timers = 0;   // phase timers without event profiling (sad_gmres_fixed)
   double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double prof2[4] = {0, 0, 0, 0};   // work_A, work_C (block 0), fin_A, fin_C (last block), ms
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
@@ -642,7 +644,7 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
   sb += (size_t)r * (m + 1) * (m + 1) * 16;  // G (persistent engine)
   sb += 2 * (size_t)(m + 1) * r * 16;        // hc, coef
   sb += (size_t)(2 * (m + 1) + 1) * r * 16;  // red
-  sb += 4 * 16 + 8 * 8;                      // barrier, err, stats
+  sb += 4 * 16 + 16 * 8;                     // barrier, err, stats
   sb += 64 * 16;                             // alignment slack
   ws->state_bytes = sb;
   if (cudaMalloc(&ws->state, sb) != cudaSuccess ||
@@ -683,7 +685,7 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
   ps.bar_count = carve<unsigned>(p, 1);
   ps.bar_gen = carve<unsigned>(p, 1);
   ps.err = carve<int>(p, 1);
-  ps.stats = carve<double>(p, 8);
+  ps.stats = carve<double>(p, 16);
   ws->stats_dev = ps.stats;
   if ((size_t)(p - ws->state) > sb) {
     sad_gmres_destroy(ws);
@@ -931,10 +933,13 @@ static double spmm_bytes(const sad_gmres* ws, const sad_op* op, bool arnoldi) {
 extern "C" int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host) {
   if (!ws) return SAD_EINVAL;
   sad_ctx* ctx = ws->ctx;
-  if (stats_host)
+  if (stats_host) {
     for (int i = 0; i < 8; ++i) stats_host[i] = ws->prof[i];
+    for (int i = 0; i < 4; ++i) stats_host[8 + i] = ws->prof2[i];
+  }
   if (enable) {
     for (int i = 0; i < 8; ++i) ws->prof[i] = 0.0;
+    for (int i = 0; i < 4; ++i) ws->prof2[i] = 0.0;
     for (int i = 0; i < 3; ++i)
       if (!ws->ev[i]) CK(ctx, cudaEventCreate(&ws->ev[i]));
   }
@@ -961,6 +966,7 @@ static cudaError_t coop_launch_t(PArgs<XT> a, sad_gmres* ws, cudaStream_t s, siz
   grid = std::min(grid, (long long)ws->max_blocks);
   a.rows_per_block = (a.n + grid - 1) / grid;
   a.pT = ws->max_blocks;
+  a.prof = ws->profile || ws->timers;
   void* args[] = {(void*)&a};
   e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
   COUNT_LAUNCH(1);
@@ -1039,7 +1045,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   CK(ctx, cudaMemsetAsync(ws->pst.bar_count, 0, sizeof(unsigned), s));
   CK(ctx, cudaMemsetAsync(ws->pst.err, 0, sizeof(int), s));
   if (ws->profile) {
-    CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 8 * sizeof(double), s));
+    CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 16 * sizeof(double), s));
     CK(ctx, cudaEventRecord(ws->ev[0], s));
   }
   const size_t m1 = ws->m + 1;
@@ -1062,8 +1068,9 @@ static int persistent_collect(sad_gmres* ws, cudaStream_t s) {
   if (ws->profile) {
     float ms = 0.f;
     CK(ctx, cudaEventElapsedTime(&ms, ws->ev[0], ws->ev[1]));
-    double st[8];
+    double st[16];
     CK(ctx, cudaMemcpy(st, ws->stats_dev, sizeof(st), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; ++i) ws->prof2[i] += st[8 + i] * 1e-6;
     ws->prof[0] += ms;
     ws->prof[1] += 1;
     ws->prof[2] += st[0];
@@ -1197,10 +1204,12 @@ extern "C" int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs, void*
     if (timing_ms) {
       CK(ctx, cudaEventCreate(&e0));
       CK(ctx, cudaEventCreate(&e1));
-      CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 8 * sizeof(double), s));
+      CK(ctx, cudaMemsetAsync(ws->stats_dev, 0, 16 * sizeof(double), s));
       CK(ctx, cudaEventRecord(e0, s));
     }
+    ws->timers = timing_ms ? 1 : 0;
     int rc = persistent_run(ws, op, rhs, x, s, 0.0, steps, 1);
+    ws->timers = 0;
     if (rc) return rc;
     if (timing_ms) CK(ctx, cudaEventRecord(e1, s));
     cudaError_t e = cudaStreamSynchronize(s);
@@ -1208,7 +1217,7 @@ extern "C" int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs, void*
     if (timing_ms) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
-      double st[8];
+      double st[16];
       CK(ctx, cudaMemcpy(st, ws->stats_dev, sizeof(st), cudaMemcpyDeviceToHost));
       // {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes}
       timing_ms[0] = ms;

@@ -35,7 +35,8 @@ struct PState {
   unsigned* bar_count;
   unsigned* bar_gen;
   int* err;              // barrier timeout flag
-  double* stats;         // [8] bytes_alg, steps, cycles, t_A, t_C, t_X, t_R (ns, block 0)
+  double* stats;         // [16] bytes_alg, steps, cycles, t_A, t_C, t_X, t_R (ns, block 0),
+                         // work_A, work_C (block 0 before arrive), fin_A, fin_C (last block)
   double spmm_bytes_arn; // algorithmic bytes of one Arnoldi SpMM
   double spmm_bytes_res; // algorithmic bytes of one residual SpMM
 };
@@ -55,6 +56,7 @@ struct PArgs {
   long long stride;      // n*R elements per basis block
   long long rows_per_block;
   int pT;                // block stride of the output-major partials
+  int prof;              // record phase timers
   PState st;
 };
 
@@ -189,8 +191,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   double2* partT = reinterpret_cast<double2*>(gs.part);
   auto put = [&](int o, double2 v) { partT[(size_t)o * pT + blockIdx.x] = v; };
   unsigned gen = 0;
-  const bool timing = (blockIdx.x == 0 && threadIdx.x == 0);
+  const bool timing = (blockIdx.x == 0 && threadIdx.x == 0);   // counters kept by block 0
+  const bool prof = a.prof != 0;                                  // phase timers (profiling)
   unsigned long long tphase = 0;
+  double acc_bytes = 0.0, acc_steps = 0.0, acc_cycles = 1.0;
+  double t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // A, C, X, R, workA, workC (ns, block 0)
 
   XT* s_acc = reinterpret_cast<XT*>(smem_p);  // [2(m+1)][kWarps][R] (phase A)
   __shared__ double s_w2[kWarps][8];
@@ -244,7 +249,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
         *gs.any_active = any;
         *gs.j = 0;
-        st.stats[2] += 1.0;
       }
       bar_release(st);
     } else {
@@ -345,49 +349,72 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
           put(2 * J * R + threadIdx.x, make_double2(t, 0.0));
         }
+        if (timing && prof) t_acc[4] += (double)(gtimer() - tphase);
         if (bar_arrive(st, gen)) {
+          const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
           const int nout = 2 * J * R + R;
-          reduce_partials_T(partT, pT, gridDim.x, nout, st.red);
+          // smem: reduced sums | S | h1 | new Gram column | active flags
+          double2* s_red = reinterpret_cast<double2*>(smem_p);
+          double2* s_h1 = s_red + nout;
+          double2* s_gc = s_h1 + J * R;
+          double* s_S = reinterpret_cast<double*>(s_gc + J * R);
+          int* s_act = reinterpret_cast<int*>(s_S + J * R);
+          for (int o = threadIdx.x; o < J * R; o += kThreads) s_S[o] = gs.S[o];
+          if (threadIdx.x < R) s_act[threadIdx.x] = gs.active[threadIdx.x];
+          reduce_partials_T(partT, pT, gridDim.x, nout, s_red);
           __syncthreads();
-          // G column j and h1 (scaled)
+          // new Gram column G[:, j] and h1 = S h_raw
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
             const int ii = o / R, cc = o - ii * R;
-            const double si = gs.S[ii * R + cc], sjj = gs.S[j * R + cc];
-            double2 graw = st.red[J * R + o];
-            double2 gij = (si == 0.0 || sjj == 0.0) ? make_double2(0.0, 0.0)
-                                                    : make_double2(si * sjj * graw.x, si * sjj * graw.y);
+            const double si = s_S[o], sjj = s_S[j * R + cc];
+            const double2 graw = s_red[J * R + o];
+            const double2 gij = (si == 0.0 || sjj == 0.0)
+                                    ? make_double2(0.0, 0.0)
+                                    : make_double2(si * sjj * graw.x, si * sjj * graw.y);
+            s_gc[o] = gij;
             double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1);
             Gc[(size_t)ii * (m + 1) + j] = gij;          // G[i][j]
             Gc[(size_t)j * (m + 1) + ii] = cconj(gij);   // G[j][i]
-            double2 hr = st.red[o];
-            st.coef[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * hr.x, si * hr.y);  // h1
+            const double2 hr = s_red[o];
+            s_h1[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * hr.x, si * hr.y);
           }
-          if (threadIdx.x < R) gs.wpre2[threadIdx.x] = st.red[2 * J * R + threadIdx.x].x;
+          if (threadIdx.x < R) gs.wpre2[threadIdx.x] = s_red[2 * J * R + threadIdx.x].x;
           __syncthreads();
-          // c = h1 + (h1 - G h1) = 2 h1 - G h1 ; coef = S c
+          // c = 2 h1 - G h1 (old G entries from global, column/row j from smem);
+          // coef = S c.  Four independent partial sums per output (fixed order).
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
             const int ii = o / R, cc = o - ii * R;
-            const double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1);
-            double2 gh = make_double2(0.0, 0.0);
-            for (int l = 0; l < J; ++l) gh = add(gh, mul(Gc[l], st.coef[l * R + cc]));
-            double2 h1 = st.coef[o];
+            double2 gh0 = make_double2(0.0, 0.0), gh1 = gh0, gh2 = gh0, gh3 = gh0;
+            if (ii < j) {
+              const double2* Grow = st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1);
+              int l = 0;
+              for (; l + 3 < j; l += 4) {
+                const double2 g0 = Grow[l], g1 = Grow[l + 1], g2 = Grow[l + 2], g3 = Grow[l + 3];
+                gh0 = add(gh0, mul(g0, s_h1[l * R + cc]));
+                gh1 = add(gh1, mul(g1, s_h1[(l + 1) * R + cc]));
+                gh2 = add(gh2, mul(g2, s_h1[(l + 2) * R + cc]));
+                gh3 = add(gh3, mul(g3, s_h1[(l + 3) * R + cc]));
+              }
+              for (; l < j; ++l) gh0 = add(gh0, mul(Grow[l], s_h1[l * R + cc]));
+            } else {
+              for (int l = 0; l < j; ++l) gh0 = add(gh0, mul(cconj(s_gc[l * R + cc]), s_h1[l * R + cc]));
+            }
+            double2 gh = add(add(gh0, gh1), add(gh2, gh3));
+            gh = add(gh, mul(s_gc[ii * R + cc], s_h1[j * R + cc]));
+            const double2 h1 = s_h1[o];
             double2 cv = make_double2(2.0 * h1.x - gh.x, 2.0 * h1.y - gh.y);
-            if (!gs.active[cc]) cv = make_double2(0.0, 0.0);
+            if (!s_act[cc]) cv = make_double2(0.0, 0.0);
             st.hc[o] = cv;
-          }
-          __syncthreads();
-          for (int o = threadIdx.x; o < J * R; o += kThreads) {
-            const int ii = o / R, cc = o - ii * R;
-            const double si = gs.S[ii * R + cc];
-            double2 cv = st.hc[o];
+            const double si = s_S[o];
             st.coef[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * cv.x, si * cv.y);
           }
+          if (prof && threadIdx.x == 0) atomicAdd(st.stats + 10, (double)(gtimer() - tfin));
           bar_release(st);
         } else {
           bar_wait(st, gen);
         }
       }
-      if (timing) { unsigned long long t = gtimer(); st.stats[3] += (double)(t - tphase); tphase = t; }
+      if (timing && prof) { unsigned long long t = gtimer(); t_acc[0] += (double)(t - tphase); tphase = t; }
       // ======== phase C: w -= V coef, ||w||^2 -> Givens ========
       {
         XT* w = a.V + (long long)J * a.stride;
@@ -428,7 +455,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
           put(threadIdx.x, make_double2(t, 0.0));
         }
+        if (timing && prof) t_acc[5] += (double)(gtimer() - tphase);
         if (bar_arrive(st, gen)) {
+          const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
           reduce_partials_T(partT, pT, gridDim.x, R, st.red);
           // stage the Hessenberg column and the previous rotations in smem
           double2* s_col = reinterpret_cast<double2*>(smem_p);        // [R][m+1]
@@ -443,10 +472,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             s_sn[cc * m + ii] = gs.sn[(size_t)cc * m + ii];
             s_cs[cc * m + ii] = gs.cs[(size_t)cc * m + ii];
           }
-          __syncthreads();
+          // per-column scalars, loaded together (one round trip)
+          int act_c = 0;
+          long long it_c = 0;
+          double wpre_c = 0.0;
+          double2 gj_c = make_double2(0.0, 0.0);
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
-            if (gs.active[cc]) {
+            act_c = gs.active[cc];
+            it_c = gs.iters[cc];
+            wpre_c = gs.wpre2[cc];
+            gj_c = gs.g[(size_t)cc * (m + 1) + j];
+          }
+          __syncthreads();
+          __shared__ int s_actn[8];
+          __shared__ int s_kd[8];
+          if (threadIdx.x < R) {
+            const int cc = threadIdx.x;
+            s_actn[cc] = 0;
+            s_kd[cc] = -1;
+            if (act_c) {
               const double hn = sqrt(st.red[cc].x);
               double2* col = s_col + (size_t)cc * (m + 1);
               const double* csv = s_cs + (size_t)cc * m;
@@ -466,17 +511,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               col[j] = rj;
               col[j + 1] = make_double2(0.0, 0.0);
               double2* gv = gs.g + (size_t)cc * (m + 1);
-              const double2 gj = gv[j];
-              const double2 gn = mul(cconj(sjv), gj);
-              gv[j + 1] = make_double2(-gn.x, -gn.y);
-              gv[j] = scal(cj, gj);
-              const long long it = ++gs.iters[cc];
+              const double2 gn = mul(cconj(sjv), gj_c);
+              const double2 gnext = make_double2(-gn.x, -gn.y);
+              gv[j + 1] = gnext;
+              gv[j] = scal(cj, gj_c);
+              const long long it = it_c + 1;
+              gs.iters[cc] = it;
               gs.kdim[cc] = j + 1;
-              const double est = cabs_(gv[j + 1]);
+              s_kd[cc] = j + 1;
+              const double est = cabs_(gnext);
               gs.S[(j + 1) * R + cc] = hn > 0.0 ? 1.0 / hn : 0.0;
               bool end = (j + 1 == m) || it >= gs.maxit;
-              if (!gs.fixed) end = end || est <= gs.tol || hn <= kLucky * sqrt(gs.wpre2[cc]);
+              if (!gs.fixed) end = end || est <= gs.tol || hn <= kLucky * sqrt(wpre_c);
               if (end) gs.active[cc] = 0;
+              s_actn[cc] = end ? 0 : 1;
             } else {
               gs.S[(j + 1) * R + cc] = 0.0;
             }
@@ -485,20 +533,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           // write the rotated column back (only columns that were active)
           for (int o = threadIdx.x; o < (j + 2) * R; o += kThreads) {
             const int cc = o / (j + 2), ii = o - cc * (j + 2);
-            if (gs.kdim[cc] == j + 1)
+            if (s_kd[cc] == j + 1)
               gs.H[((size_t)cc * m + j) * (m + 1) + ii] = s_col[cc * (m + 1) + ii];
           }
-          __syncthreads();
+          int any_now = 0;
+          for (int cc = 0; cc < R; ++cc) any_now |= s_actn[cc];
           if (threadIdx.x == 0) {
-            int any = 0;
-            for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
-            *gs.any_active = any;
+            *gs.any_active = any_now;
             *gs.j = j + 1;
-            st.stats[1] += 1.0;
-            st.stats[0] += st.spmm_bytes_arn + (2.0 * J + 2.0) * (double)a.stride * sizeof(XT);
           }
           __syncthreads();
-          if (*gs.any_active == 0) {
+          if (any_now == 0) {
             // cycle end: back substitution, one warp per column (lanes split the
             // inner products; fixed shuffle tree)
             for (int cc = warp; cc < R; cc += kWarps) {
@@ -532,12 +577,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               *gs.jx = jx;
             }
           }
+          if (prof && threadIdx.x == 0) atomicAdd(st.stats + 11, (double)(gtimer() - tfin));
           bar_release(st);
         } else {
           bar_wait(st, gen);
         }
       }
-      if (timing) { unsigned long long t = gtimer(); st.stats[4] += (double)(t - tphase); tphase = t; }
+      if (timing) {
+        if (prof) {
+          unsigned long long t = gtimer();
+          t_acc[1] += (double)(t - tphase);
+          tphase = t;
+        }
+        acc_steps += 1.0;
+        acc_bytes += st.spmm_bytes_arn + (2.0 * J + 2.0) * (double)a.stride * sizeof(XT);
+      }
       if (threadIdx.x == 0) s_any = ldcgi(gs.any_active);
       __syncthreads();
       if (!s_any) break;
@@ -559,16 +613,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           xv = FLEX ? add(xv, acc) : fma_(__ldg(a.dinv + row), acc, xv);
           a.x[row * R + c] = xv;
         }
+      if (timing) acc_bytes += (double)(jx + 2) * (double)a.stride * sizeof(XT) +
+                               (FLEX ? 0.0 : (double)n * sizeof(XT));
       if (bar_arrive(st, gen)) {
-        if (threadIdx.x == 0)
-          st.stats[0] += (double)(jx + 2) * (double)a.stride * sizeof(XT) +
-                         (FLEX ? 0.0 : (double)n * sizeof(XT));
         bar_release(st);
       } else {
         bar_wait(st, gen);
       }
     }
-    if (timing) { unsigned long long t = gtimer(); st.stats[5] += (double)(t - tphase); tphase = t; }
+    if (timing && prof) { unsigned long long t = gtimer(); t_acc[2] += (double)(t - tphase); tphase = t; }
     // phase R: V_0 = b - Op x, ||.||^2 -> restart decision
     {
       double n2 = 0.0;
@@ -619,15 +672,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           for (int cc = 0; cc < R; ++cc) any |= gs.active[cc];
           *gs.any_active = any;
           *gs.j = 0;
-          st.stats[2] += 1.0;
-          st.stats[0] += st.spmm_bytes_res;
         }
         bar_release(st);
       } else {
         bar_wait(st, gen);
       }
     }
-    if (timing) { unsigned long long t = gtimer(); st.stats[6] += (double)(t - tphase); tphase = t; }
+    if (timing) {
+      if (prof) {
+        unsigned long long t = gtimer();
+        t_acc[3] += (double)(t - tphase);
+        tphase = t;
+      }
+      acc_cycles += 1.0;
+      acc_bytes += st.spmm_bytes_res;
+    }
+  }
+  if (timing) {
+    st.stats[0] += acc_bytes;
+    st.stats[1] += acc_steps;
+    st.stats[2] += acc_cycles;
+    st.stats[3] += t_acc[0];
+    st.stats[4] += t_acc[1];
+    st.stats[5] += t_acc[2];
+    st.stats[6] += t_acc[3];
+    st.stats[8] += t_acc[4];
+    st.stats[9] += t_acc[5];
   }
 }
 

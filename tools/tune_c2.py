@@ -52,7 +52,9 @@ def main():
         print(f"engine={engine} concurrent={conc} min_elems={mepth}: solve {min(ts)*1e3:.1f} ms "
               f"(steps {rep.outer_iterations}, inner {rep.sum_inner_A}/{rep.sum_inner_B}) "
               f"kernel {prof[0]:.1f} ms, {prof[2]/prof[0]/1e6:.0f} GB/s, phaseA {prof[3]:.1f} "
-              f"phaseC {prof[5]:.1f} cycle-end {prof[6]:.1f} ms, steps {int(prof[4])}", flush=True)
+              f"phaseC {prof[5]:.1f} cycle-end {prof[6]:.1f} ms, steps {int(prof[4])} | "
+              f"workA {prof[8]:.1f} workC {prof[9]:.1f} finA {prof[10]:.1f} finC {prof[11]:.1f}",
+              flush=True)
     eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                        engine="multi")
     eng.warm()
