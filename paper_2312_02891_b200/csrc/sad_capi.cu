@@ -1049,12 +1049,25 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     CK(ctx, cudaEventRecord(ws->ev[0], s));
   }
   const size_t m1 = ws->m + 1;
-  const size_t smem = std::max({(size_t)2 * m1 * kWarps * ws->R * ws->esz,       // phase-A sums
-                                (size_t)ws->R * (m1 * 16 + ws->m * 24),          // Givens staging
-                                (size_t)kWarps * ws->m * 16});                   // back substitution
+  const size_t R = ws->R;
+  // finisher-A staging: sums (2(m+1)+1)R, h1, Gram column, S, flags, old Gram block
+  const size_t finA = ((2 * m1 + 1) * R + 2 * m1 * R) * 16 + m1 * R * 8 + 8 * 4 + 64;
+  const size_t gblk = R * m1 * m1 * 16;
+  const bool g_smem = finA + gblk <= 200 * 1024;
+  size_t smem = std::max({(size_t)2 * m1 * kWarps * R * ws->esz,       // phase-A sums
+                          R * (m1 * 16 + ws->m * 24),                  // Givens staging
+                          (size_t)kWarps * ws->m * 16,                 // back substitution
+                          finA + (g_smem ? gblk : 0)});
   cudaError_t e;
-  if (ws->dtype == SAD_F64) e = coop_dispatch_d(make_pargs<double>(ws, op, rhs, x), ws, op, s, smem);
-  else e = coop_dispatch_z(make_pargs<double2>(ws, op, rhs, x), ws, op, s, smem);
+  if (ws->dtype == SAD_F64) {
+    PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
+    a.g_smem = g_smem ? 1 : 0;
+    e = coop_dispatch_d(a, ws, op, s, smem);
+  } else {
+    PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
+    a.g_smem = g_smem ? 1 : 0;
+    e = coop_dispatch_z(a, ws, op, s, smem);
+  }
   if (e != cudaSuccess)
     return set_err(ctx, SAD_ECUDA, "cooperative GMRES launch failed: %s", cudaGetErrorString(e));
   if (ws->profile) CK(ctx, cudaEventRecord(ws->ev[1], s));

@@ -57,6 +57,7 @@ struct PArgs {
   long long rows_per_block;
   int pT;                // block stride of the output-major partials
   int prof;              // record phase timers
+  int g_smem;            // stage the Gram block in shared memory (fits)
   PState st;
 };
 
@@ -146,22 +147,29 @@ __device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
 __device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int nout,
                                   double2* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = warp; o < nout; o += kWarps) {
-    const double2* p = partT + (size_t)o * pT;
-    double2 acc = make_double2(0.0, 0.0);
-    int b = lane;
-    for (; b + 96 < nblocks; b += 128) {
-      const double2 v0 = __ldcg(p + b), v1 = __ldcg(p + b + 32);
-      const double2 v2 = __ldcg(p + b + 64), v3 = __ldcg(p + b + 96);
-      acc = add(acc, v0);
-      acc = add(acc, v1);
-      acc = add(acc, v2);
-      acc = add(acc, v3);
-    }
-    for (; b < nblocks; b += 32) acc = add(acc, __ldcg(p + b));
+  constexpr int OB = 4;   // outputs in flight per warp
+  for (int o0 = warp * OB; o0 < nout; o0 += kWarps * OB) {
+    double2 acc[OB];
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) acc = add(acc, shfl_down(acc, s));
-    if (lane == 0) out[o] = acc;
+    for (int q = 0; q < OB; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int b = lane; b < nblocks; b += 64) {
+      double2 v0[OB], v1[OB];
+#pragma unroll
+      for (int q = 0; q < OB; ++q) {
+        const bool ok = o0 + q < nout;
+        const double2* p = partT + (size_t)(o0 + q) * pT;
+        v0[q] = ok ? __ldcg(p + b) : make_double2(0.0, 0.0);
+        v1[q] = (ok && b + 32 < nblocks) ? __ldcg(p + b + 32) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < OB; ++q) acc[q] = add(add(acc[q], v0[q]), v1[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < OB; ++q) {
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) acc[q] = add(acc[q], shfl_down(acc[q], s));
+      if (lane == 0 && o0 + q < nout) out[o0 + q] = acc[q];
+    }
   }
 }
 
@@ -380,13 +388,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           }
           if (threadIdx.x < R) gs.wpre2[threadIdx.x] = s_red[2 * J * R + threadIdx.x].x;
           __syncthreads();
-          // c = 2 h1 - G h1 (old G entries from global, column/row j from smem);
-          // coef = S c.  Four independent partial sums per output (fixed order).
+          // c = 2 h1 - G h1 (old G entries, column/row j from smem); coef = S c.
+          // The old G block is staged in smem with one parallel load when it
+          // fits (a.g_smem), else read from global.  Four independent partial
+          // sums per output, combined in a fixed order.
+          double2* s_G = reinterpret_cast<double2*>(
+              (reinterpret_cast<uintptr_t>(s_act + 8) + 15) & ~uintptr_t(15));
+          const bool gsm = a.g_smem != 0;
+          if (gsm) {
+            for (int o = threadIdx.x; o < R * j * j; o += kThreads) {
+              const int cc = o / (j * j), rem = o - cc * j * j, ii = rem / j, l = rem - ii * j;
+              s_G[o] = st.G[(size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1) + l];
+            }
+            __syncthreads();
+          }
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
             const int ii = o / R, cc = o - ii * R;
             double2 gh0 = make_double2(0.0, 0.0), gh1 = gh0, gh2 = gh0, gh3 = gh0;
             if (ii < j) {
-              const double2* Grow = st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1);
+              const double2* Grow = gsm ? s_G + (size_t)cc * j * j + (size_t)ii * j
+                                        : st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1);
               int l = 0;
               for (; l + 3 < j; l += 4) {
                 const double2 g0 = Grow[l], g1 = Grow[l + 1], g2 = Grow[l + 2], g3 = Grow[l + 3];
