@@ -172,6 +172,19 @@ int sad_gram(sad_ctx* ctx, int64_t n, int r, int dtype, const void* x_dev,
 int sad_axpy(sad_ctx* ctx, int64_t n, int r, int dtype, double a_re, double a_im,
              const void* x_dev, void* y_dev, void* stream);
 
+/*
+ * Fused ADI step epilogue (adi.py:518-530) on device blocks, one launch:
+ *   w += gamma * mz ;  t += conj(gamma) * cty
+ * and the six r x r Gram matrices the host tolerance logic needs, written to
+ * gram_host[6][r][r] (complex128): resA^H resA, resB^H resB, mz^H mz,
+ * cty^H cty, w^H w (updated), t^H t (updated).  nA/nB rows on the A/B side.
+ */
+int sad_adi_epilogue(sad_ctx* ctx, int64_t nA, int64_t nB, int r, int dtype,
+                     double gamma_re, double gamma_im, const void* mz_dev,
+                     const void* resA_dev, void* w_dev, const void* cty_dev,
+                     const void* resB_dev, void* t_dev, double* gram_host,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,8 @@ SIGNATURES = {
     "sad_gram": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),
     "sad_axpy": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.c_double, _c.c_double,
                             _vp, _vp, _vp]),
+    "sad_adi_epilogue": (_c.c_int, [_vp, _i64, _i64, _c.c_int, _c.c_int, _c.c_double,
+                                    _c.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 

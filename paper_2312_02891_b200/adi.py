@@ -29,8 +29,8 @@ from enum import Enum
 
 import numpy as np
 
-from .device import (DeviceMatrix, as_csr, axpy, gram, product_norm_from_grams,
-                     sigma_max_from_gram)
+from .device import (DeviceMatrix, adi_epilogue, as_csr, axpy, gram,
+                     product_norm_from_grams, sigma_max_from_gram)
 from .krylov import GpuGmresBinding, SolverBindings
 from .shifts import ShiftSequence
 
@@ -600,19 +600,18 @@ class DeviceAdi:
             gam = gamma(alpha, beta)
             Mz = z if self.Md is None else self.Md.apply(z)
             Cty = y if self.Cd is None else self.Cd.apply(y, transpose=True)
-            rA, rB = ra.block_residual_norm, rb.block_residual_norm
-            axpy(gam, Mz, w, device=self.device)
-            axpy(np.conj(gam), Cty, t, device=self.device)
-            nMz = sigma_max_from_gram(gram(Mz, device=self.device))
-            nCy = sigma_max_from_gram(gram(Cty, device=self.device))
-            u += abs(gam) * nMz * rB
-            v += abs(gam) * nCy * rA
+            # one fused launch: w += gam Mz, t += conj(gam) C^T y and the six Grams
+            G = adi_epilogue(gam, Mz, ra.residual, w, Cty, rb.residual, t, device=self.device)
+            ra.residual_gram, rb.residual_gram = G[0], G[1]
+            rA, rB = sigma_max_from_gram(G[0]), sigma_max_from_gram(G[1])
+            u += abs(gam) * sigma_max_from_gram(G[2]) * rB
+            v += abs(gam) * sigma_max_from_gram(G[3]) * rA
             zb.append(z)
             yb.append(y)
             gammas.append(gam)
             hist.append((alpha, beta))
             k_done = k
-            Gw, Gt = gram(w, device=self.device), gram(t, device=self.device)
+            Gw, Gt = G[4], G[5]
             res = product_norm_from_grams(Gw, Gt)
             report.records.append(_record(k, res / res0, dec, rA, rB, ra, rb, u, v,
                                           1000.0 * (time.perf_counter() - ts)))

@@ -22,6 +22,7 @@
 #include "../../include/sylvadi_b200.h"
 #include "sad_kernels.cuh"
 #include "sad_persistent.cuh"
+#include "sad_adi.cuh"
 
 using namespace sad;
 
@@ -36,6 +37,9 @@ struct sad_ctx {
   double2* gram_out = nullptr;
   double2* gram_host = nullptr;  // pinned
   int scratch_blocks = 0;
+  double2* epi_part = nullptr;   // fused ADI epilogue partials (lazy)
+  double2* epi_out = nullptr;
+  double2* epi_host = nullptr;   // pinned
 };
 
 struct DevCsr {
@@ -176,6 +180,9 @@ extern "C" int sad_ctx_destroy(sad_ctx* c) {
   cudaFree(c->ticket);
   cudaFree(c->gram_out);
   cudaFreeHost(c->gram_host);
+  cudaFree(c->epi_part);
+  cudaFree(c->epi_out);
+  if (c->epi_host) cudaFreeHost(c->epi_host);
   delete c;
   return SAD_OK;
 }
@@ -1346,5 +1353,70 @@ extern "C" int sad_axpy(sad_ctx* ctx, int64_t n, int r, int dtype, double are, d
     k_axpy<double2><<<grid, 256, 0, S_(stream)>>>(count, make_double2(are, aim), (const double2*)x,
                                                   (double2*)y);
   CKL(ctx);
+  return SAD_OK;
+}
+
+// -----------------------------------------------------------------------------
+// fused ADI step epilogue
+// -----------------------------------------------------------------------------
+template <typename XT>
+static void epi_launch(int R, const EpiArgs<XT>& a, cudaStream_t s) {
+  const int grid = a.gA + a.gB;
+  switch (R) {
+    case 1: k_adi_epilogue<XT, 1><<<grid, kThreads, 0, s>>>(a); break;
+    case 2: k_adi_epilogue<XT, 2><<<grid, kThreads, 0, s>>>(a); break;
+    case 3: k_adi_epilogue<XT, 3><<<grid, kThreads, 0, s>>>(a); break;
+    case 4: k_adi_epilogue<XT, 4><<<grid, kThreads, 0, s>>>(a); break;
+    case 5: k_adi_epilogue<XT, 5><<<grid, kThreads, 0, s>>>(a); break;
+    case 6: k_adi_epilogue<XT, 6><<<grid, kThreads, 0, s>>>(a); break;
+    case 7: k_adi_epilogue<XT, 7><<<grid, kThreads, 0, s>>>(a); break;
+    case 8: k_adi_epilogue<XT, 8><<<grid, kThreads, 0, s>>>(a); break;
+  }
+}
+
+extern "C" int sad_adi_epilogue(sad_ctx* ctx, int64_t nA, int64_t nB, int r, int dtype,
+                                double g_re, double g_im, const void* mz, const void* resA,
+                                void* w, const void* cty, const void* resB, void* t,
+                                double* gram_host, void* stream) {
+  if (!ctx || !mz || !resA || !w || !cty || !resB || !t || !gram_host) return SAD_EINVAL;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  if (dtype == SAD_F64 && g_im != 0.0)
+    return set_err(ctx, SAD_EINVAL, "complex step coefficient on a real block");
+  const int cap = ctx->nsm * 2;
+  const int pT = 2 * cap;
+  if (!ctx->epi_part) {
+    CK(ctx, cudaMalloc(&ctx->epi_part, (size_t)6 * 64 * pT * sizeof(double2)));
+    CK(ctx, cudaMalloc(&ctx->epi_out, 6 * 64 * sizeof(double2)));
+    CK(ctx, cudaMallocHost(&ctx->epi_host, 6 * 64 * sizeof(double2)));
+  }
+  cudaStream_t s = S_(stream);
+  auto blocks = [&](long long rows) {
+    long long g = (rows + kThreads - 1) / kThreads;
+    return (int)std::max(1LL, std::min(g, (long long)cap));
+  };
+  if (dtype == SAD_F64) {
+    EpiArgs<double> a{};
+    a.nA = nA; a.nB = nB; a.gA = blocks(nA); a.gB = blocks(nB);
+    a.gam = make_double2(g_re, g_im);
+    a.mz = (const double*)mz; a.resA = (const double*)resA; a.w = (double*)w;
+    a.cty = (const double*)cty; a.resB = (const double*)resB; a.t = (double*)t;
+    a.partT = ctx->epi_part; a.pT = pT; a.ticket = ctx->ticket + 1; a.out = ctx->epi_out;
+    epi_launch<double>(r, a, s);
+  } else {
+    EpiArgs<double2> a{};
+    a.nA = nA; a.nB = nB; a.gA = blocks(nA); a.gB = blocks(nB);
+    a.gam = make_double2(g_re, g_im);
+    a.mz = (const double2*)mz; a.resA = (const double2*)resA; a.w = (double2*)w;
+    a.cty = (const double2*)cty; a.resB = (const double2*)resB; a.t = (double2*)t;
+    a.partT = ctx->epi_part; a.pT = pT; a.ticket = ctx->ticket + 1; a.out = ctx->epi_out;
+    epi_launch<double2>(r, a, s);
+  }
+  COUNT_LAUNCH(1);
+  CKL(ctx);
+  const size_t bytes = (size_t)6 * r * r * sizeof(double2);
+  CK(ctx, cudaMemcpyAsync(ctx->epi_host, ctx->epi_out, bytes, cudaMemcpyDeviceToHost, s));
+  CK(ctx, cudaStreamSynchronize(s));
+  std::memcpy(gram_host, ctx->epi_host, bytes);
   return SAD_OK;
 }

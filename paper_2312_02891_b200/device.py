@@ -273,3 +273,20 @@ def product_norm_from_grams(Gw, Gt):
     K = half @ Gt @ half
     ev = np.linalg.eigvalsh(0.5 * (K + K.conj().T))
     return float(np.sqrt(max(ev[-1], 0.0)))
+
+
+def adi_epilogue(gam, mz, res_a, w, cty, res_b, t, device=0, stream=None):
+    """Fused ADI step epilogue: w += gam Mz, t += conj(gam) C^T y (in place) and
+    the Gram matrices [resA, resB, Mz, C^T y, w, t] (6 x r x r complex numpy)."""
+    import torch
+    gam = complex(gam)
+    r = w.shape[1]
+    dtype = _lib.SAD_F64 if w.dtype == torch.float64 else _lib.SAD_C128
+    out = np.zeros(6 * r * r, dtype=np.complex128)
+    ctx = _lib.context(device)
+    rc = _lib.load().sad_adi_epilogue(ctx, w.shape[0], t.shape[0], r, dtype, gam.real, gam.imag,
+                                      mz.data_ptr(), res_a.data_ptr(), w.data_ptr(),
+                                      cty.data_ptr(), res_b.data_ptr(), t.data_ptr(),
+                                      out.ctypes.data, current_stream_handle(stream))
+    _lib.check(rc, ctx)
+    return out.reshape(6, r, r)

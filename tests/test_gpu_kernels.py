@@ -246,3 +246,24 @@ def test_gmres_fixed_steps_match_oracle(rng, engine):
     want = ob.solve(-5000.0, rhs, 1e-300 * 8)
     rel = np.abs(out.achieved_residual_norms - want.achieved_residual_norms) / want.achieved_residual_norms
     assert np.all(rel < 1e-6), rel
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 8])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_adi_epilogue_matches_numpy(rng, r, cplx):
+    from paper_2312_02891_b200.device import adi_epilogue
+    n, m = 5003, 3001
+    def blk(rows):
+        b = rng.standard_normal((rows, r))
+        return b + 1j * rng.standard_normal((rows, r)) if cplx else b
+    mz, ra, w, cy, rb, t = blk(n), blk(n), blk(n), blk(m), blk(m), blk(m)
+    gam = (-2.5 + 0.75j) if cplx else -2.5
+    wd, td = dev(w, cplx), dev(t, cplx)
+    G = adi_epilogue(gam, dev(mz, cplx), dev(ra, cplx), wd, dev(cy, cplx), dev(rb, cplx), td)
+    w2 = w + gam * mz
+    t2 = t + np.conj(gam) * cy
+    assert np.max(np.abs(host(wd) - w2)) <= 1e-13 * np.max(np.abs(w2))
+    assert np.max(np.abs(host(td) - t2)) <= 1e-13 * np.max(np.abs(t2))
+    for k, X in enumerate((ra, rb, mz, cy, w2, t2)):
+        ref = X.conj().T @ X
+        assert np.max(np.abs(G[k] - ref)) <= 1e-12 * np.max(np.abs(ref)), k
