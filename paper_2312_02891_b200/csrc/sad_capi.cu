@@ -23,6 +23,7 @@
 #include "sad_kernels.cuh"
 #include "sad_persistent.cuh"
 #include "sad_adi.cuh"
+#include "sad_spmm_bulk.cuh"
 
 using namespace sad;
 
@@ -60,6 +61,7 @@ struct sad_csr {
 };
 
 static std::atomic<unsigned long long> g_op_uid{1};
+static int g_nsm_bulk = 148;   // SM count for the persistent-style SpMM grids
 static std::atomic<long long> g_launches{0};   // kernels launched by this library
 #define COUNT_LAUNCH(k) g_launches.fetch_add((k), std::memory_order_relaxed)
 
@@ -161,6 +163,7 @@ extern "C" int sad_ctx_create(int device, sad_ctx** out) {
     return SAD_ECUDA;
   }
   c->nsm = nsm;
+  g_nsm_bulk = nsm;
   c->scratch_blocks = nsm * 4;
   if (cudaMalloc(&c->scratch, (size_t)c->scratch_blocks * 2 * 64 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->ticket, 64) != cudaSuccess ||
@@ -215,9 +218,10 @@ static void host_transpose(long long nr, long long nc, const std::vector<int>& r
 
 static int upload_csr(sad_ctx* ctx, DevCsr& d, const std::vector<int>& rp,
                       const std::vector<int>& ci, const std::vector<double>& v) {
-  CK(ctx, cudaMalloc(&d.rowptr, rp.size() * sizeof(int)));
-  CK(ctx, cudaMalloc(&d.colidx, std::max<size_t>(ci.size(), 1) * sizeof(int)));
-  CK(ctx, cudaMalloc(&d.vals, std::max<size_t>(v.size(), 1) * sizeof(double)));
+  // +64 bytes: the TMA bulk SpMM widens its source ranges to 16-byte alignment
+  CK(ctx, cudaMalloc(&d.rowptr, rp.size() * sizeof(int) + 64));
+  CK(ctx, cudaMalloc(&d.colidx, std::max<size_t>(ci.size(), 1) * sizeof(int) + 64));
+  CK(ctx, cudaMalloc(&d.vals, std::max<size_t>(v.size(), 1) * sizeof(double) + 64));
   CK(ctx, cudaMemcpy(d.rowptr, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
   if (!ci.empty()) {
     CK(ctx, cudaMemcpy(d.colidx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -358,17 +362,17 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
       rp[i + 1] = (int)ci.size();
     }
     size_t nz = ci.size();
-    CK(ctx, cudaMalloc(&op->own_rowptr, (n + 1) * sizeof(int)));
-    CK(ctx, cudaMalloc(&op->own_colidx, std::max<size_t>(nz, 1) * sizeof(int)));
+    CK(ctx, cudaMalloc(&op->own_rowptr, (n + 1) * sizeof(int) + 64));
+    CK(ctx, cudaMalloc(&op->own_colidx, std::max<size_t>(nz, 1) * sizeof(int) + 64));
     CK(ctx, cudaMemcpy(op->own_rowptr, rp.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
     if (nz) CK(ctx, cudaMemcpy(op->own_colidx, ci.data(), nz * sizeof(int), cudaMemcpyHostToDevice));
     if (cplx) {
       std::vector<double2> vc(nz);
       for (size_t k = 0; k < nz; ++k) vc[k] = make_double2(vr[k], vi[k]);
-      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double2)));
+      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double2) + 64));
       if (nz) CK(ctx, cudaMemcpy(op->own_vals, vc.data(), nz * sizeof(double2), cudaMemcpyHostToDevice));
     } else {
-      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double)));
+      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double) + 64));
       if (nz) CK(ctx, cudaMemcpy(op->own_vals, vr.data(), nz * sizeof(double), cudaMemcpyHostToDevice));
     }
     op->rowptr = op->own_rowptr;
@@ -433,6 +437,22 @@ extern "C" int sad_op_get_dinv(const sad_op* op, double* dinv_host) {
 // -----------------------------------------------------------------------------
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
 static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
+  if (MODE == SPMM_APPLY || MODE == SPMM_RESID) {
+    // TMA-staged SpMM; grid = resident blocks (persistent over row tiles)
+    auto kern = k_spmm_bulk<XT, VT, R, MODE, PRE, SIGMA>;
+    constexpr size_t smem = bulk_smem_bytes<VT, R>();
+    static int nb = -1;
+    if (nb < 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
+      if (nb < 1) nb = 1;
+    }
+    const long long tiles = (a.n + BulkTile<R>::TR - 1) / BulkTile<R>::TR;
+    const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_nsm_bulk));
+    kern<<<g, kThreads, smem, s>>>(a);
+    COUNT_LAUNCH(1);
+    return;
+  }
   k_spmm<XT, VT, R, MODE, PRE, SIGMA><<<grid, kThreads, 0, s>>>(a);
   COUNT_LAUNCH(1);
 }
