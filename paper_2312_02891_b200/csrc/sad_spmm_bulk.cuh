@@ -59,10 +59,13 @@ struct BulkTile {
 };
 
 // bytes of dynamic smem for a (VT, R) instantiation
+__host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) & ~size_t(127); }
+template <int R> __host__ __device__ constexpr size_t bulk_ci_bytes() { return align128((size_t)BulkTile<R>::CAP * 4 + 64); }
+template <typename VT, int R> __host__ __device__ constexpr size_t bulk_v_bytes() { return align128((size_t)BulkTile<R>::CAP * sizeof(VT) + 64); }
+template <int R> __host__ __device__ constexpr size_t bulk_rp_bytes() { return align128((size_t)(BulkTile<R>::TR + 1) * 4 + 64); }
 template <typename VT, int R>
 __host__ __device__ constexpr size_t bulk_smem_bytes() {
-  return 2 * ((size_t)BulkTile<R>::CAP * 4 + 64) + 2 * ((size_t)BulkTile<R>::CAP * sizeof(VT) + 64) +
-         3 * ((size_t)(BulkTile<R>::TR + 1) * 4 + 64) + 128;
+  return 2 * bulk_ci_bytes<R>() + 2 * bulk_v_bytes<VT, R>() + 3 * bulk_rp_bytes<R>() + 128;
 }
 
 // Issue the bulk copy of `count` elements of `esz` bytes starting at element
@@ -85,15 +88,15 @@ template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
 __global__ void __launch_bounds__(kThreads) k_spmm_bulk(SpmmArgs<XT> a) {
   using T = BulkTile<R>;
   constexpr int GPW = T::GPW, U = T::U, TR = T::TR, CAP = T::CAP;
-  extern __shared__ __align__(16) unsigned char smem_b[];
+  extern __shared__ __align__(128) unsigned char smem_b[];
   // layout: ci[2][CAP+16] | vals[2][CAP+16] | rp[3][TR+1+16] | bars
   int* s_ci[2];
   VT* s_v[2];
   int* s_rp[3];
   unsigned char* p = smem_b;
-  for (int q = 0; q < 2; ++q) { s_ci[q] = reinterpret_cast<int*>(p); p += (size_t)CAP * 4 + 64; }
-  for (int q = 0; q < 2; ++q) { s_v[q] = reinterpret_cast<VT*>(p); p += (size_t)CAP * sizeof(VT) + 64; }
-  for (int q = 0; q < 3; ++q) { s_rp[q] = reinterpret_cast<int*>(p); p += (size_t)(TR + 1) * 4 + 64; }
+  for (int q = 0; q < 2; ++q) { s_ci[q] = reinterpret_cast<int*>(p); p += bulk_ci_bytes<R>(); }
+  for (int q = 0; q < 2; ++q) { s_v[q] = reinterpret_cast<VT*>(p); p += bulk_v_bytes<VT, R>(); }
+  for (int q = 0; q < 3; ++q) { s_rp[q] = reinterpret_cast<int*>(p); p += bulk_rp_bytes<R>(); }
   unsigned long long* bar_cv = reinterpret_cast<unsigned long long*>((reinterpret_cast<size_t>(p) + 15) & ~size_t(15));
   unsigned long long* bar_rp = bar_cv + 2;
   __shared__ int s_rp_off[3];
