@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -485,7 +486,32 @@ struct SpmmV {
 
 template <typename XT, int MODE>
 static int launch_spmm(const SpmmArgs<XT>& a, int R, bool vc, bool pre, bool sigma, int nsm,
-                       cudaStream_t s, int grid_cap = 0) {
+                       cudaStream_t s, int grid_cap = 0);
+
+// A real block with an even number of columns is processed as a complex block
+// of R/2 columns (16-byte loads, half the lanes per row): for a real matrix and
+// a real shift every complex product reduces to the same two real FMAs, so
+// the results are identical.
+static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, int nsm,
+                       cudaStream_t s, int mode) {
+  if (R % 2 || pre || a.sigma.y != 0.0) return false;
+  SpmmArgs<double2> z{};
+  z.n = a.n; z.rowptr = a.rowptr; z.colidx = a.colidx; z.vals = a.vals;
+  z.x = reinterpret_cast<const double2*>(a.x);
+  z.y = reinterpret_cast<double2*>(a.y);
+  z.b = reinterpret_cast<const double2*>(a.b);
+  z.sigma = a.sigma;
+  if (mode == SPMM_APPLY) launch_spmm<double2, SPMM_APPLY>(z, R / 2, false, false, sigma, nsm, s);
+  else launch_spmm<double2, SPMM_RESID>(z, R / 2, false, false, sigma, nsm, s);
+  return true;
+}
+
+template <typename XT, int MODE>
+static int launch_spmm(const SpmmArgs<XT>& a, int R, bool vc, bool pre, bool sigma, int nsm,
+                       cudaStream_t s, int grid_cap) {
+  if constexpr (std::is_same<XT, double>::value && (MODE == SPMM_APPLY || MODE == SPMM_RESID)) {
+    if (spmm_pairs(a, R, pre, sigma, nsm, s, MODE)) return SAD_OK;
+  }
   const int gpw = 32 / R;
   const int cap = grid_cap > 0 ? grid_cap : nsm * 8;
   const int grid = grid_for(a.n, kWarps * gpw, cap);

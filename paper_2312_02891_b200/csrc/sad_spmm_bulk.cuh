@@ -53,8 +53,8 @@ __device__ __forceinline__ void fence_proxy_async() {
 template <int R>
 struct BulkTile {
   static constexpr int GPW = 32 / R;
-  static constexpr int U = (256 / (kWarps * GPW)) > 0 ? (256 / (kWarps * GPW)) : 1;
-  static constexpr int TR = kWarps * GPW * U;   // rows per tile (~256)
+  static constexpr int U = (128 / (kWarps * GPW)) > 0 ? (128 / (kWarps * GPW)) : 1;
+  static constexpr int TR = kWarps * GPW * U;   // rows per tile (~128)
   static constexpr int CAP = 10 * TR;           // staged nonzeros per tile
 };
 
@@ -203,20 +203,27 @@ __global__ void __launch_bounds__(kThreads) k_spmm_bulk(SpmmArgs<XT> a) {
       XT acc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = zero<XT>();
-      for (int q = 0; q < maxlen; q += 4) {
+      constexpr int KB = (U <= 2) ? 8 : 4;     // nonzeros per row per batch
+      for (int q = 0; q < maxlen; q += KB) {
+        // all gathers of the batch are issued before the first FMA consumes one
+        XT xg[U][KB];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int u = 0; u < U; ++u) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
+          for (int t = 0; t < KB; ++t) {
+            xg[u][t] = zero<XT>();
             if (q + t < len[u]) {
-              const int kk = k0[u] + q + t;
-              const int col = ci[kk];
-              const VT v = vv[kk];
-              XT xv = x[(long long)col * R + c];
-              if (PRE) xv = mul(__ldg(a.dinv + col), xv);
-              acc[u] = fma_(v, xv, acc[u]);
+              const int col = ci[k0[u] + q + t];
+              xg[u][t] = x[(long long)col * R + c];
+              if (PRE) xg[u][t] = mul(__ldg(a.dinv + col), xg[u][t]);
             }
           }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int t = 0; t < KB; ++t)
+            if (q + t < len[u]) acc[u] = fma_(vv[k0[u] + q + t], xg[u][t], acc[u]);
         }
       }
 #pragma unroll
