@@ -445,12 +445,12 @@ static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
     static int nb = -1;
     if (nb < 0) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads + 32, smem);
       if (nb < 1) nb = 1;
     }
     const long long tiles = (a.n + BulkTile<R>::TR - 1) / BulkTile<R>::TR;
     const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_nsm_bulk));
-    kern<<<g, kThreads, smem, s>>>(a);
+    kern<<<g, kThreads + 32, smem, s>>>(a);
     COUNT_LAUNCH(1);
     return;
   }

@@ -56,131 +56,114 @@ struct BulkTile {
   static constexpr int U = (128 / (kWarps * GPW)) > 0 ? (128 / (kWarps * GPW)) : 1;
   static constexpr int TR = kWarps * GPW * U;   // rows per tile (~128)
   static constexpr int CAP = 10 * TR;           // staged nonzeros per tile
+  static constexpr int STAGES = 3;
 };
 
-// bytes of dynamic smem for a (VT, R) instantiation
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) & ~size_t(127); }
 template <int R> __host__ __device__ constexpr size_t bulk_ci_bytes() { return align128((size_t)BulkTile<R>::CAP * 4 + 64); }
 template <typename VT, int R> __host__ __device__ constexpr size_t bulk_v_bytes() { return align128((size_t)BulkTile<R>::CAP * sizeof(VT) + 64); }
 template <int R> __host__ __device__ constexpr size_t bulk_rp_bytes() { return align128((size_t)(BulkTile<R>::TR + 1) * 4 + 64); }
 template <typename VT, int R>
+__host__ __device__ constexpr size_t bulk_stage_bytes() {
+  return bulk_ci_bytes<R>() + bulk_v_bytes<VT, R>() + bulk_rp_bytes<R>();
+}
+template <typename VT, int R>
 __host__ __device__ constexpr size_t bulk_smem_bytes() {
-  return 2 * bulk_ci_bytes<R>() + 2 * bulk_v_bytes<VT, R>() + 3 * bulk_rp_bytes<R>() + 128;
+  return BulkTile<R>::STAGES * bulk_stage_bytes<VT, R>() + 256;
 }
 
-// Issue the bulk copy of `count` elements of `esz` bytes starting at element
-// `first` of `base`; the source range is widened to 16-byte alignment (arrays
-// are padded by the allocator).  Returns the element offset of `first` inside
-// the staged buffer and adds the bytes to *tx.
-__device__ __forceinline__ int bulk_range(void* dst, const void* base, long long first, long long count,
-                                          int esz, unsigned long long* bar, unsigned* tx) {
+// Byte range [a0, a1) covering elements [first, first+count) widened to 16 B.
+__device__ __forceinline__ void aligned_range(const void* base, long long first, long long count,
+                                              int esz, unsigned long long& a0, unsigned long long& a1) {
   const char* b = reinterpret_cast<const char*>(base);
-  const unsigned long long a0 = reinterpret_cast<unsigned long long>(b + first * esz) & ~15ull;
-  const unsigned long long a1 =
-      (reinterpret_cast<unsigned long long>(b + (first + count) * esz) + 15ull) & ~15ull;
-  const unsigned bytes = (unsigned)(a1 - a0);
-  if (bytes) bulk_g2s(dst, reinterpret_cast<const void*>(a0), bytes, bar);
-  *tx += bytes;
-  return (int)((reinterpret_cast<unsigned long long>(b + first * esz) - a0) / esz);
+  a0 = reinterpret_cast<unsigned long long>(b + first * esz) & ~15ull;
+  a1 = (reinterpret_cast<unsigned long long>(b + (first + count) * esz) + 15ull) & ~15ull;
 }
 
+// Warp-specialised: warps 0..7 consume tiles, warp 8 is the TMA producer.
+// full[s]: armed by the producer with the stage's byte count; empty[s]: one
+// arrival per consumer warp when it is done with the stage.
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
-__global__ void __launch_bounds__(kThreads) k_spmm_bulk(SpmmArgs<XT> a) {
+__global__ void __launch_bounds__(kThreads + 32) k_spmm_bulk(SpmmArgs<XT> a) {
   using T = BulkTile<R>;
-  constexpr int GPW = T::GPW, U = T::U, TR = T::TR, CAP = T::CAP;
+  constexpr int GPW = T::GPW, U = T::U, TR = T::TR, CAP = T::CAP, S = T::STAGES;
   extern __shared__ __align__(128) unsigned char smem_b[];
-  // layout: ci[2][CAP+16] | vals[2][CAP+16] | rp[3][TR+1+16] | bars
-  int* s_ci[2];
-  VT* s_v[2];
-  int* s_rp[3];
-  unsigned char* p = smem_b;
-  for (int q = 0; q < 2; ++q) { s_ci[q] = reinterpret_cast<int*>(p); p += bulk_ci_bytes<R>(); }
-  for (int q = 0; q < 2; ++q) { s_v[q] = reinterpret_cast<VT*>(p); p += bulk_v_bytes<VT, R>(); }
-  for (int q = 0; q < 3; ++q) { s_rp[q] = reinterpret_cast<int*>(p); p += bulk_rp_bytes<R>(); }
-  unsigned long long* bar_cv = reinterpret_cast<unsigned long long*>((reinterpret_cast<size_t>(p) + 15) & ~size_t(15));
-  unsigned long long* bar_rp = bar_cv + 2;
-  __shared__ int s_rp_off[3];
-  __shared__ int s_cv_off[2][2];   // [buf][ci offset, val offset]
-  __shared__ int s_kb[2];
-  __shared__ int s_staged[2];
+  constexpr size_t CI = bulk_ci_bytes<R>(), VB = bulk_v_bytes<VT, R>(), RB = bulk_rp_bytes<R>();
+  constexpr size_t SB = CI + VB + RB;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_b + S * SB);
+  unsigned long long* empty = full + S;
+  __shared__ int s_off[S][3];     // element offsets of the staged ranges (ci, v, rp)
+  __shared__ int s_kb[S];
+  __shared__ int s_staged[S];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = lane / R, c = lane - grp * R;
-  const bool lane_ok = grp < GPW;
   const VT* vals = reinterpret_cast<const VT*>(a.vals);
   const long long ntiles = (a.n + TR - 1) / TR;
   const long long G = gridDim.x;
   const long long K = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
-  const XT* x = a.x;
-  XT* y = a.y;
   if (threadIdx.x == 0) {
-    for (int q = 0; q < 2; ++q) mbar_init(bar_cv + q, 1);
-    for (int q = 0; q < 3; ++q) mbar_init(bar_rp + q, 1);
+    for (int q = 0; q < S; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, kWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
-  auto tile_row0 = [&](long long k) { return (blockIdx.x + k * G) * (long long)TR; };
-  auto issue_rp = [&](long long k) {
-    const long long r0 = tile_row0(k);
-    const long long cnt = min((long long)TR, a.n - r0) + 1;
-    unsigned tx = 0;
-    const int buf = (int)(k % 3);
-    // expect_tx must be armed before the bytes can land: compute the byte count first
-    const unsigned long long a0 = reinterpret_cast<unsigned long long>(a.rowptr + r0) & ~15ull;
-    const unsigned long long a1 = (reinterpret_cast<unsigned long long>(a.rowptr + r0 + cnt) + 15ull) & ~15ull;
-    mbar_expect_tx(bar_rp + buf, (unsigned)(a1 - a0));
-    s_rp_off[buf] = bulk_range(s_rp[buf], a.rowptr, r0, cnt, 4, bar_rp + buf, &tx);
-  };
-  auto issue_cv = [&](long long k) {
-    const int rb = (int)(k % 3), cb = (int)(k % 2);
-    const long long r0 = tile_row0(k);
-    const int rows = (int)min((long long)TR, a.n - r0);
-    const int* rp = s_rp[rb] + s_rp_off[rb];
-    const int kb = rp[0], ke = rp[rows];
-    s_kb[cb] = kb;
-    const int nz = ke - kb;
-    if (nz + 8 <= CAP) {
-      const unsigned long long c0 = reinterpret_cast<unsigned long long>(a.colidx + kb) & ~15ull;
-      const unsigned long long c1 = (reinterpret_cast<unsigned long long>(a.colidx + ke) + 15ull) & ~15ull;
-      const unsigned long long v0 = reinterpret_cast<unsigned long long>(vals + kb) & ~15ull;
-      const unsigned long long v1 = (reinterpret_cast<unsigned long long>(vals + ke) + 15ull) & ~15ull;
-      mbar_expect_tx(bar_cv + cb, (unsigned)((c1 - c0) + (v1 - v0)));
-      unsigned tx = 0;
-      s_cv_off[cb][0] = bulk_range(s_ci[cb], a.colidx, kb, nz, 4, bar_cv + cb, &tx);
-      s_cv_off[cb][1] = bulk_range(s_v[cb], vals, kb, nz, (int)sizeof(VT), bar_cv + cb, &tx);
-      s_staged[cb] = 1;
-    } else {
-      s_staged[cb] = 0;
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar_cv + cb)) : "memory");
-    }
-  };
-
-  if (threadIdx.x == 0 && K > 0) {
-    issue_rp(0);
-    if (K > 1) issue_rp(1);
-    mbar_wait(bar_rp + 0, 0);
-    issue_cv(0);
-  }
-  double nacc = 0.0;
-  for (long long k = 0; k < K; ++k) {
-    const int rb = (int)(k % 3), cb = (int)(k % 2);
-    if (threadIdx.x == 0) {
-      if (k + 1 < K) {
-        mbar_wait(bar_rp + (int)((k + 1) % 3), (unsigned)(((k + 1) / 3) & 1));
-        issue_cv(k + 1);
+  if (warp == kWarps) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      for (long long k = 0; k < K; ++k) {
+        const int st = (int)(k % S);
+        if (k >= S) mbar_wait(empty + st, (unsigned)(((k / S) - 1) & 1));
+        const long long r0 = (blockIdx.x + k * G) * (long long)TR;
+        const int rows = (int)min((long long)TR, a.n - r0);
+        const int kb = __ldg(a.rowptr + r0), ke = __ldg(a.rowptr + r0 + rows);
+        const int nz = ke - kb;
+        unsigned long long p0, p1, c0, c1, v0, v1;
+        aligned_range(a.rowptr, r0, rows + 1, 4, p0, p1);
+        const bool stage_cv = nz + 8 <= CAP;
+        unsigned bytes = (unsigned)(p1 - p0);
+        if (stage_cv) {
+          aligned_range(a.colidx, kb, nz, 4, c0, c1);
+          aligned_range(vals, kb, nz, (int)sizeof(VT), v0, v1);
+          bytes += (unsigned)((c1 - c0) + (v1 - v0));
+        }
+        unsigned char* base = smem_b + st * SB;
+        s_kb[st] = kb;
+        s_staged[st] = stage_cv ? 1 : 0;
+        s_off[st][2] = (int)((reinterpret_cast<unsigned long long>(a.rowptr + r0) - p0) / 4);
+        if (stage_cv) {
+          s_off[st][0] = (int)((reinterpret_cast<unsigned long long>(a.colidx + kb) - c0) / 4);
+          s_off[st][1] = (int)((reinterpret_cast<unsigned long long>(vals + kb) - v0) / sizeof(VT));
+        }
+        fence_proxy_async();
+        mbar_expect_tx(full + st, bytes);
+        bulk_g2s(base + CI + VB, reinterpret_cast<const void*>(p0), (unsigned)(p1 - p0), full + st);
+        if (stage_cv) {
+          if (c1 > c0) bulk_g2s(base, reinterpret_cast<const void*>(c0), (unsigned)(c1 - c0), full + st);
+          if (v1 > v0) bulk_g2s(base + CI, reinterpret_cast<const void*>(v0), (unsigned)(v1 - v0), full + st);
+        }
       }
-      if (k + 2 < K) issue_rp(k + 2);
     }
-    mbar_wait(bar_rp + rb, (unsigned)((k / 3) & 1));
-    mbar_wait(bar_cv + cb, (unsigned)((k / 2) & 1));
-    __syncthreads();   // s_staged / offsets written by thread 0 are visible
-    const long long r0 = tile_row0(k);
-    const int* rp = s_rp[rb] + s_rp_off[rb];
-    const bool staged = s_staged[cb] != 0;
-    const int kb = s_kb[cb];
-    const int* ci = staged ? s_ci[cb] + s_cv_off[cb][0] - kb : a.colidx;
-    const VT* vv = staged ? s_v[cb] + s_cv_off[cb][1] - kb : vals;
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int grp = lane / R, c = lane - grp * R;
+  const bool lane_ok = grp < GPW;
+  const XT* x = a.x;
+  XT* y = a.y;
+  for (long long k = 0; k < K; ++k) {
+    const int st = (int)(k % S);
+    mbar_wait(full + st, (unsigned)((k / S) & 1));
+    const unsigned char* base = smem_b + st * SB;
+    const long long r0 = (blockIdx.x + k * G) * (long long)TR;
+    const int* rp = reinterpret_cast<const int*>(base + CI + VB) + s_off[st][2];
+    const bool staged = s_staged[st] != 0;
+    const int kb = s_kb[st];
+    const int* ci = staged ? reinterpret_cast<const int*>(base) + s_off[st][0] - kb : a.colidx;
+    const VT* vv = staged ? reinterpret_cast<const VT*>(base + CI) + s_off[st][1] - kb : vals;
     if (lane_ok) {
       int k0[U], len[U];
       long long idx[U];
@@ -189,7 +172,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm_bulk(SpmmArgs<XT> a) {
       for (int u = 0; u < U; ++u) {
         const int lr = (u * kWarps + warp) * GPW + grp;
         const long long row = r0 + lr;
-        if (lr < TR && row < a.n) {
+        if (row < a.n) {
           idx[u] = row * R + c;
           k0[u] = rp[lr];
           len[u] = rp[lr + 1] - k0[u];
@@ -203,9 +186,8 @@ __global__ void __launch_bounds__(kThreads) k_spmm_bulk(SpmmArgs<XT> a) {
       XT acc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = zero<XT>();
-      constexpr int KB = (U <= 2) ? 8 : 4;     // nonzeros per row per batch
+      constexpr int KB = (U <= 2) ? 8 : 4;
       for (int q = 0; q < maxlen; q += KB) {
-        // all gathers of the batch are issued before the first FMA consumes one
         XT xg[U][KB];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -237,13 +219,11 @@ __global__ void __launch_bounds__(kThreads) k_spmm_bulk(SpmmArgs<XT> a) {
         }
         if (MODE == SPMM_RESID || MODE == SPMM_RESID_CYCLE) vres = sub(a.b[idx[u]], vres);
         y[idx[u]] = vres;
-        if (MODE == SPMM_RESID_CYCLE) nacc += abs2(vres);
       }
     }
-    __syncthreads();      // buffers of tile k are free
-    if (threadIdx.x == 0) fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + st)) : "memory");
   }
-  (void)nacc;
 }
 
 }  // namespace sad
