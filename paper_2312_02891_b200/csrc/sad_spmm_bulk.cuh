@@ -50,13 +50,25 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+#ifndef SAD_BULK_ROWS
+#define SAD_BULK_ROWS 64       // target rows per tile (tuned: tools/spmm_tune.cu)
+#endif
+#ifndef SAD_BULK_STAGES
+#define SAD_BULK_STAGES 2      // TMA pipeline depth
+#endif
+#ifndef SAD_BULK_KB
+#define SAD_BULK_KB 4          // nonzeros per row gathered per batch
+#endif
+#ifndef SAD_BULK_MINB
+#define SAD_BULK_MINB 1        // __launch_bounds__ min blocks per SM (register cap)
+#endif
 template <int R>
 struct BulkTile {
   static constexpr int GPW = 32 / R;
-  static constexpr int U = (128 / (kWarps * GPW)) > 0 ? (128 / (kWarps * GPW)) : 1;
-  static constexpr int TR = kWarps * GPW * U;   // rows per tile (~128)
+  static constexpr int U = (SAD_BULK_ROWS / (kWarps * GPW)) > 0 ? (SAD_BULK_ROWS / (kWarps * GPW)) : 1;
+  static constexpr int TR = kWarps * GPW * U;   // rows per tile
   static constexpr int CAP = 10 * TR;           // staged nonzeros per tile
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = SAD_BULK_STAGES;
 };
 
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) & ~size_t(127); }
@@ -84,7 +96,7 @@ __device__ __forceinline__ void aligned_range(const void* base, long long first,
 // full[s]: armed by the producer with the stage's byte count; empty[s]: one
 // arrival per consumer warp when it is done with the stage.
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
-__global__ void __launch_bounds__(kThreads + 32) k_spmm_bulk(SpmmArgs<XT> a) {
+__global__ void __launch_bounds__(kThreads + 32, SAD_BULK_MINB) k_spmm_bulk(SpmmArgs<XT> a) {
   using T = BulkTile<R>;
   constexpr int GPW = T::GPW, U = T::U, TR = T::TR, CAP = T::CAP, S = T::STAGES;
   extern __shared__ __align__(128) unsigned char smem_b[];
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(kThreads + 32) k_spmm_bulk(SpmmArgs<XT> a) {
       XT acc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = zero<XT>();
-      constexpr int KB = (U <= 2) ? 8 : 4;
+      constexpr int KB = SAD_BULK_KB;
       for (int q = 0; q < maxlen; q += KB) {
         XT xg[U][KB];
 #pragma unroll

@@ -1,0 +1,63 @@
+// Stand-alone tuning harness for the TMA-staged SpMM (config-4 operator).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DSAD_BULK_ROWS=.. -DSAD_BULK_STAGES=..
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <random>
+#include "../paper_2312_02891_b200/csrc/sad_spmm_bulk.cuh"
+using namespace sad;
+int main(int argc, char** argv) {
+  const int n0 = argc > 1 ? atoi(argv[1]) : 4096;
+  const long long n = (long long)n0 * n0;
+  const double h = 1.0 / (n0 + 1), w = 100.0;
+  std::vector<int> rp(n + 1), ci;
+  std::vector<double> v;
+  ci.reserve(5 * n); v.reserve(5 * n);
+  for (long long i = 0; i < n; ++i) {
+    int ix = i % n0, iy = i / n0;
+    auto push = [&](long long c, double val) { ci.push_back((int)c); v.push_back(val); };
+    if (iy > 0) push(i - n0, 1 / (h * h) + w / (2 * h));
+    if (ix > 0) push(i - 1, 1 / (h * h) + w / (2 * h));
+    push(i, -4 / (h * h));
+    if (ix < n0 - 1) push(i + 1, 1 / (h * h) - w / (2 * h));
+    if (iy < n0 - 1) push(i + n0, 1 / (h * h) - w / (2 * h));
+    rp[i + 1] = (int)ci.size();
+  }
+  const long long nnz = ci.size();
+  int *drp, *dci; double* dv; double2 *dx, *dy;
+  cudaMalloc(&drp, (n + 1) * 4 + 64); cudaMalloc(&dci, nnz * 4 + 64); cudaMalloc(&dv, nnz * 8 + 64);
+  cudaMalloc(&dx, n * 4 * 16); cudaMalloc(&dy, n * 4 * 16);
+  cudaMemcpy(drp, rp.data(), (n + 1) * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dci, ci.data(), nnz * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dv, v.data(), nnz * 8, cudaMemcpyHostToDevice);
+  cudaMemset(dx, 0, n * 64);
+  SpmmArgs<double2> a{};
+  a.n = n; a.rowptr = drp; a.colidx = dci; a.vals = dv; a.x = dx; a.y = dy;
+  a.sigma = make_double2(-1e6, 0.0);
+  auto kern = k_spmm_bulk<double2, double, 4, SPMM_APPLY, false, true>;
+  constexpr size_t smem = bulk_smem_bytes<double, 4>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int nb = 0, nsm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads + 32, smem);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const long long tiles = (n + BulkTile<4>::TR - 1) / BulkTile<4>::TR;
+  int grid = (int)std::min(tiles, (long long)nb * nsm);
+  void* flush; cudaMalloc(&flush, 512 << 20);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e9, sum = 0;
+  for (int it = 0; it < 12; ++it) {
+    cudaMemset(flush, it, 512 << 20);
+    cudaEventRecord(e0);
+    kern<<<grid, kThreads + 32, smem>>>(a);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (it >= 2) { best = std::min(best, ms); sum += ms; }
+  }
+  cudaError_t e = cudaGetLastError();
+  const double bytes = nnz * 12.0 + 4.0 * (n + 1) + 2.0 * n * 64;
+  printf("rows=%d stages=%d TR=%d nb=%d grid=%d smem=%zu err=%s best=%.3f ms avg=%.3f ms -> %.0f GB/s (best)\n",
+         SAD_BULK_ROWS, SAD_BULK_STAGES, BulkTile<4>::TR, nb, grid, smem, cudaGetErrorString(e), best,
+         sum / 10, bytes / (best * 1e-3) / 1e9);
+  return 0;
+}
