@@ -671,7 +671,7 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
     return set_err(ctx, SAD_ECUDA, "cudaFuncSetAttribute failed");
   }
   ws->dot_blocks_per_sm = std::max(1, std::min(8, (int)((200 * 1024) / dsm)));
-  if (cudaMalloc(&ws->V, blk * (m + 1)) != cudaSuccess) {
+  if (cudaMalloc(&ws->V, blk * (m + 1) + 64) != cudaSuccess) {
     delete ws;
     return set_err(ctx, SAD_ENOMEM, "basis allocation of %zu bytes failed", blk * (m + 1));
   }
@@ -1107,7 +1107,10 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t finA = ((2 * m1 + 1) * R + 2 * m1 * R) * 16 + m1 * R * 8 + 8 * 4 + 64;
   const size_t gblk = R * m1 * m1 * 16;
   const bool g_smem = finA + gblk <= 200 * 1024;
-  size_t smem = std::max({(size_t)2 * m1 * kWarps * R * ws->esz,       // phase-A sums
+  // phase-A TMA stages: one block-tile (kWarps * GPW * UA rows) of one basis block
+  const size_t gpw = 32 / R, ua = ws->esz == 8 ? 8 : 4;
+  const size_t stage = ((size_t)kWarps * gpw * ua * R * ws->esz + 32 + 127) & ~size_t(127);
+  size_t smem = std::max({(size_t)kStages * stage + 2 * m1 * R * ws->esz,   // ring + sums
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
                           finA + (g_smem ? gblk : 0)});
@@ -1115,10 +1118,12 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   if (ws->dtype == SAD_F64) {
     PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
     a.g_smem = g_smem ? 1 : 0;
+    a.stage_bytes = (int)stage;
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
     a.g_smem = g_smem ? 1 : 0;
+    a.stage_bytes = (int)stage;
     e = coop_dispatch_z(a, ws, op, s, smem);
   }
   if (e != cudaSuccess)

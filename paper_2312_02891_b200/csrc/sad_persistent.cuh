@@ -23,8 +23,11 @@
 #pragma once
 
 #include "sad_kernels.cuh"
+#include "sad_spmm_bulk.cuh"
 
 namespace sad {
+
+constexpr int kStages = 4;   // phase-A TMA ring depth
 
 struct PState {
   GState g;              // j, any_active, active, done, kdim, iters, S, H, cs, sn, g, ycoef, ...
@@ -58,6 +61,7 @@ struct PArgs {
   int pT;                // block stride of the output-major partials
   int prof;              // record phase timers
   int g_smem;            // stage the Gram block in shared memory (fits)
+  int stage_bytes;       // bytes of one phase-A TMA stage (128-aligned)
   PState st;
 };
 
@@ -205,9 +209,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   double acc_bytes = 0.0, acc_steps = 0.0, acc_cycles = 1.0;
   double t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // A, C, X, R, workA, workC (ns, block 0)
 
-  XT* s_acc = reinterpret_cast<XT*>(smem_p);  // [2(m+1)][kWarps][R] (phase A)
   __shared__ double s_w2[kWarps][8];
   __shared__ int s_any;
+  // phase-A TMA ring
+  __shared__ __align__(8) unsigned long long s_full[kStages];
+  __shared__ int s_soff[kStages];
+  __shared__ XT s_ph[2][kWarps][R], s_pg[2][kWarps][R];
+  unsigned long long ring = 0;   // basis-tile copies issued so far (block-uniform)
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kStages; ++q) mbar_init(s_full + q, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
 
   // ---- init: x = 0, V_0 = b, ||b||^2 -> restart decision --------------------
   {
@@ -279,20 +292,39 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         const XT* vj = a.V + (long long)j * a.stride;
         XT* w = a.V + (long long)J * a.stride;
         const double sj = lane_ok ? ldcg1(gs.S + j * R + c) : 0.0;
-        for (int o = threadIdx.x; o < 2 * J * kWarps * R; o += kThreads) s_acc[o] = zero<XT>();
+        // The basis is streamed through a ring of TMA stages (one stage = the
+        // tile's rows of one basis block); per basis block the block reduces its
+        // h / g contributions through shared memory in a fixed order.
+        XT* s_blk = reinterpret_cast<XT*>(smem_p + (size_t)kStages * a.stage_bytes);  // [2J][R]
+        for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) s_blk[o] = zero<XT>();
         double w2 = 0.0;
         __syncthreads();
-        // rows of a block-tile are dealt to the warps GPW at a time (u-major), so
-        // every warp gets work even when the block owns few rows; for fixed u a
-        // warp reads GPW consecutive rows = 32 consecutive elements (coalesced)
-        for (long long base = r0; base < r1; base += (long long)kWarps * GPW * UA) {
-          // warp-uniform loop: the shuffles below need every lane present
+        constexpr int T = kWarps * GPW * UA;   // rows per block-tile
+        for (long long base = r0; base < r1; base += T) {
+          const long long nrows = min((long long)T, r1 - base);
+          auto issue = [&](int i, int q) {
+            const unsigned long long src =
+                reinterpret_cast<unsigned long long>(a.V + (long long)i * a.stride + base * R);
+            const unsigned long long e = src + (unsigned long long)(nrows * R) * sizeof(XT);
+            const unsigned long long a0 = src & ~15ull, a1 = (e + 15ull) & ~15ull;
+            s_soff[q] = (int)((src - a0) / sizeof(XT));
+            mbar_expect_tx(s_full + q, (unsigned)(a1 - a0));
+            bulk_g2s(smem_p + (size_t)q * a.stage_bytes, reinterpret_cast<const void*>(a0),
+                     (unsigned)(a1 - a0), s_full + q);
+          };
+          if (threadIdx.x == 0) {
+            fence_proxy_async();
+            for (int i = 0; i < min(kStages, J); ++i) issue(i, (int)((ring + i) % kStages));
+          }
+          // the tile's SpMM (overlaps with the first basis copies)
           XT wv[UA], xv[UA];
           long long idx[UA];
+          int lr[UA];
 #pragma unroll
           for (int u = 0; u < UA; ++u) {
-            const long long row = base + ((long long)u * kWarps + warp) * GPW + grp;
-            idx[u] = (lane_ok && row < r1) ? row * R + c : -1;
+            lr[u] = (u * kWarps + warp) * GPW + grp;
+            const long long row = base + lr[u];
+            idx[u] = (lane_ok && lr[u] < nrows) ? row * R + c : -1;
           }
           spmm_rows<XT, VT, PRE, SIGMA, R, UA>(a.rowptr, a.colidx,
                                                reinterpret_cast<const VT*>(a.vals), a.dinv,
@@ -309,49 +341,47 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               w2 += abs2(wv[u]);
             }
           }
-          for (int i0 = 0; i0 < J; i0 += IB) {
-            // IB basis blocks per round: IB*UA independent loads in flight
-            XT ph[IB], pg[IB];
+          for (int i = 0; i < J; ++i) {
+            const int q = (int)((ring + i) % kStages);
+            mbar_wait(s_full + q, (unsigned)(((ring + i) / kStages) & 1));
+            const XT* Vs = reinterpret_cast<const XT*>(smem_p + (size_t)q * a.stage_bytes) + s_soff[q];
+            XT ph = zero<XT>(), pg = zero<XT>();
 #pragma unroll
-            for (int ib = 0; ib < IB; ++ib) { ph[ib] = zero<XT>(); pg[ib] = zero<XT>(); }
-#pragma unroll
-            for (int ib = 0; ib < IB; ++ib) {
-              if (i0 + ib < J) {
-                const XT* vi = a.V + (long long)(i0 + ib) * a.stride;
-#pragma unroll
-                for (int u = 0; u < UA; ++u) {
-                  if (idx[u] >= 0) {
-                    const XT v = vi[idx[u]];
-                    ph[ib] = cfma(v, wv[u], ph[ib]);
-                    pg[ib] = cfma(v, xv[u], pg[ib]);
-                  }
-                }
+            for (int u = 0; u < UA; ++u) {
+              if (idx[u] >= 0) {
+                const XT v = Vs[lr[u] * R + c];
+                ph = cfma(v, wv[u], ph);
+                pg = cfma(v, xv[u], pg);
               }
             }
+            ph = group_reduce<R>(ph, grp);
+            pg = group_reduce<R>(pg, grp);
+            if (grp == 0 && lane_ok) {
+              s_ph[i & 1][warp][c] = ph;
+              s_pg[i & 1][warp][c] = pg;
+            }
+            __syncthreads();
+            if (warp == 0 && lane < R) {
+              XT th = s_blk[i * R + lane], tg = s_blk[(J + i) * R + lane];
 #pragma unroll
-            for (int ib = 0; ib < IB; ++ib) {
-              if (i0 + ib < J) {
-                const XT h = group_reduce<R>(ph[ib], grp);
-                const XT gq = group_reduce<R>(pg[ib], grp);
-                if (grp == 0 && lane_ok) {
-                  XT* s0 = s_acc + ((size_t)(i0 + ib) * kWarps + warp) * R + c;
-                  *s0 = add(*s0, h);
-                  XT* s1 = s_acc + ((size_t)(J + i0 + ib) * kWarps + warp) * R + c;
-                  *s1 = add(*s1, gq);
-                }
+              for (int wq = 0; wq < kWarps; ++wq) {
+                th = add(th, s_ph[i & 1][wq][lane]);
+                tg = add(tg, s_pg[i & 1][wq][lane]);
               }
+              s_blk[i * R + lane] = th;
+              s_blk[(J + i) * R + lane] = tg;
+            }
+            if (threadIdx.x == 0 && i + kStages < J) {
+              fence_proxy_async();
+              issue(i + kStages, q);
             }
           }
+          ring += J;
         }
         w2 = group_reduce<R>(w2, grp);
         if (grp == 0 && lane_ok) s_w2[warp][c] = w2;
         __syncthreads();
-        for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) {
-          const int ii = o / R, cc = o - ii * R;
-          XT t = zero<XT>();
-          for (int wq = 0; wq < kWarps; ++wq) t = add(t, s_acc[((size_t)ii * kWarps + wq) * R + cc]);
-          put(o, to_c(t));
-        }
+        for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) put(o, to_c(s_blk[o]));
         if (threadIdx.x < R) {
           double t = 0.0;
           for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
