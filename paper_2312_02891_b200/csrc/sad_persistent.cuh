@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         // The basis is streamed through a ring of TMA stages (one stage = the
         // tile's rows of one basis block); per basis block the block reduces its
         // h / g contributions through shared memory in a fixed order.
-        XT* s_blk = reinterpret_cast<XT*>(smem_p + (size_t)kStages * a.stage_bytes);  // [2J][R]
+        unsigned char* const smem_c = reinterpret_cast<unsigned char*>(smem_p);
+        XT* s_blk = reinterpret_cast<XT*>(smem_c + (size_t)kStages * a.stage_bytes);  // [2J][R]
         for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) s_blk[o] = zero<XT>();
         double w2 = 0.0;
         __syncthreads();
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             const unsigned long long a0 = src & ~15ull, a1 = (e + 15ull) & ~15ull;
             s_soff[q] = (int)((src - a0) / sizeof(XT));
             mbar_expect_tx(s_full + q, (unsigned)(a1 - a0));
-            bulk_g2s(smem_p + (size_t)q * a.stage_bytes, reinterpret_cast<const void*>(a0),
+            bulk_g2s(smem_c + (size_t)q * a.stage_bytes, reinterpret_cast<const void*>(a0),
                      (unsigned)(a1 - a0), s_full + q);
           };
           if (threadIdx.x == 0) {
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           for (int i = 0; i < J; ++i) {
             const int q = (int)((ring + i) % kStages);
             mbar_wait(s_full + q, (unsigned)(((ring + i) / kStages) & 1));
-            const XT* Vs = reinterpret_cast<const XT*>(smem_p + (size_t)q * a.stage_bytes) + s_soff[q];
+            const XT* Vs = reinterpret_cast<const XT*>(smem_c + (size_t)q * a.stage_bytes) + s_soff[q];
             XT ph = zero<XT>(), pg = zero<XT>();
 #pragma unroll
             for (int u = 0; u < UA; ++u) {
