@@ -137,6 +137,17 @@ int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
                     uint8_t* conv_host);
 
 /*
+ * The same solve split in two: sad_gmres_launch enqueues it on `stream` and
+ * returns (persistent engine; the multi-kernel engine runs to completion
+ * inside launch); sad_gmres_finish waits and fills the result arrays.  Lets
+ * one host thread keep the A- and B-side solves in flight together.
+ */
+int sad_gmres_launch(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
+                     double tol_col, int maxit, void* stream);
+int sad_gmres_finish(sad_gmres* ws, void* res_dev, void* stream, int64_t* iters_host,
+                     double* resnorm_host, uint8_t* conv_host);
+
+/*
  * Same solve, but a fixed number of Arnoldi steps (no stopping test inside the
  * cycle; config 4 "100 fixed block-GMRES iterations").  When timing_ms_host is
  * not NULL it receives (CUDA events on `stream`):

@@ -47,6 +47,8 @@ SIGNATURES = {
     "sad_gmres_set_option": (_c.c_int, [_vp, _c.c_int, _c.c_int]),
     "sad_gmres_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp,
                                    _vp, _vp, _vp]),
+    "sad_gmres_launch": (_c.c_int, [_vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp]),
+    "sad_gmres_finish": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "sad_gmres_fixed": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_int, _vp, _vp, _vp]),
     "sad_gram": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),
     "sad_axpy": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.c_double, _c.c_double,

@@ -525,6 +525,7 @@ class DeviceAdi:
                     f"{config.strategy.value}: direct inner solves are not on the GPU hot path")
         self.problem, self.config, self.shifts = problem, config, shift_sequence
         self.device = device
+        self.engine = engine
         self.concurrent = concurrent
         self.dev = torch.device("cuda", device)
         pairs = [shift_sequence.at(k) for k in range(1, min(config.kmax, _seq_len(shift_sequence)) + 1)]
@@ -631,6 +632,16 @@ class DeviceAdi:
         cur = torch.cuda.current_stream(self.dev)
         self.sA.wait_stream(cur)
         self.sB.wait_stream(cur)
+        if self.engine == "persistent" and w.shape[1] <= 8:
+            # both persistent solves in flight from this thread, one wait each
+            resA = torch.empty_like(w)
+            resB = torch.empty_like(t)
+            ta = self.bA.begin_device(beta, w, dA, z, resA, self.sA)
+            tb = self.bB.begin_device(alpha, t, dB, y, resB, self.sB)
+            ra, rb = self.bA.end_device(ta), self.bB.end_device(tb)
+            cur.wait_stream(self.sA)
+            cur.wait_stream(self.sB)
+            return ra, rb
 
         def side(binding, stream, shift, rhs, delta, x):
             with torch.cuda.device(self.dev):

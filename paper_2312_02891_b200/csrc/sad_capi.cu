@@ -112,6 +112,8 @@ struct sad_gmres {
   double* stats_dev = nullptr;
   // profiling (sad_gmres_profile): synchronous stepping with CUDA events
   int profile = 0;
+  int pending_multi = 0;
+  double pending_tol = 0.0;
   int timers = 0;   // phase timers without event profiling (sad_gmres_fixed)
   double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double prof2[4] = {0, 0, 0, 0};   // work_A, work_C (block 0), fin_A, fin_C (last block), ms
@@ -1470,4 +1472,35 @@ extern "C" int sad_adi_epilogue(sad_ctx* ctx, int64_t nA, int64_t nB, int r, int
   CK(ctx, cudaStreamSynchronize(s));
   std::memcpy(gram_host, ctx->epi_host, bytes);
   return SAD_OK;
+}
+
+// -----------------------------------------------------------------------------
+// split launch / finish (two solves in flight from one host thread)
+// -----------------------------------------------------------------------------
+extern "C" int sad_gmres_launch(sad_gmres* ws, sad_op* op, const void* rhs, void* x, double tol_col,
+                                int maxit, void* stream) {
+  if (!ws) return SAD_EINVAL;
+  sad_ctx* ctx = ws->ctx;
+  if (!(tol_col > 0.0)) return set_err(ctx, SAD_EINVAL, "abs_tolerance must be positive");
+  if (maxit < 0) return set_err(ctx, SAD_EINVAL, "maxit must be >= 0");
+  ws->pending_tol = tol_col;
+  if (ws->engine != SAD_ENGINE_PERSISTENT) {
+    // the multi-kernel engine is host-driven: run it to completion here
+    ws->pending_multi = 1;
+    return sad_gmres_solve(ws, op, rhs, x, nullptr, tol_col, maxit, stream, nullptr, nullptr,
+                           nullptr);
+  }
+  ws->pending_multi = 0;
+  return persistent_run(ws, op, rhs, x, S_(stream), tol_col, maxit, 0);
+}
+
+extern "C" int sad_gmres_finish(sad_gmres* ws, void* res, void* stream, int64_t* iters_host,
+                                double* resnorm_host, uint8_t* conv_host) {
+  if (!ws) return SAD_EINVAL;
+  cudaStream_t s = S_(stream);
+  if (!ws->pending_multi) {
+    int rc = persistent_collect(ws, s);
+    if (rc) return rc;
+  }
+  return read_results(ws, res, s, iters_host, resnorm_host, conv_host, ws->pending_tol);
 }

@@ -177,6 +177,38 @@ __device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int
   }
 }
 
+// nout <= 8 outputs: every thread loads its blocks' partials for all outputs
+// (one round of independent loads), then a fixed shuffle tree per warp and a
+// fixed-order sum over warps.
+__device__ void reduce_partials_small(const double2* partT, int pT, int nblocks, int nout,
+                                      double2* out) {
+  __shared__ double2 s_ws[kWarps][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2 acc[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] = make_double2(0.0, 0.0);
+  for (int b = threadIdx.x; b < nblocks; b += kThreads) {
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if (o < nout) acc[o] = add(acc[o], __ldcg(partT + (size_t)o * pT + b));
+  }
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    if (o < nout) {
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) acc[o] = add(acc[o], shfl_down(acc[o], sh));
+      if (lane == 0) s_ws[warp][o] = acc[o];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nout) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int w = 0; w < kWarps; ++w) t = add(t, s_ws[w][threadIdx.x]);
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
 // ----------------------------------------------------------------------------
 // the persistent solve kernel
 // ----------------------------------------------------------------------------
@@ -247,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
       put(threadIdx.x, make_double2(t, 0.0));
     }
     if (bar_arrive(st, gen)) {
-      reduce_partials_T(partT, pT, gridDim.x, R, st.red);
+      reduce_partials_small(partT, pT, gridDim.x, R, st.red);
       __syncthreads();
       __shared__ double s_n2[8];
       if (threadIdx.x < R) s_n2[threadIdx.x] = st.red[threadIdx.x].x;
@@ -456,9 +488,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             const double2 h1 = s_h1[o];
             double2 cv = make_double2(2.0 * h1.x - gh.x, 2.0 * h1.y - gh.y);
             if (!s_act[cc]) cv = make_double2(0.0, 0.0);
-            st.hc[o] = cv;
+            s_red[o] = cv;     // reuse (sums no longer needed): Hessenberg column before rotation
             const double si = s_S[o];
             st.coef[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * cv.x, si * cv.y);
+          }
+          __syncthreads();
+          // Apply the previous Givens rotations to the new Hessenberg column now
+          // (they do not depend on h_{j+1,j}), so the phase-C finisher only has to
+          // form the new rotation.  Rotations staged in smem (s_h1 / s_S reused).
+          {
+            double2* s_snr = s_h1;                                    // [R][j]
+            double* s_csr = s_S;                                      // [R][j]
+            for (int o = threadIdx.x; o < j * R; o += kThreads) {
+              const int cc = o / j, ii = o - cc * j;
+              s_snr[cc * j + ii] = gs.sn[(size_t)cc * m + ii];
+              s_csr[cc * j + ii] = gs.cs[(size_t)cc * m + ii];
+            }
+            __syncthreads();
+            if (threadIdx.x < R && s_act[threadIdx.x]) {
+              const int cc = threadIdx.x;
+              double2 x0 = s_red[cc];
+              for (int ii = 0; ii < j; ++ii) {
+                const double2 x1 = s_red[(ii + 1) * R + cc];
+                const double ci = s_csr[cc * j + ii];
+                const double2 si = s_snr[cc * j + ii];
+                s_red[ii * R + cc] = add(scal(ci, x0), mul(si, x1));
+                x0 = sub(scal(ci, x1), mul(cconj(si), x0));
+              }
+              st.hc[j * R + cc] = x0;   // partially rotated diagonal entry
+            }
+            __syncthreads();
+            for (int o = threadIdx.x; o < j * R; o += kThreads) {
+              const int ii = o / R, cc = o - ii * R;
+              if (s_act[cc]) gs.H[((size_t)cc * m + j) * (m + 1) + ii] = s_red[o];
+            }
           }
           if (prof && threadIdx.x == 0) atomicAdd(st.stats + 10, (double)(gtimer() - tfin));
           bar_release(st);
@@ -510,56 +573,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         if (timing && prof) t_acc[5] += (double)(gtimer() - tphase);
         if (bar_arrive(st, gen)) {
           const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
-          reduce_partials_T(partT, pT, gridDim.x, R, st.red);
-          // stage the Hessenberg column and the previous rotations in smem
-          double2* s_col = reinterpret_cast<double2*>(smem_p);        // [R][m+1]
-          double2* s_sn = s_col + (size_t)R * (m + 1);                 // [R][m]
-          double* s_cs = reinterpret_cast<double*>(s_sn + (size_t)R * m);  // [R][m]
-          for (int o = threadIdx.x; o < (j + 1) * R; o += kThreads) {
-            const int ii = o / R, cc = o - ii * R;
-            s_col[cc * (m + 1) + ii] = st.hc[o];
-          }
-          for (int o = threadIdx.x; o < j * R; o += kThreads) {
-            const int cc = o / j, ii = o - cc * j;
-            s_sn[cc * m + ii] = gs.sn[(size_t)cc * m + ii];
-            s_cs[cc * m + ii] = gs.cs[(size_t)cc * m + ii];
-          }
+          reduce_partials_small(partT, pT, gridDim.x, R, st.red);
           // per-column scalars, loaded together (one round trip)
-          int act_c = 0;
-          long long it_c = 0;
-          double wpre_c = 0.0;
-          double2 gj_c = make_double2(0.0, 0.0);
-          if (threadIdx.x < R) {
-            const int cc = threadIdx.x;
-            act_c = gs.active[cc];
-            it_c = gs.iters[cc];
-            wpre_c = gs.wpre2[cc];
-            gj_c = gs.g[(size_t)cc * (m + 1) + j];
-          }
-          __syncthreads();
           __shared__ int s_actn[8];
-          __shared__ int s_kd[8];
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
+            const int act_c = gs.active[cc];
             s_actn[cc] = 0;
-            s_kd[cc] = -1;
             if (act_c) {
+              const long long it_c = gs.iters[cc];
+              const double wpre_c = gs.wpre2[cc];
+              const double2 gj_c = gs.g[(size_t)cc * (m + 1) + j];
+              const double2 hjj = st.hc[j * R + cc];
               const double hn = sqrt(st.red[cc].x);
-              double2* col = s_col + (size_t)cc * (m + 1);
-              const double* csv = s_cs + (size_t)cc * m;
-              const double2* snv = s_sn + (size_t)cc * m;
-              double2 x0 = col[0];
-              for (int ii = 0; ii < j; ++ii) {
-                const double2 x1 = col[ii + 1];
-                const double ci = csv[ii];
-                const double2 si = snv[ii];
-                col[ii] = add(scal(ci, x0), mul(si, x1));
-                x0 = sub(scal(ci, x1), mul(cconj(si), x0));
-              }
               double cj; double2 sjv, rj;
-              givens(x0, make_double2(hn, 0.0), cj, sjv, rj);
+              givens(hjj, make_double2(hn, 0.0), cj, sjv, rj);
               gs.cs[(size_t)cc * m + j] = cj;
               gs.sn[(size_t)cc * m + j] = sjv;
+              double2* col = gs.H + ((size_t)cc * m + j) * (m + 1);
               col[j] = rj;
               col[j + 1] = make_double2(0.0, 0.0);
               double2* gv = gs.g + (size_t)cc * (m + 1);
@@ -570,7 +601,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               const long long it = it_c + 1;
               gs.iters[cc] = it;
               gs.kdim[cc] = j + 1;
-              s_kd[cc] = j + 1;
               const double est = cabs_(gnext);
               gs.S[(j + 1) * R + cc] = hn > 0.0 ? 1.0 / hn : 0.0;
               bool end = (j + 1 == m) || it >= gs.maxit;
@@ -582,12 +612,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             }
           }
           __syncthreads();
-          // write the rotated column back (only columns that were active)
-          for (int o = threadIdx.x; o < (j + 2) * R; o += kThreads) {
-            const int cc = o / (j + 2), ii = o - cc * (j + 2);
-            if (s_kd[cc] == j + 1)
-              gs.H[((size_t)cc * m + j) * (m + 1) + ii] = s_col[cc * (m + 1) + ii];
-          }
           int any_now = 0;
           for (int cc = 0; cc < R; ++cc) any_now |= s_actn[cc];
           if (threadIdx.x == 0) {
@@ -705,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         put(threadIdx.x, make_double2(t, 0.0));
       }
       if (bar_arrive(st, gen)) {
-        reduce_partials_T(partT, pT, gridDim.x, R, st.red);
+        reduce_partials_small(partT, pT, gridDim.x, R, st.red);
         __syncthreads();
         if (threadIdx.x < R) {
           const int cc = threadIdx.x;

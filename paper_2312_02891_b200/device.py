@@ -209,6 +209,25 @@ class GmresWorkspace:
         _lib.check(rc, self._ctx)
         return iters, norms, conv.astype(bool)
 
+    def launch(self, op, rhs, x, tol_col, maxit, stream=None):
+        """Enqueue a solve (returns immediately for the persistent engine)."""
+        rc = _lib.load().sad_gmres_launch(self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
+                                          float(tol_col), int(maxit),
+                                          current_stream_handle(stream))
+        _lib.check(rc, self._ctx)
+
+    def finish(self, res, stream=None):
+        """Wait for the launched solve; (iterations, residual norms, converged)."""
+        r = self.r
+        iters = np.zeros(r, dtype=np.int64)
+        norms = np.zeros(r, dtype=np.float64)
+        conv = np.zeros(r, dtype=np.uint8)
+        rc = _lib.load().sad_gmres_finish(self.handle, None if res is None else res.data_ptr(),
+                                          current_stream_handle(stream), iters.ctypes.data,
+                                          norms.ctypes.data, conv.ctypes.data)
+        _lib.check(rc, self._ctx)
+        return iters, norms, conv.astype(bool)
+
     def fixed(self, op, rhs, x, res, steps, stream=None, timed=False):
         norms = np.zeros(self.r, dtype=np.float64)
         timing = np.zeros(4, dtype=np.float64)

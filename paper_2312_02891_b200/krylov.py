@@ -193,6 +193,28 @@ class GpuGmresBinding:
         return DeviceSolveResult(solution=x, residual=res, achieved_residual_norms=norms,
                                  iterations=iters, converged=conv)
 
+    def begin_device(self, shift, rhs, delta, x, res, stream=None):
+        """Enqueue a device solve (r <= 8 columns); pair with ``end_device``."""
+        import torch
+        if delta <= 0.0:
+            raise ValueError("abs_tolerance must be positive")
+        n, r = rhs.shape
+        if n != self.n or r > MAX_BLOCK:
+            raise ValueError("begin_device needs an (n, r<=8) block")
+        op = self.operator(shift)
+        if rhs.dtype == torch.float64 and not op.is_real:
+            raise ValueError("complex shift requires a complex128 block")
+        dtype = _lib.SAD_F64 if rhs.dtype == torch.float64 else _lib.SAD_C128
+        ws = self.workspace(r, dtype)
+        ws.launch(op, rhs, x, float(delta) / r, self.max_iterations, stream)
+        return (ws, x, res, stream)
+
+    def end_device(self, token):
+        ws, x, res, stream = token
+        it, nr, cv = ws.finish(res, stream)
+        return DeviceSolveResult(solution=x, residual=res, achieved_residual_norms=nr,
+                                 iterations=it, converged=cv)
+
     def solve(self, shift, rhs, delta):
         """SolverBinding.solve (adi.py:473-488) on host numpy blocks."""
         import torch
