@@ -33,6 +33,10 @@ import warnings
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
+if "--impl" in sys.argv and "reference" in sys.argv:
+    # the reference's CPU path is scalar numpy/scipy: pin BLAS to one thread
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(_v, "1")
 
 import numpy as np  # noqa: E402
 
@@ -184,47 +188,36 @@ def cpu_reference_solve(kmax=None):
     return time.perf_counter() - t0, run.outer_iterations, bool(run.converged)
 
 
-def _pool_solve(_):
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    return cpu_reference_solve()
-
-
 def run_reference_arm(args, dist):
-    """--impl reference: rank 0 times the reference's CPU path; other ranks exit."""
+    """--impl reference: rank 0 times the reference's CPU path (Jacobi-BiCGstab
+    ADI, restated in oracle/) on the host, one full config-2 solve per step,
+    sequentially in this process; other ranks exit without work."""
     if dist.rank != 0:
         return None
-    import multiprocessing as mp
-    cores = len(os.sched_getaffinity(0))
-    workers = max(1, min(args.steps, cores))
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(workers) as pool:
-        for _ in range(args.warmup):
-            pool.map(_warm_solve, range(workers))
-        t0 = time.perf_counter()
-        results = pool.map(_pool_solve, range(args.steps))
-        wall = time.perf_counter() - t0
-    secs = [r[0] for r in results]
+    for _ in range(args.warmup):
+        cpu_reference_solve(kmax=1)
+    secs, steps_cpu, conv = [], 0, True
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        t, steps_cpu, c = cpu_reference_solve()
+        secs.append(t)
+        conv = conv and c
+    wall = time.perf_counter() - t0
     value = statistics.mean(secs)
     spec, prob, _, _, _ = build_c2()
-    line = {
+    return {
         "metric": "wall time to 1e-8 ADI residual", "value": value, "unit": "s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * value, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded reference generators)",
-        "config": c2_config_json(spec, prob, {"outer_steps": results[0][1],
-                                              "converged": all(r[2] for r in results),
+        "config": c2_config_json(spec, prob, {"outer_steps": steps_cpu, "converged": conv,
                                               "inner": "Jacobi-BiCGstab (reference path)"}),
-        "cpu_baseline": {"value": value, "unit": "s", "cores": workers, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "port",
                          "sample": f"{args.steps} full config-2 solves of the reference's "
-                                   f"Jacobi-BiCGstab ADI (oracle/ restatement), one per "
-                                   f"process on {workers} host cores; wall {wall:.1f}s"},
+                                   f"Jacobi-BiCGstab ADI (oracle/ restatement), sequential, "
+                                   f"one core (BLAS threads 1); wall {wall:.1f}s"},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    return line
-
-
-def _warm_solve(_):
-    return cpu_reference_solve(kmax=1)
 
 
 def profile_pass(eng):
