@@ -284,10 +284,18 @@ class LowRankSolution:
 
     @staticmethod
     def _stack(blocks, rows, r):
+        """(rows, k*r) complex128 host array; each device block is copied
+        straight into its column slice of one pinned buffer."""
         if not blocks:
             return np.zeros((rows, 0), dtype=complex)
         import torch
-        return torch.cat(blocks, dim=1).cpu().numpy().astype(complex)
+        k = len(blocks)
+        host = torch.empty((rows, k * r), dtype=torch.complex128, pin_memory=True)
+        for i, b in enumerate(blocks):
+            src = b if b.dtype == torch.complex128 else b.to(torch.complex128)
+            host[:, i * r:(i + 1) * r].copy_(src, non_blocking=True)
+        torch.cuda.synchronize(blocks[0].device)
+        return host.numpy()
 
     @property
     def Z(self):

@@ -388,11 +388,14 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   }
   // Jacobi dinv (precond.py:272-276): 1/diag(assembled op); identity when "none"
   const long long n = op->n;
-  CK(ctx, cudaMalloc(&op->dinv_c, std::max<long long>(n, 1) * sizeof(double2)));
-  CK(ctx, cudaMalloc(&op->dinv_r, std::max<long long>(n, 1) * sizeof(double)));
-  int* d_bd = nullptr;
-  CK(ctx, cudaMalloc(&d_bd, sizeof(int)));
-  CK(ctx, cudaMemset(d_bd, 0, sizeof(int)));
+  // one allocation for both dinv copies; the breakdown flag lives in the ctx
+  char* dbuf = nullptr;
+  const size_t nn = (size_t)std::max<long long>(n, 1);
+  CK(ctx, cudaMalloc(&dbuf, nn * sizeof(double2) + nn * sizeof(double) + 256));
+  op->dinv_c = reinterpret_cast<double2*>(dbuf);
+  op->dinv_r = reinterpret_cast<double*>(dbuf + ((nn * sizeof(double2) + 255) & ~size_t(255)));
+  int* d_bd = reinterpret_cast<int*>(ctx->ticket + 8);
+  CK(ctx, cudaMemsetAsync(d_bd, 0, sizeof(int), 0));
   const int blocks = grid_for(n, 256, ctx->nsm * 16);
   if (precond_kind == SAD_PRECOND_JACOBI) {
     if (op->vals_complex)
@@ -409,7 +412,6 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   CKL(ctx);
   int brk = 0;
   CK(ctx, cudaMemcpy(&brk, d_bd, sizeof(int), cudaMemcpyDeviceToHost));
-  cudaFree(d_bd);
   if (brk) {
     sad_op_destroy(op);
     return set_err(ctx, SAD_EBREAKDOWN, "zero diagonal entry for Jacobi");
@@ -423,8 +425,7 @@ extern "C" int sad_op_destroy(sad_op* op) {
   cudaFree(op->own_rowptr);
   cudaFree(op->own_colidx);
   cudaFree(op->own_vals);
-  cudaFree(op->dinv_c);
-  cudaFree(op->dinv_r);
+  cudaFree(op->dinv_c);   // dinv_r lives in the same allocation
   delete op;
   return SAD_OK;
 }

@@ -27,6 +27,40 @@ from .device import (DeviceMatrix, DeviceOperator, GmresWorkspace, gram,
 MAX_BLOCK = 8   # columns per device solve; wider blocks are split (columns are independent)
 
 
+class _WorkspacePool:
+    """Krylov workspaces are reused across bindings with the same shape
+    (device, n, r, dtype, restart, flexible, engine, SM cap): a caching
+    allocator for the (m+1)-block basis, like cuBLAS handles.  A workspace is
+    owned by at most one binding at a time."""
+
+    def __init__(self, keep=4):
+        self.free = {}
+        self.keep = keep
+
+    def take(self, key):
+        lst = self.free.get(key)
+        if lst:
+            return lst.pop()
+        dev, n, r, dtype, restart, flexible, engine, max_sms = key
+        ws = GmresWorkspace(n, r, dtype, restart, flexible, dev, engine=engine, max_sms=max_sms)
+        ws.pool_key = key
+        return ws
+
+    def give(self, ws):
+        key = getattr(ws, "pool_key", None)
+        if key is None:
+            return
+        lst = self.free.setdefault(key, [])
+        if len(lst) < self.keep:
+            lst.append(ws)
+
+    def clear(self):
+        self.free = {}
+
+
+_POOL = _WorkspacePool()
+
+
 @dataclass
 class InnerSolveResult:
     """Mirror of krylov.py:41-58."""
@@ -141,10 +175,15 @@ class GpuGmresBinding:
         key = (r, dtype)
         ws = self._workspaces.get(key)
         if ws is None:
-            ws = GmresWorkspace(self.n, r, dtype, self.restart, self.flexible, self.device,
-                                engine=self.engine, max_sms=self.max_sms)
+            ws = _POOL.take((self.device, self.n, r, dtype, self.restart, self.flexible,
+                             self.engine, self.max_sms))
             self._workspaces[key] = ws
         return ws
+
+    def __del__(self):
+        for ws in getattr(self, "_workspaces", {}).values():
+            _POOL.give(ws)
+        self._workspaces = {}
 
     # -- solves -------------------------------------------------------------
     def solve_device(self, shift, rhs, delta, x=None, res=None, stream=None,
