@@ -290,11 +290,12 @@ class LowRankSolution:
             return np.zeros((rows, 0), dtype=complex)
         import torch
         k = len(blocks)
+        dev = torch.cat(blocks, dim=1)            # (rows, k*r) contiguous on the device
+        if dev.dtype != torch.complex128:
+            dev = dev.to(torch.complex128)
         host = torch.empty((rows, k * r), dtype=torch.complex128, pin_memory=True)
-        for i, b in enumerate(blocks):
-            src = b if b.dtype == torch.complex128 else b.to(torch.complex128)
-            host[:, i * r:(i + 1) * r].copy_(src, non_blocking=True)
-        torch.cuda.synchronize(blocks[0].device)
+        host.copy_(dev, non_blocking=True)        # one contiguous D2H copy
+        torch.cuda.synchronize(dev.device)
         return host.numpy()
 
     @property
