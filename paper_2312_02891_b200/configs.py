@@ -77,6 +77,16 @@ def _c5_matrices(n0_a=200, n0_b=160):
     return A, B, None, None
 
 
+def _c3s_matrices():
+    """Config 3 at reduced size (same generator, operators and convection)."""
+    return _c3_matrices(n0_a=48, n0_b=40)
+
+
+def _c5s_matrices():
+    """Config 5 operator family at proxy size (n0=16 / 13)."""
+    return _c5_matrices(n0_a=16, n0_b=13)
+
+
 CONFIGS = {
     "c1": ConfigSpec("c1", "2-D conv-diff 64^2 / 48^2, r=1, GMRES(50)",
                      r=1, seed=0, kmax=150, restart=50, flexible=False,
@@ -93,10 +103,14 @@ CONFIGS = {
     "c5": ConfigSpec("c5", "3-D conv-diff 200^3 / 160^3, r=4, GMRES(30)",
                      r=4, seed=0, kmax=700, restart=30, flexible=False,
                      npairs=16),
+    "c3s": ConfigSpec("c3s", "config 3 at 48^2 / 40^2 (generalised pencils), r=3, GMRES(40)",
+                      r=3, seed=0, kmax=150, restart=40, flexible=False, npairs=10),
+    "c5s": ConfigSpec("c5s", "config 5 family at 16^3 / 13^3, r=4, GMRES(30)",
+                      r=4, seed=0, kmax=400, restart=30, flexible=False, npairs=16),
 }
 
 _BUILDERS = {"c1": _c1_matrices, "c2": _c2_matrices, "c3": _c3_matrices,
-             "c5": _c5_matrices}
+             "c5": _c5_matrices, "c3s": _c3s_matrices, "c5s": _c5s_matrices}
 
 
 def build_problem(name, **sizes):

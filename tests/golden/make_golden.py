@@ -231,10 +231,52 @@ def oracle_run(name):
           f" sum inner {run.sum_inner_A}/{run.sum_inner_B}, {run.wall_ms/1e3:.1f}s")
 
 
+def make_shifts_generalised(name, A, M, B, C, npairs):
+    """Reference heuristic shifts for pencils (A, M), (B, C) (shifts.py:107-132)."""
+    path = os.path.join(REPO, "configs", f"shifts_{name}.json")
+    if os.path.exists(path):
+        print("keep", path)
+        return
+    to = lambda X: None if X is None else sv.SparseMatrix(X)
+    seq = sv.heuristic_shifts(sv.pencil_ritz_sets(to(A), to(M)),
+                              sv.pencil_ritz_sets(to(B), to(C)), npairs=npairs)
+    seq.to_json(path)
+    print("wrote", path)
+
+
+def small_configs():
+    """Reduced configs 3 and 5: reference shifts + oracle GMRES goldens."""
+    for name in ("c3s", "c5s"):
+        A, B, M, C, f, g = cfgs.build_problem(name)
+        make_shifts_generalised(name, A, M, B, C, cfgs.CONFIGS[name].npairs)
+        oracle_run(name)
+    # the reference's own driver on the generalised small config (BiCGstab):
+    # pins the mass-matrix handling of the oracle driver (adi.py:520-528)
+    A, B, M, C, f, g = cfgs.build_problem("c3s")
+    seq = sv.ShiftSequence.from_json(os.path.join(REPO, "configs", "shifts_c3s.json"))
+    problem = sv.SylvesterProblem(A=sv.SparseMatrix(A), B=sv.SparseMatrix(B), f=f, g=g,
+                                  M=sv.SparseMatrix(M), C=sv.SparseMatrix(C))
+    cfg = sv.AdiConfig(strategy="dynamic_mid_bl", kmax=150, precond_kind_A="jacobi",
+                       precond_kind_B="jacobi")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        _, rep, _ = sv.run_with_state(problem, cfg, seq)
+    write_csv(os.path.join(GOLD, "ref_c3s_dynamic_mid_bl_bicgstab.csv"), rep)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-c2", action="store_true")
+    ap.add_argument("--small", action="store_true", help="only the reduced configs 3/5")
+    ap.add_argument("--c3-shifts", action="store_true", help="full-size config-3 shifts")
     args = ap.parse_args()
+    if args.small:
+        small_configs()
+        return
+    if args.c3_shifts:
+        A, B, M, C, f, g = cfgs.build_problem("c3")
+        make_shifts_generalised("c3", A, M, B, C, cfgs.CONFIGS["c3"].npairs)
+        return
     os.makedirs(GOLD, exist_ok=True)
     problem_hashes()
     small_cases()

@@ -93,3 +93,11 @@ def test_c1_serial_and_concurrent_sides_agree(engine):
 def test_c2_device_driver_matches_oracle():
     sol, rep, state = _gpu_run("c2")
     _check_against_golden(rep, "c2")
+
+
+@pytest.mark.parametrize("name", ["c3s", "c5s"])
+def test_reduced_configs_match_oracle(name):
+    """Generalised pencils (config 3 family, mass matrices on both sides) and
+    the 3-D r=4 config-5 family at reduced size."""
+    sol, rep, state = _gpu_run(name)
+    _check_against_golden(rep, name)

@@ -159,3 +159,23 @@ def test_oracle_driver_matches_reference_driver_with_gmres():
     assert len(gold) == len(mine) == 91
     for a, b in zip(gold, mine):
         assert a == b
+
+
+def test_oracle_bicgstab_adi_matches_reference_generalised():
+    """Generalised pencils (A, M), (B, C) of the reduced config 3: the restated
+    driver (M z, C^T y, assembled Jacobi) reproduces the reference's run."""
+    gold = read_steps_csv(os.path.join(GOLD, "ref_c3s_dynamic_mid_bl_bicgstab.csv"))
+    spec = cfgs.CONFIGS["c3s"]
+    A, B, M, C, f, g = cfgs.build_problem("c3s")
+    pairs, cyclic = spec.load_shift_pairs()
+    cfg = orc.Config(strategy="dynamic_mid_bl", kmax=150)
+    bA = orc.Binding("A", A, M, solver="bicgstab")
+    bB = orc.Binding("B", B, C, solver="bicgstab")
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        run = orc.run_adi(A, B, f, g, cfg, pairs, bA, bB, M=M, C=C, cyclic=cyclic)
+    assert run.outer_iterations == len(gold)
+    for rec, gd in zip(run.records, gold):
+        assert rec.inner_it_A == gd["inner_it_A"] and rec.inner_it_B == gd["inner_it_B"]
+        assert abs(rec.scaled_res - gd["scaled_res"]) <= 1e-8 * gd["scaled_res"]
