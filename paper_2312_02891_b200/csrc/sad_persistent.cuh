@@ -28,6 +28,7 @@
 namespace sad {
 
 constexpr int kStages = 4;   // phase-A TMA ring depth
+constexpr int kGroup = 2;    // basis blocks reduced per __syncthreads (kStages = 2 * kGroup)
 
 struct PState {
   GState g;              // j, any_active, active, done, kdim, iters, S, H, cs, sn, g, ycoef, ...
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   // phase-A TMA ring
   __shared__ __align__(8) unsigned long long s_full[kStages];
   __shared__ int s_soff[kStages];
-  __shared__ XT s_ph[2][kWarps][R], s_pg[2][kWarps][R];
+  __shared__ XT s_ph[kGroup][kWarps][R], s_pg[kGroup][kWarps][R];
   unsigned long long ring = 0;   // basis-tile copies issued so far (block-uniform)
   if (threadIdx.x == 0) {
     for (int q = 0; q < kStages; ++q) mbar_init(s_full + q, 1);
@@ -374,40 +375,64 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               w2 += abs2(wv[u]);
             }
           }
-          for (int i = 0; i < J; ++i) {
-            const int q = (int)((ring + i) % kStages);
-            mbar_wait(s_full + q, (unsigned)(((ring + i) / kStages) & 1));
-            const XT* Vs = reinterpret_cast<const XT*>(smem_c + (size_t)q * a.stage_bytes) + s_soff[q];
-            XT ph = zero<XT>(), pg = zero<XT>();
+          // basis blocks in groups of kGroup per __syncthreads (the other half of
+          // the ring is in flight meanwhile)
+          for (int i0 = 0; i0 < J; i0 += kGroup) {
+            const int ng = min(kGroup, J - i0);
+            XT ph[kGroup], pg[kGroup];
 #pragma unroll
-            for (int u = 0; u < UA; ++u) {
-              if (idx[u] >= 0) {
-                const XT v = Vs[lr[u] * R + c];
-                ph = cfma(v, wv[u], ph);
-                pg = cfma(v, xv[u], pg);
+            for (int gi = 0; gi < kGroup; ++gi) {
+              ph[gi] = zero<XT>();
+              pg[gi] = zero<XT>();
+              if (gi < ng) {
+                const long long kk = ring + i0 + gi;
+                const int q = (int)(kk % kStages);
+                mbar_wait(s_full + q, (unsigned)((kk / kStages) & 1));
+                const XT* Vs =
+                    reinterpret_cast<const XT*>(smem_c + (size_t)q * a.stage_bytes) + s_soff[q];
+#pragma unroll
+                for (int u = 0; u < UA; ++u) {
+                  if (idx[u] >= 0) {
+                    const XT v = Vs[lr[u] * R + c];
+                    ph[gi] = cfma(v, wv[u], ph[gi]);
+                    pg[gi] = cfma(v, xv[u], pg[gi]);
+                  }
+                }
               }
             }
-            ph = group_reduce<R>(ph, grp);
-            pg = group_reduce<R>(pg, grp);
-            if (grp == 0 && lane_ok) {
-              s_ph[i & 1][warp][c] = ph;
-              s_pg[i & 1][warp][c] = pg;
+#pragma unroll
+            for (int gi = 0; gi < kGroup; ++gi) {
+              if (gi < ng) {
+                const XT h = group_reduce<R>(ph[gi], grp);
+                const XT gq = group_reduce<R>(pg[gi], grp);
+                if (grp == 0 && lane_ok) {
+                  s_ph[gi][warp][c] = h;
+                  s_pg[gi][warp][c] = gq;
+                }
+              }
             }
             __syncthreads();
             if (warp == 0 && lane < R) {
-              XT th = s_blk[i * R + lane], tg = s_blk[(J + i) * R + lane];
+              for (int gi = 0; gi < ng; ++gi) {
+                const int i = i0 + gi;
+                XT th = s_blk[i * R + lane], tg = s_blk[(J + i) * R + lane];
 #pragma unroll
-              for (int wq = 0; wq < kWarps; ++wq) {
-                th = add(th, s_ph[i & 1][wq][lane]);
-                tg = add(tg, s_pg[i & 1][wq][lane]);
+                for (int wq = 0; wq < kWarps; ++wq) {
+                  th = add(th, s_ph[gi][wq][lane]);
+                  tg = add(tg, s_pg[gi][wq][lane]);
+                }
+                s_blk[i * R + lane] = th;
+                s_blk[(J + i) * R + lane] = tg;
               }
-              s_blk[i * R + lane] = th;
-              s_blk[(J + i) * R + lane] = tg;
             }
-            if (threadIdx.x == 0 && i + kStages < J) {
+            if (threadIdx.x == 0) {
               fence_proxy_async();
-              issue(i + kStages, q);
+              for (int gi = 0; gi < ng; ++gi) {
+                const int i = i0 + gi;
+                if (i + kStages < J) issue(i + kStages, (int)((ring + i) % kStages));
+              }
             }
+            __syncthreads();   // s_ph/s_pg reused by the next group
           }
           ring += J;
         }
