@@ -22,7 +22,8 @@
 
 #include "../../include/sylvadi_b200.h"
 #include "sad_kernels.cuh"
-#include "sad_persistent.cuh"
+#include "sad_coop.cuh"
+#include "sad_spmm_launch.cuh"
 #include "sad_adi.cuh"
 #include "sad_spmm_bulk.cuh"
 
@@ -62,9 +63,12 @@ struct sad_csr {
 };
 
 static std::atomic<unsigned long long> g_op_uid{1};
-static int g_nsm_bulk = 148;   // SM count for the persistent-style SpMM grids
 static std::atomic<long long> g_launches{0};   // kernels launched by this library
 #define COUNT_LAUNCH(k) g_launches.fetch_add((k), std::memory_order_relaxed)
+namespace sad {
+void count_launches(long long k) { COUNT_LAUNCH(k); }
+int g_spmm_bulk_sms = 148;
+}
 
 struct sad_op {
   sad_ctx* ctx = nullptr;
@@ -166,7 +170,7 @@ extern "C" int sad_ctx_create(int device, sad_ctx** out) {
     return SAD_ECUDA;
   }
   c->nsm = nsm;
-  g_nsm_bulk = nsm;
+  g_spmm_bulk_sms = nsm;
   c->scratch_blocks = nsm * 4;
   if (cudaMalloc(&c->scratch, (size_t)c->scratch_blocks * 2 * 64 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->ticket, 64) != cudaSuccess ||
@@ -433,102 +437,6 @@ extern "C" int sad_op_destroy(sad_op* op) {
 extern "C" int sad_op_get_dinv(const sad_op* op, double* dinv_host) {
   if (!op || !dinv_host) return SAD_EINVAL;
   CK(op->ctx, cudaMemcpy(dinv_host, op->dinv_c, op->n * sizeof(double2), cudaMemcpyDeviceToHost));
-  return SAD_OK;
-}
-
-// -----------------------------------------------------------------------------
-// SpMM dispatch
-// -----------------------------------------------------------------------------
-template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
-static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
-  if (MODE == SPMM_APPLY || MODE == SPMM_RESID) {
-    // TMA-staged SpMM; grid = resident blocks (persistent over row tiles)
-    auto kern = k_spmm_bulk<XT, VT, R, MODE, PRE, SIGMA>;
-    constexpr size_t smem = bulk_smem_bytes<VT, R>();
-    static int nb = -1;
-    if (nb < 0) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads + 32, smem);
-      if (nb < 1) nb = 1;
-    }
-    const long long tiles = (a.n + BulkTile<R>::TR - 1) / BulkTile<R>::TR;
-    const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_nsm_bulk));
-    kern<<<g, kThreads + 32, smem, s>>>(a);
-    COUNT_LAUNCH(1);
-    return;
-  }
-  k_spmm<XT, VT, R, MODE, PRE, SIGMA><<<grid, kThreads, 0, s>>>(a);
-  COUNT_LAUNCH(1);
-}
-
-template <typename XT, typename VT, int R, int MODE>
-static void launch_spmm_ps(const SpmmArgs<XT>& a, bool pre, bool sigma, int grid, cudaStream_t s) {
-  if (pre) {
-    if (sigma) launch_spmm_t<XT, VT, R, MODE, true, true>(a, grid, s);
-    else launch_spmm_t<XT, VT, R, MODE, true, false>(a, grid, s);
-  } else {
-    if (sigma) launch_spmm_t<XT, VT, R, MODE, false, true>(a, grid, s);
-    else launch_spmm_t<XT, VT, R, MODE, false, false>(a, grid, s);
-  }
-}
-
-template <typename XT, int R, int MODE>
-static void launch_spmm_v(const SpmmArgs<XT>& a, bool vc, bool pre, bool sigma, int grid,
-                          cudaStream_t s);
-template <int R, int MODE>
-struct SpmmV {
-  static void run(const SpmmArgs<double>& a, bool, bool pre, bool sigma, int grid, cudaStream_t s) {
-    launch_spmm_ps<double, double, R, MODE>(a, pre, sigma, grid, s);
-  }
-  static void run(const SpmmArgs<double2>& a, bool vc, bool pre, bool sigma, int grid,
-                  cudaStream_t s) {
-    if (vc) launch_spmm_ps<double2, double2, R, MODE>(a, pre, false, grid, s);
-    else launch_spmm_ps<double2, double, R, MODE>(a, pre, sigma, grid, s);
-  }
-};
-
-template <typename XT, int MODE>
-static int launch_spmm(const SpmmArgs<XT>& a, int R, bool vc, bool pre, bool sigma, int nsm,
-                       cudaStream_t s, int grid_cap = 0);
-
-// A real block with an even number of columns is processed as a complex block
-// of R/2 columns (16-byte loads, half the lanes per row): for a real matrix and
-// a real shift every complex product reduces to the same two real FMAs, so
-// the results are identical.
-static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, int nsm,
-                       cudaStream_t s, int mode) {
-  if (R % 2 || pre || a.sigma.y != 0.0) return false;
-  SpmmArgs<double2> z{};
-  z.n = a.n; z.rowptr = a.rowptr; z.colidx = a.colidx; z.vals = a.vals;
-  z.x = reinterpret_cast<const double2*>(a.x);
-  z.y = reinterpret_cast<double2*>(a.y);
-  z.b = reinterpret_cast<const double2*>(a.b);
-  z.sigma = a.sigma;
-  if (mode == SPMM_APPLY) launch_spmm<double2, SPMM_APPLY>(z, R / 2, false, false, sigma, nsm, s);
-  else launch_spmm<double2, SPMM_RESID>(z, R / 2, false, false, sigma, nsm, s);
-  return true;
-}
-
-template <typename XT, int MODE>
-static int launch_spmm(const SpmmArgs<XT>& a, int R, bool vc, bool pre, bool sigma, int nsm,
-                       cudaStream_t s, int grid_cap) {
-  if constexpr (std::is_same<XT, double>::value && (MODE == SPMM_APPLY || MODE == SPMM_RESID)) {
-    if (spmm_pairs(a, R, pre, sigma, nsm, s, MODE)) return SAD_OK;
-  }
-  const int gpw = 32 / R;
-  const int cap = grid_cap > 0 ? grid_cap : nsm * 8;
-  const int grid = grid_for(a.n, kWarps * gpw, cap);
-  switch (R) {
-    case 1: SpmmV<1, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 2: SpmmV<2, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 3: SpmmV<3, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 4: SpmmV<4, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 5: SpmmV<5, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 6: SpmmV<6, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 7: SpmmV<7, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    case 8: SpmmV<8, MODE>::run(a, vc, pre, sigma, grid, s); break;
-    default: return SAD_EINVAL;
-  }
   return SAD_OK;
 }
 
@@ -1004,63 +912,42 @@ extern "C" int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host) 
 }
 
 // ---- persistent (cooperative) engine ------------------------------------------
-template <typename XT, typename VT, int R, bool SIGMA, bool FLEX>
-static cudaError_t coop_launch_t(PArgs<XT> a, sad_gmres* ws, cudaStream_t s, size_t smem) {
-  auto kern = k_gmres_persistent<XT, VT, R, true, SIGMA, FLEX>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int nb = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (nb < 1) return cudaErrorInvalidConfiguration;
-  const int nsm = ws->ctx->nsm;
-  const int sms = ws->max_sms > 0 ? std::min(ws->max_sms, nsm) : nsm;
-  const long long elems = a.n * R;
-  const long long per_block = (long long)kThreads * std::max(1, ws->min_elems_per_thread);
-  long long grid = (elems + per_block - 1) / per_block;
-  grid = std::max(1LL, std::min(grid, (long long)nb * sms));
-  grid = std::min(grid, (long long)ws->max_blocks);
-  a.rows_per_block = (a.n + grid - 1) / grid;
-  a.pT = ws->max_blocks;
-  a.prof = ws->profile || ws->timers;
-  void* args[] = {(void*)&a};
-  e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
+static CoopCfg coop_cfg(const sad_gmres* ws) {
+  CoopCfg c;
+  c.nsm = ws->ctx->nsm;
+  c.max_sms = ws->max_sms;
+  c.min_elems_per_thread = ws->min_elems_per_thread;
+  c.max_blocks = ws->max_blocks;
+  return c;
+}
+
+static cudaError_t coop_dispatch_d(PArgs<double> a, sad_gmres* ws, sad_op* op,
+                                   cudaStream_t s, size_t smem) {
+  const CoopCfg c = coop_cfg(ws);
+  const int R = ws->R;
+  int g = 0;
+  cudaError_t e;
+  if (op->sigma_identity)
+    e = ws->flexible ? coop_launch_d_s1_f1(R, a, c, s, smem, &g) : coop_launch_d_s1_f0(R, a, c, s, smem, &g);
+  else
+    e = ws->flexible ? coop_launch_d_s0_f1(R, a, c, s, smem, &g) : coop_launch_d_s0_f0(R, a, c, s, smem, &g);
   COUNT_LAUNCH(1);
   return e;
 }
-
-template <typename XT, typename VT, bool SIGMA, bool FLEX>
-static cudaError_t coop_R(int R, const PArgs<XT>& a, sad_gmres* ws, cudaStream_t s, size_t smem) {
-  switch (R) {
-    case 1: return coop_launch_t<XT, VT, 1, SIGMA, FLEX>(a, ws, s, smem);
-    case 2: return coop_launch_t<XT, VT, 2, SIGMA, FLEX>(a, ws, s, smem);
-    case 3: return coop_launch_t<XT, VT, 3, SIGMA, FLEX>(a, ws, s, smem);
-    case 4: return coop_launch_t<XT, VT, 4, SIGMA, FLEX>(a, ws, s, smem);
-    case 5: return coop_launch_t<XT, VT, 5, SIGMA, FLEX>(a, ws, s, smem);
-    case 6: return coop_launch_t<XT, VT, 6, SIGMA, FLEX>(a, ws, s, smem);
-    case 7: return coop_launch_t<XT, VT, 7, SIGMA, FLEX>(a, ws, s, smem);
-    case 8: return coop_launch_t<XT, VT, 8, SIGMA, FLEX>(a, ws, s, smem);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <typename XT, typename VT, bool SIGMA>
-static cudaError_t coop_flex(bool flex, int R, const PArgs<XT>& a, sad_gmres* ws, cudaStream_t s,
-                             size_t smem) {
-  return flex ? coop_R<XT, VT, SIGMA, true>(R, a, ws, s, smem)
-              : coop_R<XT, VT, SIGMA, false>(R, a, ws, s, smem);
-}
-
-static cudaError_t coop_dispatch_d(const PArgs<double>& a, sad_gmres* ws, sad_op* op,
+static cudaError_t coop_dispatch_z(PArgs<double2> a, sad_gmres* ws, sad_op* op,
                                    cudaStream_t s, size_t smem) {
-  return op->sigma_identity ? coop_flex<double, double, true>(ws->flexible, ws->R, a, ws, s, smem)
-                            : coop_flex<double, double, false>(ws->flexible, ws->R, a, ws, s, smem);
-}
-static cudaError_t coop_dispatch_z(const PArgs<double2>& a, sad_gmres* ws, sad_op* op,
-                                   cudaStream_t s, size_t smem) {
-  if (op->vals_complex) return coop_flex<double2, double2, false>(ws->flexible, ws->R, a, ws, s, smem);
-  return op->sigma_identity ? coop_flex<double2, double, true>(ws->flexible, ws->R, a, ws, s, smem)
-                            : coop_flex<double2, double, false>(ws->flexible, ws->R, a, ws, s, smem);
+  const CoopCfg c = coop_cfg(ws);
+  const int R = ws->R;
+  int g = 0;
+  cudaError_t e;
+  if (op->vals_complex)
+    e = ws->flexible ? coop_launch_zc_s0_f1(R, a, c, s, smem, &g) : coop_launch_zc_s0_f0(R, a, c, s, smem, &g);
+  else if (op->sigma_identity)
+    e = ws->flexible ? coop_launch_z_s1_f1(R, a, c, s, smem, &g) : coop_launch_z_s1_f0(R, a, c, s, smem, &g);
+  else
+    e = ws->flexible ? coop_launch_z_s0_f1(R, a, c, s, smem, &g) : coop_launch_z_s0_f0(R, a, c, s, smem, &g);
+  COUNT_LAUNCH(1);
+  return e;
 }
 
 template <typename XT>
@@ -1079,6 +966,7 @@ static PArgs<XT> make_pargs(sad_gmres* ws, sad_op* op, const void* rhs, void* x)
   a.Z = reinterpret_cast<XT*>(ws->Z);
   a.stride = ws->n * ws->R;
   a.st = ws->pst;
+  a.prof = ws->profile || ws->timers;
   return a;
 }
 

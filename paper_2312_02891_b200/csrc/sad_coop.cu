@@ -1,0 +1,78 @@
+// sad_coop.cu -- one variant of the cooperative persistent GMRES launcher
+// (see sad_coop.cuh).  Compiled once per -DSAD_COOP_VARIANT=<n> (0..9) by
+// paper_2312_02891_b200/_build.py.
+#include "sad_coop.cuh"
+
+#ifndef SAD_COOP_VARIANT
+#error "compile with -DSAD_COOP_VARIANT=<0..9>"
+#endif
+
+namespace sad {
+
+template <typename XT, typename VT, int R, bool SIGMA, bool FLEX>
+static cudaError_t coop_launch_t(PArgs<XT> a, const CoopCfg& cfg, cudaStream_t s, size_t smem,
+                                 int* grid_out) {
+  auto kern = k_gmres_persistent<XT, VT, R, true, SIGMA, FLEX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int nb = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (nb < 1) return cudaErrorInvalidConfiguration;
+  const int sms = cfg.max_sms > 0 ? (cfg.max_sms < cfg.nsm ? cfg.max_sms : cfg.nsm) : cfg.nsm;
+  const long long elems = a.n * R;
+  const long long per_block = (long long)kThreads * (cfg.min_elems_per_thread > 1 ? cfg.min_elems_per_thread : 1);
+  long long grid = (elems + per_block - 1) / per_block;
+  if (grid > (long long)nb * sms) grid = (long long)nb * sms;
+  if (grid > (long long)cfg.max_blocks) grid = cfg.max_blocks;
+  if (grid < 1) grid = 1;
+  a.rows_per_block = (a.n + grid - 1) / grid;
+  a.pT = cfg.max_blocks;
+  void* args[] = {(void*)&a};
+  if (grid_out) *grid_out = (int)grid;
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kThreads), args,
+                                     smem, s);
+}
+
+#define SAD_COOP_DEF(tag, XT, VT, SIGMA, FLEX)                                               \
+  cudaError_t coop_launch_##tag(int R, PArgs<XT> a, const CoopCfg& cfg, cudaStream_t s,     \
+                                size_t smem, int* grid_out) {                               \
+    switch (R) {                                                                            \
+      case 1: return coop_launch_t<XT, VT, 1, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 2: return coop_launch_t<XT, VT, 2, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 3: return coop_launch_t<XT, VT, 3, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 4: return coop_launch_t<XT, VT, 4, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 5: return coop_launch_t<XT, VT, 5, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 6: return coop_launch_t<XT, VT, 6, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 7: return coop_launch_t<XT, VT, 7, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+      case 8: return coop_launch_t<XT, VT, 8, SIGMA, FLEX>(a, cfg, s, smem, grid_out);      \
+    }                                                                                       \
+    return cudaErrorInvalidValue;                                                           \
+  }
+
+// the SAD_COOP_VARIANT-th entry of SAD_COOP_VARIANTS
+#if SAD_COOP_VARIANT == 0
+SAD_COOP_DEF(d_s0_f0, double, double, false, false)
+#elif SAD_COOP_VARIANT == 1
+SAD_COOP_DEF(d_s0_f1, double, double, false, true)
+#elif SAD_COOP_VARIANT == 2
+SAD_COOP_DEF(d_s1_f0, double, double, true, false)
+#elif SAD_COOP_VARIANT == 3
+SAD_COOP_DEF(d_s1_f1, double, double, true, true)
+#elif SAD_COOP_VARIANT == 4
+SAD_COOP_DEF(z_s0_f0, double2, double, false, false)
+#elif SAD_COOP_VARIANT == 5
+SAD_COOP_DEF(z_s0_f1, double2, double, false, true)
+#elif SAD_COOP_VARIANT == 6
+SAD_COOP_DEF(z_s1_f0, double2, double, true, false)
+#elif SAD_COOP_VARIANT == 7
+SAD_COOP_DEF(z_s1_f1, double2, double, true, true)
+#elif SAD_COOP_VARIANT == 8
+SAD_COOP_DEF(zc_s0_f0, double2, double2, false, false)
+#elif SAD_COOP_VARIANT == 9
+SAD_COOP_DEF(zc_s0_f1, double2, double2, false, true)
+#else
+#error "SAD_COOP_VARIANT out of range"
+#endif
+
+}  // namespace sad

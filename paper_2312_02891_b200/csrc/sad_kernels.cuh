@@ -184,7 +184,7 @@ __device__ __forceinline__ double block_sum_partials(const double* part, int pst
 // finishers (run by the last block)
 // ----------------------------------------------------------------------------
 // After the true residual V_0 = b - Op x: restart decision.
-__device__ void fin_cycle(const GState& st, const double* n2) {
+static __device__ void fin_cycle(const GState& st, const double* n2) {
   const int R = st.R;
   if (threadIdx.x < R) {
     int c = threadIdx.x;
@@ -211,7 +211,7 @@ __device__ void fin_cycle(const GState& st, const double* n2) {
 }
 
 // After pass-2 update with ||w||^2: Hessenberg column, Givens, stopping test.
-__device__ void fin_givens(const GState& st, const double* n2) {
+static __device__ void fin_givens(const GState& st, const double* n2) {
   const int R = st.R, m = st.m;
   const int j = *st.j;
   if (threadIdx.x < R) {
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kThreads) k_update(OrthArgs a) {
 // ----------------------------------------------------------------------------
 // cycle end: back substitution of the rotated Hessenberg, x-update coefficients
 // ----------------------------------------------------------------------------
-__global__ void k_trisolve(GState st, int flexible) {
+static __global__ void k_trisolve(GState st, int flexible) {
   const int R = st.R, m = st.m;
   const int c = threadIdx.x;
   if (c < R) {
@@ -682,7 +682,7 @@ __global__ void k_trisolve(GState st, int flexible) {
 }
 
 // solve start: counters and flags
-__global__ void k_init(GState st) {
+static __global__ void k_init(GState st) {
   if (threadIdx.x < st.R) {
     st.iters[threadIdx.x] = 0;
     st.done[threadIdx.x] = 0;
@@ -777,7 +777,7 @@ __global__ void k_jacobi(long long n, const int* rowptr, const int* colidx, cons
   }
 }
 
-__global__ void k_c2r(long long n, const double2* in, double* out) {
+static __global__ void k_c2r(long long n, const double2* in, double* out) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     out[i] = in[i].x;

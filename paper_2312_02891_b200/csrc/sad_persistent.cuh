@@ -149,7 +149,7 @@ __device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
 // Deterministic reduction of per-block partials stored OUTPUT-MAJOR:
 // partT[o * pT + b] (complex).  One warp per output: lane l sums blocks
 // l, l+32, ... (coalesced, independent loads), then a fixed shuffle tree.
-__device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int nout,
+static __device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int nout,
                                   double2* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int OB = 4;   // outputs in flight per warp
@@ -181,7 +181,7 @@ __device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int
 // nout <= 8 outputs: every thread loads its blocks' partials for all outputs
 // (one round of independent loads), then a fixed shuffle tree per warp and a
 // fixed-order sum over warps.
-__device__ void reduce_partials_small(const double2* partT, int pT, int nblocks, int nout,
+static __device__ void reduce_partials_small(const double2* partT, int pT, int nblocks, int nout,
                                       double2* out) {
   __shared__ double2 s_ws[kWarps][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
