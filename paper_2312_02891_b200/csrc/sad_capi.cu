@@ -112,6 +112,7 @@ struct sad_gmres {
   int engine = SAD_ENGINE_PERSISTENT;
   int max_sms = 0;              // 0 = all SMs
   int min_elems_per_thread = 2;
+  int direct_a = -1;            // phase-A path: -1 auto, 0 TMA ring, 1 direct loads
   PState pst{};
   double* stats_dev = nullptr;
   // profiling (sad_gmres_profile): synchronous stepping with CUDA events
@@ -994,14 +995,23 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   }
   const size_t m1 = ws->m + 1;
   const size_t R = ws->R;
-  // finisher-A staging: sums (2(m+1)+1)R, h1, Gram column, S, flags, old Gram block
-  const size_t finA = ((2 * m1 + 1) * R + 2 * m1 * R) * 16 + m1 * R * 8 + 8 * 4 + 64;
+  // finisher-A staging: sums (2(m+1)+1)R, h1, Gram column, rotations (sn, cs), S,
+  // flags, old Gram block
+  const size_t finA = ((2 * m1 + 1) * R + 2 * m1 * R + ws->m * R) * 16 + (m1 + ws->m) * R * 8 +
+                      8 * 4 + 64;
   const size_t gblk = R * m1 * m1 * 16;
   const bool g_smem = finA + gblk <= 200 * 1024;
   // phase-A TMA stages: one block-tile (kWarps * GPW * UA rows) of one basis block
   const size_t gpw = 32 / R, ua = ws->esz == 8 ? 8 : 4;
-  const size_t stage = ((size_t)kWarps * gpw * ua * R * ws->esz + 32 + 127) & ~size_t(127);
-  size_t smem = std::max({(size_t)kStages * stage + 2 * m1 * R * ws->esz,   // ring + sums
+  const size_t tile_rows = (size_t)kWarps * gpw * ua;
+  // Direct phase A when every block owns at most two tiles even at one block
+  // per SM (latency-bound small slabs); else the TMA ring.
+  const int sms = ws->max_sms > 0 ? std::min(ws->max_sms, ctx->nsm) : ctx->nsm;
+  const bool direct = ws->direct_a >= 0 ? ws->direct_a != 0
+                                        : (size_t)ws->n <= 2 * tile_rows * (size_t)sms;
+  const size_t stage = direct ? 0 : ((tile_rows * R * ws->esz + 32 + 127) & ~size_t(127));
+  const size_t sums = 2 * m1 * R * ws->esz * (direct ? 1 + kWarps : 1);
+  size_t smem = std::max({(size_t)kStages * stage + sums,                 // ring + sums
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
                           finA + (g_smem ? gblk : 0)});
@@ -1010,11 +1020,13 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
+    a.direct_a = direct ? 1 : 0;
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
+    a.direct_a = direct ? 1 : 0;
     e = coop_dispatch_z(a, ws, op, s, smem);
   }
   if (e != cudaSuccess)
@@ -1060,6 +1072,10 @@ extern "C" int sad_gmres_set_option(sad_gmres* ws, int key, int value) {
     case SAD_OPT_MIN_ELEMS_PER_THREAD:
       if (value < 1) return set_err(ws->ctx, SAD_EINVAL, "min elements per thread must be >= 1");
       ws->min_elems_per_thread = value;
+      return SAD_OK;
+    case SAD_OPT_DIRECT_A:
+      if (value < -1 || value > 1) return set_err(ws->ctx, SAD_EINVAL, "direct-A option must be -1, 0 or 1");
+      ws->direct_a = value;
       return SAD_OK;
   }
   return set_err(ws->ctx, SAD_EINVAL, "unknown option %d", key);

@@ -63,6 +63,7 @@ struct PArgs {
   int prof;              // record phase timers
   int g_smem;            // stage the Gram block in shared memory (fits)
   int stage_bytes;       // bytes of one phase-A TMA stage (128-aligned)
+  int direct_a;          // phase A with direct loads and per-warp sums (small slabs)
   PState st;
 };
 
@@ -147,27 +148,34 @@ __device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
 }
 
 // Deterministic reduction of per-block partials stored OUTPUT-MAJOR:
-// partT[o * pT + b] (complex).  One warp per output: lane l sums blocks
-// l, l+32, ... (coalesced, independent loads), then a fixed shuffle tree.
+// partT[o * pT + b] (complex).  One warp per OB outputs: lane l sums blocks
+// l, l+32, ... (coalesced; the KB loads per output of a chunk of 32*KB blocks
+// are all issued before the first add, so a chunk costs one L2 round trip),
+// then a fixed shuffle tree.
 static __device__ void reduce_partials_T(const double2* partT, int pT, int nblocks, int nout,
-                                  double2* out) {
+                                         double2* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int OB = 4;   // outputs in flight per warp
+  constexpr int OB = 4;   // outputs per warp
+  constexpr int KB = 5;   // 32-block groups per load round (160 blocks)
   for (int o0 = warp * OB; o0 < nout; o0 += kWarps * OB) {
     double2 acc[OB];
 #pragma unroll
     for (int q = 0; q < OB; ++q) acc[q] = make_double2(0.0, 0.0);
-    for (int b = lane; b < nblocks; b += 64) {
-      double2 v0[OB], v1[OB];
+    for (int b0 = 0; b0 < nblocks; b0 += 32 * KB) {
+      double2 v[OB][KB];
 #pragma unroll
       for (int q = 0; q < OB; ++q) {
-        const bool ok = o0 + q < nout;
-        const double2* p = partT + (size_t)(o0 + q) * pT;
-        v0[q] = ok ? __ldcg(p + b) : make_double2(0.0, 0.0);
-        v1[q] = (ok && b + 32 < nblocks) ? __ldcg(p + b + 32) : make_double2(0.0, 0.0);
+        const double2* p = partT + (size_t)min(o0 + q, nout - 1) * pT;
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+          const int b = b0 + k * 32 + lane;
+          v[q][k] = (o0 + q < nout && b < nblocks) ? __ldcg(p + b) : make_double2(0.0, 0.0);
+        }
       }
 #pragma unroll
-      for (int q = 0; q < OB; ++q) acc[q] = add(add(acc[q], v0[q]), v1[q]);
+      for (int q = 0; q < OB; ++q)
+#pragma unroll
+        for (int k = 0; k < KB; ++k) acc[q] = add(acc[q], v[q][k]);
     }
 #pragma unroll
     for (int q = 0; q < OB; ++q) {
@@ -334,107 +342,182 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         double w2 = 0.0;
         __syncthreads();
         constexpr int T = kWarps * GPW * UA;   // rows per block-tile
-        for (long long base = r0; base < r1; base += T) {
-          const long long nrows = min((long long)T, r1 - base);
-          auto issue = [&](int i, int q) {
-            const unsigned long long src =
-                reinterpret_cast<unsigned long long>(a.V + (long long)i * a.stride + base * R);
-            const unsigned long long e = src + (unsigned long long)(nrows * R) * sizeof(XT);
-            const unsigned long long a0 = src & ~15ull, a1 = (e + 15ull) & ~15ull;
-            s_soff[q] = (int)((src - a0) / sizeof(XT));
-            mbar_expect_tx(s_full + q, (unsigned)(a1 - a0));
-            bulk_g2s(smem_c + (size_t)q * a.stage_bytes, reinterpret_cast<const void*>(a0),
-                     (unsigned)(a1 - a0), s_full + q);
-          };
-          if (threadIdx.x == 0) {
-            fence_proxy_async();
-            for (int i = 0; i < min(kStages, J); ++i) issue(i, (int)((ring + i) % kStages));
-          }
-          // the tile's SpMM (overlaps with the first basis copies)
-          XT wv[UA], xv[UA];
-          long long idx[UA];
-          int lr[UA];
+        if (a.direct_a) {
+          // Small slabs (one or two tiles per block): every warp sweeps the
+          // basis for its own rows with direct loads (IB blocks in flight) and
+          // keeps its per-basis-block sums in its own shared-memory slots, so
+          // the block synchronises once per phase instead of once per group.
+          XT* s_wp = s_blk + 2 * J * R;   // [2J][kWarps][R]
+          for (int o = threadIdx.x; o < 2 * J * kWarps * R; o += kThreads) s_wp[o] = zero<XT>();
+          __syncthreads();
+          constexpr int UD = UA / 2;                 // rows per lane per direct tile
+          constexpr int TD = kWarps * GPW * UD;
+          for (long long base = r0; base < r1; base += TD) {
+            const long long nrows = min((long long)TD, r1 - base);
+            XT wv[UD], xv[UD];
+            long long idx[UD];
 #pragma unroll
-          for (int u = 0; u < UA; ++u) {
-            lr[u] = (u * kWarps + warp) * GPW + grp;
-            const long long row = base + lr[u];
-            idx[u] = (lane_ok && lr[u] < nrows) ? row * R + c : -1;
-          }
-          spmm_rows<XT, VT, PRE, SIGMA, R, UA>(a.rowptr, a.colidx,
-                                               reinterpret_cast<const VT*>(a.vals), a.dinv,
-                                               a.sigma, vj, idx, c, wv, xv);
-#pragma unroll
-          for (int u = 0; u < UA; ++u) {
-            if (idx[u] >= 0) {
-              wv[u] = sscal(sj, wv[u]);
-              w[idx[u]] = wv[u];
-              if (FLEX) {
-                XT zi = PRE ? mul(__ldg(a.dinv + idx[u] / R), xv[u]) : xv[u];
-                a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
-              }
-              w2 += abs2(wv[u]);
+            for (int u = 0; u < UD; ++u) {
+              const int lr = (u * kWarps + warp) * GPW + grp;
+              idx[u] = (lane_ok && lr < nrows) ? (base + lr) * R + c : -1;
             }
-          }
-          // basis blocks in groups of kGroup per __syncthreads (the other half of
-          // the ring is in flight meanwhile)
-          for (int i0 = 0; i0 < J; i0 += kGroup) {
-            const int ng = min(kGroup, J - i0);
-            XT ph[kGroup], pg[kGroup];
+            spmm_rows<XT, VT, PRE, SIGMA, R, UD>(a.rowptr, a.colidx,
+                                                 reinterpret_cast<const VT*>(a.vals), a.dinv,
+                                                 a.sigma, vj, idx, c, wv, xv);
 #pragma unroll
-            for (int gi = 0; gi < kGroup; ++gi) {
-              ph[gi] = zero<XT>();
-              pg[gi] = zero<XT>();
-              if (gi < ng) {
-                const long long kk = ring + i0 + gi;
-                const int q = (int)(kk % kStages);
-                mbar_wait(s_full + q, (unsigned)((kk / kStages) & 1));
-                const XT* Vs =
-                    reinterpret_cast<const XT*>(smem_c + (size_t)q * a.stage_bytes) + s_soff[q];
+            for (int u = 0; u < UD; ++u) {
+              if (idx[u] >= 0) {
+                wv[u] = sscal(sj, wv[u]);
+                w[idx[u]] = wv[u];
+                if (FLEX) {
+                  XT zi = PRE ? mul(__ldg(a.dinv + idx[u] / R), xv[u]) : xv[u];
+                  a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
+                }
+                w2 += abs2(wv[u]);
+              }
+            }
+            constexpr int IBD = 4;   // basis blocks in flight
+            for (int i0 = 0; i0 < J; i0 += IBD) {
+              XT vb[IBD][UD];
 #pragma unroll
-                for (int u = 0; u < UA; ++u) {
-                  if (idx[u] >= 0) {
-                    const XT v = Vs[lr[u] * R + c];
-                    ph[gi] = cfma(v, wv[u], ph[gi]);
-                    pg[gi] = cfma(v, xv[u], pg[gi]);
+              for (int ib = 0; ib < IBD; ++ib) {
+                const XT* Vi = a.V + (long long)min(i0 + ib, J - 1) * a.stride;
+#pragma unroll
+                for (int u = 0; u < UD; ++u)
+                  vb[ib][u] = (idx[u] >= 0 && i0 + ib < J) ? Vi[idx[u]] : zero<XT>();
+              }
+#pragma unroll
+              for (int ib = 0; ib < IBD; ++ib) {
+                if (i0 + ib < J) {
+                  XT ph = zero<XT>(), pg = zero<XT>();
+#pragma unroll
+                  for (int u = 0; u < UD; ++u) {
+                    ph = cfma(vb[ib][u], wv[u], ph);
+                    pg = cfma(vb[ib][u], xv[u], pg);
+                  }
+                  ph = group_reduce<R>(ph, grp);
+                  pg = group_reduce<R>(pg, grp);
+                  if (grp == 0 && lane_ok) {
+                    XT* ph_s = s_wp + ((size_t)(i0 + ib) * kWarps + warp) * R + c;
+                    XT* pg_s = s_wp + ((size_t)(J + i0 + ib) * kWarps + warp) * R + c;
+                    *ph_s = add(*ph_s, ph);
+                    *pg_s = add(*pg_s, pg);
                   }
                 }
               }
             }
+          }
+          __syncthreads();
+          for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) {
+            const int ii = o / R, cc = o - ii * R;
+            XT t = zero<XT>();
 #pragma unroll
-            for (int gi = 0; gi < kGroup; ++gi) {
-              if (gi < ng) {
-                const XT h = group_reduce<R>(ph[gi], grp);
-                const XT gq = group_reduce<R>(pg[gi], grp);
-                if (grp == 0 && lane_ok) {
-                  s_ph[gi][warp][c] = h;
-                  s_pg[gi][warp][c] = gq;
-                }
-              }
-            }
-            __syncthreads();
-            if (warp == 0 && lane < R) {
-              for (int gi = 0; gi < ng; ++gi) {
-                const int i = i0 + gi;
-                XT th = s_blk[i * R + lane], tg = s_blk[(J + i) * R + lane];
-#pragma unroll
-                for (int wq = 0; wq < kWarps; ++wq) {
-                  th = add(th, s_ph[gi][wq][lane]);
-                  tg = add(tg, s_pg[gi][wq][lane]);
-                }
-                s_blk[i * R + lane] = th;
-                s_blk[(J + i) * R + lane] = tg;
-              }
-            }
+            for (int wq = 0; wq < kWarps; ++wq) t = add(t, s_wp[((size_t)ii * kWarps + wq) * R + cc]);
+            s_blk[o] = t;
+          }
+        } else {
+          for (long long base = r0; base < r1; base += T) {
+            const long long nrows = min((long long)T, r1 - base);
+            auto issue = [&](int i, int q) {
+              const unsigned long long src =
+                  reinterpret_cast<unsigned long long>(a.V + (long long)i * a.stride + base * R);
+              const unsigned long long e = src + (unsigned long long)(nrows * R) * sizeof(XT);
+              const unsigned long long a0 = src & ~15ull, a1 = (e + 15ull) & ~15ull;
+              s_soff[q] = (int)((src - a0) / sizeof(XT));
+              mbar_expect_tx(s_full + q, (unsigned)(a1 - a0));
+              bulk_g2s(smem_c + (size_t)q * a.stage_bytes, reinterpret_cast<const void*>(a0),
+                       (unsigned)(a1 - a0), s_full + q);
+            };
             if (threadIdx.x == 0) {
               fence_proxy_async();
-              for (int gi = 0; gi < ng; ++gi) {
-                const int i = i0 + gi;
-                if (i + kStages < J) issue(i + kStages, (int)((ring + i) % kStages));
+              for (int i = 0; i < min(kStages, J); ++i) issue(i, (int)((ring + i) % kStages));
+            }
+            // the tile's SpMM (overlaps with the first basis copies)
+            XT wv[UA], xv[UA];
+            long long idx[UA];
+            int lr[UA];
+  #pragma unroll
+            for (int u = 0; u < UA; ++u) {
+              lr[u] = (u * kWarps + warp) * GPW + grp;
+              const long long row = base + lr[u];
+              idx[u] = (lane_ok && lr[u] < nrows) ? row * R + c : -1;
+            }
+            spmm_rows<XT, VT, PRE, SIGMA, R, UA>(a.rowptr, a.colidx,
+                                                 reinterpret_cast<const VT*>(a.vals), a.dinv,
+                                                 a.sigma, vj, idx, c, wv, xv);
+  #pragma unroll
+            for (int u = 0; u < UA; ++u) {
+              if (idx[u] >= 0) {
+                wv[u] = sscal(sj, wv[u]);
+                w[idx[u]] = wv[u];
+                if (FLEX) {
+                  XT zi = PRE ? mul(__ldg(a.dinv + idx[u] / R), xv[u]) : xv[u];
+                  a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
+                }
+                w2 += abs2(wv[u]);
               }
             }
-            __syncthreads();   // s_ph/s_pg reused by the next group
+            // basis blocks in groups of kGroup per __syncthreads (the other half of
+            // the ring is in flight meanwhile)
+            for (int i0 = 0; i0 < J; i0 += kGroup) {
+              const int ng = min(kGroup, J - i0);
+              XT ph[kGroup], pg[kGroup];
+  #pragma unroll
+              for (int gi = 0; gi < kGroup; ++gi) {
+                ph[gi] = zero<XT>();
+                pg[gi] = zero<XT>();
+                if (gi < ng) {
+                  const long long kk = ring + i0 + gi;
+                  const int q = (int)(kk % kStages);
+                  mbar_wait(s_full + q, (unsigned)((kk / kStages) & 1));
+                  const XT* Vs =
+                      reinterpret_cast<const XT*>(smem_c + (size_t)q * a.stage_bytes) + s_soff[q];
+  #pragma unroll
+                  for (int u = 0; u < UA; ++u) {
+                    if (idx[u] >= 0) {
+                      const XT v = Vs[lr[u] * R + c];
+                      ph[gi] = cfma(v, wv[u], ph[gi]);
+                      pg[gi] = cfma(v, xv[u], pg[gi]);
+                    }
+                  }
+                }
+              }
+  #pragma unroll
+              for (int gi = 0; gi < kGroup; ++gi) {
+                if (gi < ng) {
+                  const XT h = group_reduce<R>(ph[gi], grp);
+                  const XT gq = group_reduce<R>(pg[gi], grp);
+                  if (grp == 0 && lane_ok) {
+                    s_ph[gi][warp][c] = h;
+                    s_pg[gi][warp][c] = gq;
+                  }
+                }
+              }
+              __syncthreads();
+              if (warp == 0 && lane < R) {
+                for (int gi = 0; gi < ng; ++gi) {
+                  const int i = i0 + gi;
+                  XT th = s_blk[i * R + lane], tg = s_blk[(J + i) * R + lane];
+  #pragma unroll
+                  for (int wq = 0; wq < kWarps; ++wq) {
+                    th = add(th, s_ph[gi][wq][lane]);
+                    tg = add(tg, s_pg[gi][wq][lane]);
+                  }
+                  s_blk[i * R + lane] = th;
+                  s_blk[(J + i) * R + lane] = tg;
+                }
+              }
+              if (threadIdx.x == 0) {
+                fence_proxy_async();
+                for (int gi = 0; gi < ng; ++gi) {
+                  const int i = i0 + gi;
+                  if (i + kStages < J) issue(i + kStages, (int)((ring + i) % kStages));
+                }
+              }
+              __syncthreads();   // s_ph/s_pg reused by the next group
+            }
+            ring += J;
           }
-          ring += J;
         }
         w2 = group_reduce<R>(w2, grp);
         if (grp == 0 && lane_ok) s_w2[warp][c] = w2;
@@ -453,10 +536,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           double2* s_red = reinterpret_cast<double2*>(smem_p);
           double2* s_h1 = s_red + nout;
           double2* s_gc = s_h1 + J * R;
-          double* s_S = reinterpret_cast<double*>(s_gc + J * R);
-          int* s_act = reinterpret_cast<int*>(s_S + J * R);
-          for (int o = threadIdx.x; o < J * R; o += kThreads) s_S[o] = gs.S[o];
-          if (threadIdx.x < R) s_act[threadIdx.x] = gs.active[threadIdx.x];
+          double2* s_snr = s_gc + J * R;                            // [R][j] previous rotations
+          double* s_S = reinterpret_cast<double*>(s_snr + j * R);
+          double* s_csr = s_S + J * R;                              // [R][j]
+          int* s_act = reinterpret_cast<int*>(s_csr + j * R);
+          double2* s_G = reinterpret_cast<double2*>(
+              (reinterpret_cast<uintptr_t>(s_act + 8) + 15) & ~uintptr_t(15));
+          const bool gsm = a.g_smem != 0;
+          // everything the finisher reads besides the partials, in one round of
+          // independent loads issued before the reduction
+          for (int o = threadIdx.x; o < J * R; o += kThreads) s_S[o] = ldcg1(gs.S + o);
+          if (threadIdx.x < R) s_act[threadIdx.x] = ldcgi(gs.active + threadIdx.x);
+          for (int o = threadIdx.x; o < j * R; o += kThreads) {
+            const int cc = o / j, ii = o - cc * j;
+            s_snr[cc * j + ii] = ldcg2(gs.sn + (size_t)cc * m + ii);
+            s_csr[cc * j + ii] = ldcg1(gs.cs + (size_t)cc * m + ii);
+          }
+          if (gsm) {
+            for (int o = threadIdx.x; o < R * j * j; o += kThreads) {
+              const int cc = o / (j * j), rem = o - cc * j * j, ii = rem / j, l = rem - ii * j;
+              s_G[o] = ldcg2(st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1) + l);
+            }
+          }
           reduce_partials_T(partT, pT, gridDim.x, nout, s_red);
           __syncthreads();
           // new Gram column G[:, j] and h1 = S h_raw
@@ -480,16 +581,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           // The old G block is staged in smem with one parallel load when it
           // fits (a.g_smem), else read from global.  Four independent partial
           // sums per output, combined in a fixed order.
-          double2* s_G = reinterpret_cast<double2*>(
-              (reinterpret_cast<uintptr_t>(s_act + 8) + 15) & ~uintptr_t(15));
-          const bool gsm = a.g_smem != 0;
-          if (gsm) {
-            for (int o = threadIdx.x; o < R * j * j; o += kThreads) {
-              const int cc = o / (j * j), rem = o - cc * j * j, ii = rem / j, l = rem - ii * j;
-              s_G[o] = st.G[(size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1) + l];
-            }
-            __syncthreads();
-          }
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
             const int ii = o / R, cc = o - ii * R;
             double2 gh0 = make_double2(0.0, 0.0), gh1 = gh0, gh2 = gh0, gh3 = gh0;
@@ -520,16 +611,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           __syncthreads();
           // Apply the previous Givens rotations to the new Hessenberg column now
           // (they do not depend on h_{j+1,j}), so the phase-C finisher only has to
-          // form the new rotation.  Rotations staged in smem (s_h1 / s_S reused).
+          // form the new rotation.
           {
-            double2* s_snr = s_h1;                                    // [R][j]
-            double* s_csr = s_S;                                      // [R][j]
-            for (int o = threadIdx.x; o < j * R; o += kThreads) {
-              const int cc = o / j, ii = o - cc * j;
-              s_snr[cc * j + ii] = gs.sn[(size_t)cc * m + ii];
-              s_csr[cc * j + ii] = gs.cs[(size_t)cc * m + ii];
-            }
-            __syncthreads();
             if (threadIdx.x < R && s_act[threadIdx.x]) {
               const int cc = threadIdx.x;
               double2 x0 = s_red[cc];
@@ -598,19 +681,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         if (timing && prof) t_acc[5] += (double)(gtimer() - tphase);
         if (bar_arrive(st, gen)) {
           const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
-          reduce_partials_small(partT, pT, gridDim.x, R, st.red);
-          // per-column scalars, loaded together (one round trip)
+          // per-column scalars, loaded together and before the reduction (one
+          // round trip overlapping it)
           __shared__ int s_actn[8];
+          __shared__ double2 s_nrm[8];
+          int act_c = 0;
+          long long it_c = 0;
+          double wpre_c = 0.0;
+          double2 gj_c = make_double2(0.0, 0.0), hjj = gj_c;
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
-            const int act_c = gs.active[cc];
+            act_c = ldcgi(gs.active + cc);
+            it_c = __ldcg(gs.iters + cc);
+            wpre_c = ldcg1(gs.wpre2 + cc);
+            gj_c = ldcg2(gs.g + (size_t)cc * (m + 1) + j);
+            hjj = ldcg2(st.hc + j * R + cc);
+          }
+          reduce_partials_small(partT, pT, gridDim.x, R, s_nrm);
+          if (threadIdx.x < R) {
+            const int cc = threadIdx.x;
             s_actn[cc] = 0;
             if (act_c) {
-              const long long it_c = gs.iters[cc];
-              const double wpre_c = gs.wpre2[cc];
-              const double2 gj_c = gs.g[(size_t)cc * (m + 1) + j];
-              const double2 hjj = st.hc[j * R + cc];
-              const double hn = sqrt(st.red[cc].x);
+              const double hn = sqrt(s_nrm[cc].x);
               double cj; double2 sjv, rj;
               givens(hjj, make_double2(hn, 0.0), cj, sjv, rj);
               gs.cs[(size_t)cc * m + j] = cj;

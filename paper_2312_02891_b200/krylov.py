@@ -116,16 +116,21 @@ def validate_request(n, rhs, abs_tolerance):
     return rhs
 
 
+PHASE_A = {"auto": -1, "tma": 0, "direct": 1}
+
+
 class GpuGmresBinding:
     """Per-side GPU inner solver with shift-keyed operator cache (adi.py:422-488).
 
     Extra keyword-only knobs (no slot in the reference's AdiConfig):
-    ``restart`` (GMRES restart length m) and ``flexible`` (FGMRES form).
+    ``restart`` (GMRES restart length m) and ``flexible`` (FGMRES form);
+    engine tuning: ``engine``, ``max_sms`` and ``phase_a`` (persistent engine's
+    basis sweep: "tma" ring, "direct" loads for small slabs, or "auto").
     """
 
     def __init__(self, side, base, mass, mode="iterative", precond_kind="jacobi",
                  droptol=0.1, max_iterations=1000, *, restart=50, flexible=False,
-                 device=0, engine="persistent", max_sms=0):
+                 device=0, engine="persistent", max_sms=0, phase_a="auto"):
         if side not in ("A", "B"):
             raise ValueError("side must be 'A' or 'B'")
         if mode != "iterative":
@@ -145,6 +150,9 @@ class GpuGmresBinding:
         self.device = device
         self.engine = engine
         self.max_sms = int(max_sms)
+        if phase_a not in PHASE_A:
+            raise ValueError(f"phase_a must be one of {sorted(PHASE_A)}")
+        self.phase_a = phase_a
         adjoint = (side == "B")
         self.base = base if isinstance(base, DeviceMatrix) else DeviceMatrix(base, adjoint, device)
         self.mass = (None if mass is None else
@@ -178,6 +186,7 @@ class GpuGmresBinding:
             ws = _POOL.take((self.device, self.n, r, dtype, self.restart, self.flexible,
                              self.engine, self.max_sms))
             self._workspaces[key] = ws
+        ws.set_option(_lib.SAD_OPT_DIRECT_A, PHASE_A[self.phase_a])
         return ws
 
     def __del__(self):

@@ -131,7 +131,14 @@ def test_gram_and_axpy(rng, r):
 
 # -- GMRES solves against the oracle ---------------------------------------------------
 
-ENGINES = [("persistent", "dcgs2"), ("multi", "cgs2")]
+# persistent engine with each phase-A path (auto picks "direct" at these sizes)
+ENGINES = [("persistent", "dcgs2"), ("persistent-tma", "dcgs2"), ("multi", "cgs2")]
+
+
+def _binding_kw(engine):
+    if engine == "persistent-tma":
+        return dict(engine="persistent", phase_a="tma")
+    return dict(engine=engine)
 
 
 def _solve_both(mat, adjoint, shift, rhs, delta, restart, flexible=False, maxit=1000,
@@ -140,7 +147,7 @@ def _solve_both(mat, adjoint, shift, rhs, delta, restart, flexible=False, maxit=
     side = "B" if adjoint else "A"
     orth = dict(ENGINES)[engine]
     gb = GpuGmresBinding(side, mat, None, precond_kind=precond, max_iterations=maxit,
-                         restart=restart, flexible=flexible, engine=engine)
+                         restart=restart, flexible=flexible, **_binding_kw(engine))
     got = gb.solve(shift, rhs, delta)
     ob = orc.Binding(side, mat, None, solver="fgmres" if flexible else "gmres",
                      max_iterations=maxit, restart=restart, precond=precond, orth=orth)
@@ -186,7 +193,7 @@ def test_gmres_known_answers(rng, engine):
     from paper_2312_02891_b200 import GpuGmresBinding
     # identity: <= 1 iteration (test_krylov.py:15-20)
     b = rng.standard_normal((6, 1))
-    gb = GpuGmresBinding("A", sp.eye(6, format="csr"), None, restart=5, engine=engine)
+    gb = GpuGmresBinding("A", sp.eye(6, format="csr"), None, restart=5, **_binding_kw(engine))
     res = gb.solve(0.0, b, 1e-12)
     assert res.total_iterations <= 1 and np.max(np.abs(res.solution - b)) < 1e-12
     # loose tolerance: 0 iterations, zero solution (test_krylov.py:27-33)
@@ -196,7 +203,7 @@ def test_gmres_known_answers(rng, engine):
     # achieved norms are independent recomputes (test_krylov.py:45-54)
     d = rng.standard_normal((12, 12)) + 12 * np.eye(12)
     b = rng.standard_normal((12, 3))
-    gb = GpuGmresBinding("A", sp.csr_matrix(d), None, restart=10, engine=engine)
+    gb = GpuGmresBinding("A", sp.csr_matrix(d), None, restart=10, **_binding_kw(engine))
     res = gb.solve(0.0, b, 1e-8)
     for c in range(3):
         check = np.linalg.norm(b[:, c] - d @ res.solution[:, c])
@@ -238,7 +245,7 @@ def test_gmres_fixed_steps_match_oracle(rng, engine):
     from paper_2312_02891_b200 import GpuGmresBinding
     A = cfgs.convdiff_fd(2, 128, (100.0, 100.0))
     rhs = rng.standard_normal((A.shape[0], 8))
-    gb = GpuGmresBinding("A", A, None, restart=40, engine=engine)
+    gb = GpuGmresBinding("A", A, None, restart=40, **_binding_kw(engine))
     out = gb.solve_device(-5000.0, torch.from_numpy(rhs).cuda(), 1.0, fixed_steps=40)
     assert np.all(out.iterations == 40)
     ob = orc.Binding("A", A, None, solver="gmres", restart=40, max_iterations=40,
