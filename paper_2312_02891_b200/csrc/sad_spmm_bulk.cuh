@@ -54,13 +54,13 @@ __device__ __forceinline__ void fence_proxy_async() {
 #define SAD_BULK_ROWS 64       // target rows per tile (tuned: tools/spmm_tune.cu)
 #endif
 #ifndef SAD_BULK_STAGES
-#define SAD_BULK_STAGES 2      // TMA pipeline depth
+#define SAD_BULK_STAGES 4      // TMA pipeline depth
 #endif
 #ifndef SAD_BULK_KB
-#define SAD_BULK_KB 4          // nonzeros per row gathered per batch
+#define SAD_BULK_KB 5          // nonzeros per row gathered per batch
 #endif
 #ifndef SAD_BULK_MINB
-#define SAD_BULK_MINB 1        // __launch_bounds__ min blocks per SM (register cap)
+#define SAD_BULK_MINB 4        // __launch_bounds__ min blocks per SM (register cap)
 #endif
 template <int R>
 struct BulkTile {
@@ -95,8 +95,15 @@ __device__ __forceinline__ void aligned_range(const void* base, long long first,
 // Warp-specialised: warps 0..7 consume tiles, warp 8 is the TMA producer.
 // full[s]: armed by the producer with the stage's byte count; empty[s]: one
 // arrival per consumer warp when it is done with the stage.
+// Register cap: complex blocks with two rows per lane (R >= 7) need more than
+// the 56 registers of four blocks per SM.
+template <typename XT, int R>
+__host__ __device__ constexpr int bulk_min_blocks() {
+  return (sizeof(XT) == 16 && BulkTile<R>::U >= 2) ? 2 : SAD_BULK_MINB;
+}
+
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
-__global__ void __launch_bounds__(kThreads + 32, SAD_BULK_MINB) k_spmm_bulk(SpmmArgs<XT> a) {
+__global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spmm_bulk(SpmmArgs<XT> a) {
   using T = BulkTile<R>;
   constexpr int GPW = T::GPW, U = T::U, TR = T::TR, CAP = T::CAP, S = T::STAGES;
   extern __shared__ __align__(128) unsigned char smem_b[];
