@@ -52,6 +52,20 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback"
 
 
+TRAFFIC_FILE = os.path.join(REPO, "profiles", "traffic.json")
+
+
+def ncu_traffic(key):
+    """DRAM bytes per launch of a kernel from a committed ncu capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            ent = json.load(fh)[key]
+        return float(ent["traffic_bytes_per_launch"]), ent
+    except Exception:
+        return None, None
+
+
 # -- distributed plumbing --------------------------------------------------------
 
 class Dist:
@@ -277,6 +291,7 @@ def run_ours_c2(args, dist):
     peak, peak_kind = hbm_peak()
     kern_ms, kern_launches, kern_bytes = prof[0], prof[1], prof[2]
     ach = kern_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
+    traffic, tr_ent = ncu_traffic("c2_persistent")
     # e2e through the public API with host inputs
     e2e_times = []
     A, B, M, C, f, g, pairs, cyclic = raw
@@ -308,7 +323,10 @@ def run_ours_c2(args, dist):
             "sum_inner_A": rep.sum_inner_A, "sum_inner_B": rep.sum_inner_B,
             "inner": "Jacobi-FGMRES(30) batched per column, CGS2, device Givens"}),
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "traffic": None, "kernel": "k_gmres_persistent",
+                     "frac": ach / peak, "traffic": traffic, "kernel": "k_gmres_persistent",
+                     "traffic_source": tr_ent and (f"profiles/traffic.json[c2_persistent]: "
+                                                   f"{tr_ent['launches']} launches, "
+                                                   f"{tr_ent['note']}"),
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": kern_bytes / max(kern_launches, 1),
                      "avg_launch_ms": kern_ms / max(kern_launches, 1),
@@ -389,6 +407,8 @@ def run_ours_c4(args, dist):
     ck = clocks.stop()
     peak, peak_kind = hbm_peak()
     solve_gbs = tm[3] / (tm[0] * 1e-3) / 1e9
+    traffic, tr_ent = ncu_traffic("c4_spmm")
+    straffic, str_ent = ncu_traffic("c4_persistent")
     line = {"metric": "inner SpMM GB/s", "value": value, "unit": "GB/s",
             "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": spmm_ms, "higher_is_better": True,
@@ -398,11 +418,14 @@ def run_ours_c4(args, dist):
                                             "n": n, "nnz": int(A.nnz),
                                             "l2": "flushed between timed SpMMs"},
             "roofline": {"bound": "hbm", "achieved": spmm_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": spmm_gbs / peak, "traffic": None, "kernel": "k_spmm",
+                         "frac": spmm_gbs / peak, "traffic": traffic, "kernel": "k_spmm_bulk",
+                         "traffic_source": tr_ent and (f"profiles/traffic.json[c4_spmm]: "
+                                                       f"{tr_ent['note']}"),
                          "peak_kind": peak_kind, "algorithmic_bytes_per_launch": spmm_b},
             "inner_solve": {"kernel": "k_gmres_persistent", "steps": steps,
                             "kernel_ms": tm[0], "phaseA_ms": tm[1], "phaseC_ms": tm[2],
                             "algorithmic_bytes": tm[3], "gbs": solve_gbs,
+                            "traffic": straffic,
                             "frac": solve_gbs / peak,
                             "iterations_per_s": steps * r / (tm[0] * 1e-3)},
             "gpu_launches": int(launches), "clocks": ck}
