@@ -197,6 +197,21 @@ int sad_adi_epilogue(sad_ctx* ctx, int64_t nA, int64_t nB, int r, int dtype,
                      const void* resB_dev, void* t_dev, double* gram_host,
                      void* stream);
 
+/*
+ * Tall-skinny products over a low-rank factor X (n x K, row-major, leading
+ * dimension ldx >= K, F64 or C128) for the verification diagnostics: the
+ * power iteration of true_residual_norm (adi.py:682-726) evaluates
+ * `Y.conj().T @ x` and `Z @ c` (adi.py:692-705) with these.
+ *   sad_ts_hgemv: out_host[K][nvec] = X^H V   (V: n x nvec complex128 device
+ *                 block, nvec in {1, 2}; deterministic block-ordered sums)
+ *   sad_ts_gemv:  Y[n][nvec] (+)= X C        (C_host: K x nvec complex128;
+ *                 accumulate != 0 adds to Y; Y complex128 device block)
+ */
+int sad_ts_hgemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int xdtype, const void* x_dev,
+                 int nvec, const void* v_dev, double* out_host, void* stream);
+int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int xdtype, const void* x_dev,
+                int nvec, const double* c_host, void* y_dev, int accumulate, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

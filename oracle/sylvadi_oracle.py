@@ -667,6 +667,53 @@ def factored_relative_difference(Z1, g1, Y1, Z2, g2, Y2):
     return float(num / den)
 
 
+def true_residual_norm(A, B, f, g, Z, Y, gdiag, M=None, C=None, tol=1e-6,
+                       max_iterations=200):
+    """Spectral norm of R = A X C + M X B + f g^*, X = Z diag(gdiag) Y^*, by
+    power iteration on x -> R^*(R x) (adi.py:682-726: x0 = ones/sqrt(m),
+    lambda = ||R x||^2, stop on a relative change <= tol).  Real coefficient
+    matrices, so the adjoint products are transposes (adi.py:729-733)."""
+    f = np.asarray(f, dtype=complex)
+    g = np.asarray(g, dtype=complex)
+    gd = np.asarray(gdiag, dtype=complex)
+
+    def apply_R(x):
+        Cx = x if C is None else C @ x
+        Bx = B @ x
+        out = f @ (g.conj().T @ x)
+        if Z.shape[1]:
+            out = out + A @ (Z @ (gd[:, None] * (Y.conj().T @ Cx)))
+            zb = Z @ (gd[:, None] * (Y.conj().T @ Bx))
+            out = out + (zb if M is None else M @ zb)
+        return out
+
+    def apply_Rh(x):
+        out = g @ (f.conj().T @ x)
+        if Z.shape[1]:
+            ya = Y @ (np.conj(gd)[:, None] * (Z.conj().T @ (A.T @ x)))
+            out = out + (ya if C is None else C.T @ ya)
+            mx = x if M is None else M.T @ x
+            out = out + B.T @ (Y @ (np.conj(gd)[:, None] * (Z.conj().T @ mx)))
+        return out
+
+    m = g.shape[0]
+    x = np.ones((m, 1), dtype=complex) / np.sqrt(m)
+    lam = 0.0
+    for _ in range(max_iterations):
+        Rx = apply_R(x)
+        y = apply_Rh(Rx)
+        lam_new = float(np.linalg.norm(Rx) ** 2)
+        ny = np.linalg.norm(y)
+        if ny == 0.0:
+            return 0.0
+        x = y / ny
+        if lam > 0.0 and abs(lam_new - lam) <= tol * lam_new:
+            lam = lam_new
+            break
+        lam = lam_new
+    return float(np.sqrt(lam))
+
+
 def steps_csv(run):
     """adi.py:211-239 row format without wall_ms."""
     rows = ["step,scaled_res,delta_A,delta_B,achieved_rA,achieved_rB,"

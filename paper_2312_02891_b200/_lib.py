@@ -55,6 +55,10 @@ SIGNATURES = {
                             _vp, _vp, _vp]),
     "sad_adi_epilogue": (_c.c_int, [_vp, _i64, _i64, _c.c_int, _c.c_int, _c.c_double,
                                     _c.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "sad_ts_hgemv": (_c.c_int, [_vp, _i64, _i64, _i64, _c.c_int, _vp, _c.c_int, _vp, _vp,
+                                _vp]),
+    "sad_ts_gemv": (_c.c_int, [_vp, _i64, _i64, _i64, _c.c_int, _vp, _c.c_int, _vp, _vp,
+                               _c.c_int, _vp]),
 }
 
 

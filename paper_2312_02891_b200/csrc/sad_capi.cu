@@ -24,6 +24,7 @@
 #include "sad_kernels.cuh"
 #include "sad_coop.cuh"
 #include "sad_spmm_launch.cuh"
+#include "sad_verify.cuh"
 #include "sad_adi.cuh"
 #include "sad_spmm_bulk.cuh"
 
@@ -43,6 +44,12 @@ struct sad_ctx {
   double2* epi_part = nullptr;   // fused ADI epilogue partials (lazy)
   double2* epi_out = nullptr;
   double2* epi_host = nullptr;   // pinned
+  // tall-skinny products (verification diagnostics), grown on demand
+  double2* ts_part = nullptr;
+  size_t ts_part_elems = 0;
+  double2* ts_dev = nullptr;     // reduced outputs / coefficients
+  double2* ts_host = nullptr;    // pinned staging
+  size_t ts_elems = 0;
 };
 
 struct DevCsr {
@@ -194,6 +201,9 @@ extern "C" int sad_ctx_destroy(sad_ctx* c) {
   cudaFree(c->epi_part);
   cudaFree(c->epi_out);
   if (c->epi_host) cudaFreeHost(c->epi_host);
+  cudaFree(c->ts_part);
+  cudaFree(c->ts_dev);
+  if (c->ts_host) cudaFreeHost(c->ts_host);
   delete c;
   return SAD_OK;
 }
@@ -1408,4 +1418,110 @@ extern "C" int sad_gmres_finish(sad_gmres* ws, void* res, void* stream, int64_t*
     if (rc) return rc;
   }
   return read_results(ws, res, s, iters_host, resnorm_host, conv_host, ws->pending_tol);
+}
+
+// -----------------------------------------------------------------------------
+// tall-skinny products over the low-rank factors (true_residual_norm's power
+// iteration, adi.py:682-726)
+// -----------------------------------------------------------------------------
+static int ts_reserve(sad_ctx* ctx, size_t part_elems, size_t out_elems) {
+  if (part_elems > ctx->ts_part_elems) {
+    cudaFree(ctx->ts_part);
+    ctx->ts_part = nullptr;
+    ctx->ts_part_elems = 0;
+    CK(ctx, cudaMalloc(&ctx->ts_part, part_elems * sizeof(double2)));
+    ctx->ts_part_elems = part_elems;
+  }
+  if (out_elems > ctx->ts_elems) {
+    cudaFree(ctx->ts_dev);
+    if (ctx->ts_host) cudaFreeHost(ctx->ts_host);
+    ctx->ts_dev = nullptr;
+    ctx->ts_host = nullptr;
+    ctx->ts_elems = 0;
+    CK(ctx, cudaMalloc(&ctx->ts_dev, out_elems * sizeof(double2)));
+    CK(ctx, cudaMallocHost(&ctx->ts_host, out_elems * sizeof(double2)));
+    ctx->ts_elems = out_elems;
+  }
+  return SAD_OK;
+}
+
+template <typename XT, int S>
+static void ts_hgemv_launch(long long n, long long K, long long ldx, const void* X, const void* V,
+                            long long rpb, int CW, int grid, double2* part, cudaStream_t s) {
+  k_ts_hgemv<XT, S><<<grid, 256, 0, s>>>(n, K, ldx, (const XT*)X, (const double2*)V, rpb, CW, part);
+}
+
+extern "C" int sad_ts_hgemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int xdtype,
+                            const void* X, int nvec, const void* V, double* out_host,
+                            void* stream) {
+  if (!ctx || !X || !V || !out_host) return SAD_EINVAL;
+  if (n < 1 || K < 1 || ldx < K) return set_err(ctx, SAD_EINVAL, "bad factor shape n=%lld K=%lld ldx=%lld", (long long)n, (long long)K, (long long)ldx);
+  if (nvec != 1 && nvec != 2) return set_err(ctx, SAD_EINVAL, "nvec must be 1 or 2");
+  if (xdtype != SAD_F64 && xdtype != SAD_C128) return set_err(ctx, SAD_EINVAL, "bad dtype %d", xdtype);
+  cudaStream_t s = S_(stream);
+  const int CW = (int)std::min<long long>(256, ((K + 31) / 32) * 32);
+  const long long min_rows = 64;
+  int grid = (int)std::min<long long>((n + min_rows - 1) / min_rows, (long long)ctx->nsm * 4);
+  grid = std::max(grid, 1);
+  const long long rpb = (n + grid - 1) / grid;
+  const size_t nout = (size_t)K * nvec;
+  int rc = ts_reserve(ctx, (size_t)grid * nout, nout);
+  if (rc) return rc;
+  if (xdtype == SAD_F64) {
+    if (nvec == 1) ts_hgemv_launch<double, 1>(n, K, ldx, X, V, rpb, CW, grid, ctx->ts_part, s);
+    else ts_hgemv_launch<double, 2>(n, K, ldx, X, V, rpb, CW, grid, ctx->ts_part, s);
+  } else {
+    if (nvec == 1) ts_hgemv_launch<double2, 1>(n, K, ldx, X, V, rpb, CW, grid, ctx->ts_part, s);
+    else ts_hgemv_launch<double2, 2>(n, K, ldx, X, V, rpb, CW, grid, ctx->ts_part, s);
+  }
+  CKL(ctx);
+  k_ts_reduce<<<(unsigned)((nout * 32 + 255) / 256), 256, 0, s>>>(ctx->ts_part, grid, (long long)nout, ctx->ts_dev);
+  COUNT_LAUNCH(2);
+  CKL(ctx);
+  CK(ctx, cudaMemcpyAsync(ctx->ts_host, ctx->ts_dev, nout * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  CK(ctx, cudaStreamSynchronize(s));
+  std::memcpy(out_host, ctx->ts_host, nout * sizeof(double2));
+  return SAD_OK;
+}
+
+template <typename XT, int S>
+static cudaError_t ts_gemv_launch(long long n, long long K, long long ldx, const void* X,
+                                  const double2* C, void* Y, int acc, int grid, cudaStream_t s) {
+  const size_t smem = (size_t)K * S * sizeof(double2);
+  auto kern = k_ts_gemv<XT, S>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<grid, 256, smem, s>>>(n, K, ldx, (const XT*)X, C, (double2*)Y, acc);
+  return cudaGetLastError();
+}
+
+extern "C" int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int xdtype,
+                           const void* X, int nvec, const double* C_host, void* Y,
+                           int accumulate, void* stream) {
+  if (!ctx || !X || !C_host || !Y) return SAD_EINVAL;
+  if (n < 1 || K < 1 || ldx < K) return set_err(ctx, SAD_EINVAL, "bad factor shape n=%lld K=%lld ldx=%lld", (long long)n, (long long)K, (long long)ldx);
+  if (nvec != 1 && nvec != 2) return set_err(ctx, SAD_EINVAL, "nvec must be 1 or 2");
+  if (xdtype != SAD_F64 && xdtype != SAD_C128) return set_err(ctx, SAD_EINVAL, "bad dtype %d", xdtype);
+  const size_t ncoef = (size_t)K * nvec;
+  if (ncoef * sizeof(double2) > 200 * 1024)
+    return set_err(ctx, SAD_EINVAL, "K=%lld too large for the staged coefficients", (long long)K);
+  cudaStream_t s = S_(stream);
+  int rc = ts_reserve(ctx, 0, ncoef);
+  if (rc) return rc;
+  CK(ctx, cudaStreamSynchronize(s));   // the pinned staging buffer may still be in flight
+  std::memcpy(ctx->ts_host, C_host, ncoef * sizeof(double2));
+  CK(ctx, cudaMemcpyAsync(ctx->ts_dev, ctx->ts_host, ncoef * sizeof(double2), cudaMemcpyHostToDevice, s));
+  const int grid = (int)std::max<long long>(1, std::min<long long>((n + 7) / 8, (long long)ctx->nsm * 8));
+  cudaError_t e;
+  if (xdtype == SAD_F64)
+    e = nvec == 1 ? ts_gemv_launch<double, 1>(n, K, ldx, X, ctx->ts_dev, Y, accumulate, grid, s)
+                  : ts_gemv_launch<double, 2>(n, K, ldx, X, ctx->ts_dev, Y, accumulate, grid, s);
+  else
+    e = nvec == 1 ? ts_gemv_launch<double2, 1>(n, K, ldx, X, ctx->ts_dev, Y, accumulate, grid, s)
+                  : ts_gemv_launch<double2, 2>(n, K, ldx, X, ctx->ts_dev, Y, accumulate, grid, s);
+  COUNT_LAUNCH(1);
+  if (e != cudaSuccess) return set_err(ctx, SAD_ECUDA, "ts_gemv launch failed: %s", cudaGetErrorString(e));
+  return SAD_OK;
 }

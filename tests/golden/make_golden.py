@@ -264,12 +264,41 @@ def small_configs():
     write_csv(os.path.join(GOLD, "ref_c3s_dynamic_mid_bl_bicgstab.csv"), rep)
 
 
+def verify_goldens():
+    """The reference's true_residual_norm / residual_gap (adi.py:655-726) on
+    short runs of its own driver: a standard pair (config 1, 6 steps) and a
+    generalised pair (config 3 at 48^2 / 40^2, 4 steps).  Factors, gammas and
+    the reference values go to tests/golden/ref_verify_<case>.npz."""
+    cases = (("c1", 6), ("c3s", 4))
+    for name, kmax in cases:
+        A, B, M, C, f, g = cfgs.build_problem(name)
+        seq = sv.ShiftSequence.from_json(os.path.join(REPO, "configs", f"shifts_{name}.json"))
+        to = lambda X: None if X is None else sv.SparseMatrix(X)
+        problem = sv.SylvesterProblem(A=to(A), B=to(B), f=f, g=g, M=to(M), C=to(C))
+        cfg = sv.AdiConfig(strategy="dynamic_mid_bl", kmax=kmax, precond_kind_A="jacobi",
+                           precond_kind_B="jacobi", keep_inner_residuals=True)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            sol, rep, state = sv.run_with_state(problem, cfg, seq)
+        trn = sv.true_residual_norm(problem, sol)
+        gap = sv.residual_gap(problem, state)
+        path = os.path.join(GOLD, f"ref_verify_{name}.npz")
+        np.savez_compressed(path, Z=sol.Z, Y=sol.Y, gdiag=sol.gamma_diag(),
+                            true_residual_norm=trn, residual_gap=gap,
+                            steps=rep.outer_iterations)
+        print(f"{path}: {rep.outer_iterations} steps, true residual {trn:.6e}, gap {gap:.6e}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-c2", action="store_true")
     ap.add_argument("--small", action="store_true", help="only the reduced configs 3/5")
     ap.add_argument("--c3-shifts", action="store_true", help="full-size config-3 shifts")
+    ap.add_argument("--verify", action="store_true", help="true_residual_norm goldens")
     args = ap.parse_args()
+    if args.verify:
+        verify_goldens()
+        return
     if args.small:
         small_configs()
         return

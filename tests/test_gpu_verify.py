@@ -1,0 +1,86 @@
+"""GPU verification diagnostics against the oracle and the
+reference's own true_residual_norm values."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD
+from oracle import sylvadi_oracle as orc
+from paper_2312_02891_b200 import configs as cfgs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("K", [1, 37, 300])
+@pytest.mark.parametrize("nvec", [1, 2])
+def test_tall_skinny_products(rng, cplx, K, nvec):
+    from paper_2312_02891_b200 import _lib
+    from paper_2312_02891_b200.verify import _Factor
+    n = 5003
+    X = rng.standard_normal((n, K))
+    if cplx:
+        X = X + 1j * rng.standard_normal((n, K))
+    V = rng.standard_normal((n, nvec)) + 1j * rng.standard_normal((n, nvec))
+    F = _Factor(X, n, 0)
+    ctx = _lib.context(0)
+    s = torch.cuda.current_stream().cuda_stream
+    Vd = torch.from_numpy(V).cuda()
+    got = F.hgemv(ctx, Vd, s)
+    want = X.conj().T @ V
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want)) * np.sqrt(n)
+    Cc = rng.standard_normal((K, nvec)) + 1j * rng.standard_normal((K, nvec))
+    Y = torch.zeros((n, nvec), dtype=torch.complex128, device="cuda")
+    F.gemv(ctx, Cc, Y, s)
+    F.gemv(ctx, Cc, Y, s, accumulate=True)
+    want = 2.0 * (X @ Cc)
+    got = Y.cpu().numpy()
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want)) * np.sqrt(K)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_true_residual_norm_matches_reference(name):
+    """Device power iteration = the reference's value on its own factors."""
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200.verify import true_residual_norm
+    gold = np.load(os.path.join(GOLD, f"ref_verify_{name}.npz"))
+    A, B, M, C, f, g = cfgs.build_problem(name)
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
+    r = f.shape[1]
+    gd = gold["gdiag"]
+    sol = pb.LowRankSolution(Z=gold["Z"], gammas=gd[::r], Y=gold["Y"], r=r)
+    got = true_residual_norm(prob, sol)
+    want = float(gold["true_residual_norm"])
+    assert abs(got - want) <= 1e-8 * want, (got, want)
+
+
+def test_true_residual_of_converged_device_run():
+    """A converged device ADI run (config 1): the device true residual equals
+    the oracle's on the downloaded factors, and the equation is solved to the
+    outer tolerance (true residual <= 2 tau ||f g^*||)."""
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200.verify import true_residual_norm
+    spec = cfgs.CONFIGS["c1"]
+    A, B, M, C, f, g = cfgs.build_problem("c1")
+    pairs, cyclic = spec.load_shift_pairs()
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
+    cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax, precond_kind_A="jacobi",
+                       precond_kind_B="jacobi")
+    sol, rep = pb.run(prob, cfg, pb.ShiftSequence(pairs=pairs, cyclic=cyclic),
+                      restart=spec.restart, flexible=spec.flexible)
+    assert rep.converged
+    dev = true_residual_norm(prob, sol)
+    host = orc.true_residual_norm(A, B, f, g, sol.Z, sol.Y, sol.gamma_diag())
+    assert abs(dev - host) <= 1e-6 * host, (dev, host)
+    fg = np.linalg.norm(f) * np.linalg.norm(g)   # = ||f g^*||_2 for r = 1
+    assert dev <= 2.0 * cfg.outer_tolerance * fg, dev / fg

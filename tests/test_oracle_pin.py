@@ -179,3 +179,14 @@ def test_oracle_bicgstab_adi_matches_reference_generalised():
     for rec, gd in zip(run.records, gold):
         assert rec.inner_it_A == gd["inner_it_A"] and rec.inner_it_B == gd["inner_it_B"]
         assert abs(rec.scaled_res - gd["scaled_res"]) <= 1e-8 * gd["scaled_res"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_true_residual_norm_matches_reference(name):
+    """oracle.true_residual_norm reproduces the reference's own value
+    (adi.py:682-726) on factors its driver produced (ref_verify_<name>.npz)."""
+    gold = np.load(os.path.join(GOLD, f"ref_verify_{name}.npz"))
+    A, B, M, C, f, g = cfgs.build_problem(name)
+    got = orc.true_residual_norm(A, B, f, g, gold["Z"], gold["Y"], gold["gdiag"], M=M, C=C)
+    want = float(gold["true_residual_norm"])
+    assert abs(got - want) <= 1e-9 * want, (got, want)
