@@ -423,7 +423,7 @@ def run(problem, config, shift_sequence, bindings=None, **kw):
 
 
 def run_with_state(problem, config, shift_sequence, bindings=None, *, restart=50,
-                   flexible=False, device=0, concurrent=True, keep_on_device=False,
+                   flexible=False, device=0, concurrent="auto", keep_on_device=False,
                    engine="persistent"):
     """adi.py:553-607.  ``bindings=None`` runs the device-resident driver with
     GpuGmresBinding(restart, flexible) on both sides; otherwise the host loop
@@ -517,12 +517,17 @@ def _record(k, scaled, dec, rA, rB, ra, rb, u, v, wall_ms):
     return rec
 
 
+#: largest A-side block (n x r complex128 bytes) for which the A and B solves
+#: run concurrently by default (DeviceAdi(concurrent="auto"))
+CONCURRENT_MAX_BLOCK_BYTES = 16 << 20
+
+
 class DeviceAdi:
     """Device-resident ADI engine: uploads once, then ``run()`` may be repeated
     (the bench times repeated runs with the inputs already in HBM)."""
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
-                 device=0, concurrent=True, engine="persistent"):
+                 device=0, concurrent="auto", engine="persistent", phase_a="auto"):
         import torch
         if not isinstance(problem, SylvesterProblem):
             problem = SylvesterProblem.from_reference(problem)
@@ -535,7 +540,12 @@ class DeviceAdi:
         self.problem, self.config, self.shifts = problem, config, shift_sequence
         self.device = device
         self.engine = engine
-        self.concurrent = concurrent
+        if concurrent == "auto":
+            # Small blocks are latency-bound: the two solves overlap on disjoint
+            # SM sets.  Large blocks are HBM-bound: one solve at a time on every
+            # SM (no idle SMs while the shorter side waits for the longer one).
+            concurrent = problem.n * problem.r * 16 <= CONCURRENT_MAX_BLOCK_BYTES
+        self.concurrent = bool(concurrent)
         self.dev = torch.device("cuda", device)
         pairs = [shift_sequence.at(k) for k in range(1, min(config.kmax, _seq_len(shift_sequence)) + 1)]
         complex_run = (any(complex(a).imag != 0.0 or complex(b).imag != 0.0 for a, b in pairs)
@@ -552,11 +562,11 @@ class DeviceAdi:
         self.bA = GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
-                                  max_sms=sm_a)
+                                  max_sms=sm_a, phase_a=phase_a)
         self.bB = GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
-                                  max_sms=sm_b)
+                                  max_sms=sm_b, phase_a=phase_a)
         self.Md = self.bA.mass      # M (for M z)
         self.Cd = self.bB.mass      # C with transpose (for C^T y)
         self.f = torch.from_numpy(np.ascontiguousarray(problem.f)).to(self.dev, self.tdtype)
