@@ -154,11 +154,19 @@ class Clocks:
 
 # -- workloads ------------------------------------------------------------------------
 
-def build_c2():
+WORKLOADS = {
+    "c2": "config 2: ADI to 1e-8, 3-D conv-diff 40^3/30^3, r=2, complex128, "
+          "Jacobi-FGMRES(30), dynamic_mid_bl",
+    "c3": "config 3: ADI to 1e-8, generalised 2-D Q1-FEM pencils 1000^2/700^2 (A+sM, B+sC), "
+          "r=3, complex128, Jacobi-GMRES(40), dynamic_mid_bl",
+}
+
+
+def build_c2(name="c2"):
     import paper_2312_02891_b200 as pb
     from paper_2312_02891_b200 import configs as cfgs
-    spec = cfgs.CONFIGS["c2"]
-    A, B, M, C, f, g = cfgs.build_problem("c2")
+    spec = cfgs.CONFIGS[name]
+    A, B, M, C, f, g = cfgs.build_problem(name)
     pairs, cyclic = spec.load_shift_pairs()
     prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
     cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax,
@@ -169,12 +177,12 @@ def build_c2():
 
 
 def c2_config_json(spec, prob, extra=None):
-    out = {"workload": "config 2: ADI to 1e-8, 3-D conv-diff 40^3/30^3, r=2, complex128, "
-                       "Jacobi-FGMRES(30), dynamic_mid_bl",
+    out = {"workload": WORKLOADS[spec.name],
            "n": prob.n, "m": prob.m, "r": prob.r, "nnz_A": int(prob.A.nnz),
            "nnz_B": int(prob.B.nnz), "kmax": spec.kmax, "restart": spec.restart,
            "flexible": spec.flexible, "strategy": spec.strategy,
-           "shifts": "configs/shifts_c2.json (reference heuristic_shifts, npairs=12)",
+           "shifts": f"configs/shifts_{spec.name}.json (reference heuristic_shifts, "
+                     f"npairs={spec.npairs})",
            "seed": spec.seed, "l2": "flushed between timed steps (256 MiB write)",
            "parallelism": "replicas"}
     if extra:
@@ -200,6 +208,28 @@ def cpu_reference_solve(kmax=None):
         warnings.simplefilter("ignore")
         run = orc.run_adi(A, B, f, g, cfg, pairs, bA, bB, cyclic=cyclic)
     return time.perf_counter() - t0, run.outer_iterations, bool(run.converged)
+
+
+def cpu_reference_sample_c3(max_inner=10):
+    """Bounded CPU sample for config 3 (a full reference solve would take hours
+    on one core): the first outer step of the reference's Jacobi-BiCGstab ADI
+    (oracle/ restatement) with the inner iterations capped per column."""
+    from oracle import sylvadi_oracle as orc
+    from paper_2312_02891_b200 import configs as cfgs
+    spec = cfgs.CONFIGS["c3"]
+    A, B, M, C, f, g = cfgs.build_problem("c3")
+    pairs, cyclic = spec.load_shift_pairs()
+    cfg = orc.Config(strategy=spec.strategy, kmax=1, outer_tolerance=spec.outer_tolerance)
+    bA = orc.Binding("A", A, M, solver="bicgstab", max_iterations=max_inner)
+    bB = orc.Binding("B", B, C, solver="bicgstab", max_iterations=max_inner)
+    from threadpoolctl import threadpool_limits
+    t0 = time.perf_counter()
+    with warnings.catch_warnings(), threadpool_limits(1):
+        warnings.simplefilter("ignore")
+        run = orc.run_adi(A, B, f, g, cfg, pairs, bA, bB, M=M, C=C, cyclic=cyclic)
+    secs = time.perf_counter() - t0
+    its = run.records[0].inner_it_A + run.records[0].inner_it_B if run.records else 0
+    return secs, its
 
 
 def run_reference_arm(args, dist):
@@ -248,14 +278,14 @@ def profile_pass(eng):
     return tot, rep
 
 
-def run_ours_c2(args, dist):
+def run_ours_c2(args, dist, name="c2"):
     import torch
     import paper_2312_02891_b200 as pb
     from paper_2312_02891_b200 import _lib
     dev = dist.local
     torch.cuda.set_device(dev)
     lib = _lib.load()
-    spec, prob, cfg, seq, raw = build_c2()
+    spec, prob, cfg, seq, raw = build_c2(name)
     eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible, device=dev)
     eng.warm()
     for _ in range(args.warmup):
@@ -291,7 +321,7 @@ def run_ours_c2(args, dist):
     peak, peak_kind = hbm_peak()
     kern_ms, kern_launches, kern_bytes = prof[0], prof[1], prof[2]
     ach = kern_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
-    traffic, tr_ent = ncu_traffic("c2_persistent")
+    traffic, tr_ent = ncu_traffic(f"{name}_persistent")
     # e2e through the public API with host inputs
     e2e_times = []
     A, B, M, C, f, g, pairs, cyclic = raw
@@ -299,7 +329,7 @@ def run_ours_c2(args, dist):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hprob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
+        hprob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
         sol, erep = pb.run(hprob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                            device=dev)
         Zh, Yh = sol.Z, sol.Y
@@ -307,9 +337,9 @@ def run_ours_c2(args, dist):
         if i >= args.warmup:
             e2e_times.append(dt)
     e2e = dist.max(statistics.mean(e2e_times))
-    h2d = (A.indptr.nbytes + A.indices.nbytes + A.data.nbytes
-           + 2 * (B.indptr.nbytes + B.indices.nbytes + B.data.nbytes)
-           + f.nbytes + g.nbytes)
+    def csr_bytes(X):
+        return 0 if X is None else X.indptr.nbytes + X.indices.nbytes + X.data.nbytes
+    h2d = csr_bytes(A) + csr_bytes(M) + 2 * (csr_bytes(B) + csr_bytes(C)) + f.nbytes + g.nbytes
     d2h = Zh.nbytes + Yh.nbytes
 
     line = {
@@ -321,10 +351,12 @@ def run_ours_c2(args, dist):
             "outer_steps": rep.outer_iterations, "converged": rep.converged,
             "final_scaled_residual": rep.final_scaled_residual,
             "sum_inner_A": rep.sum_inner_A, "sum_inner_B": rep.sum_inner_B,
-            "inner": "Jacobi-FGMRES(30) batched per column, CGS2, device Givens"}),
+            "inner": f"Jacobi-{'F' if spec.flexible else ''}GMRES({spec.restart}) batched per "
+                     f"column, delayed-Gram CGS2, device Givens",
+            "ab_solves": "concurrent" if eng.concurrent else "sequential"}),
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "traffic": traffic, "kernel": "k_gmres_persistent",
-                     "traffic_source": tr_ent and (f"profiles/traffic.json[c2_persistent]: "
+                     "traffic_source": tr_ent and (f"profiles/traffic.json[{name}_persistent]: "
                                                    f"{tr_ent['launches']} launches, "
                                                    f"{tr_ent['note']}"),
                      "peak_kind": peak_kind,
@@ -344,7 +376,20 @@ def run_ours_c2(args, dist):
         "gpu_launches": int(launches),
         "clocks": ck,
     }
-    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+    if name == "c3":
+        from paper_2312_02891_b200.verify import true_residual_norm
+        sol, _, _ = eng.run()
+        trn = true_residual_norm(prob, sol)
+        line["config"]["true_scaled_residual"] = trn / rep.rhs_norm
+        line["config"]["true_residual"] = "GPU power iteration (verify.true_residual_norm)"
+    if name == "c3" and dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        secs, its = cpu_reference_sample_c3()
+        line["cpu_baseline"] = {"value": secs, "unit": "s", "cores": 1, "kind": "port",
+                                "sample": f"NOT a full solve: first outer step of the "
+                                          f"reference's Jacobi-BiCGstab ADI (oracle/ "
+                                          f"restatement) with inner iterations capped at 10 "
+                                          f"per column ({its} inner iterations in total)"}
+    elif dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         secs, steps_cpu, conv = cpu_reference_solve()
         line["cpu_baseline"] = {"value": secs, "unit": "s", "cores": 1, "kind": "port",
                                 "sample": f"one full config-2 solve of the reference's "
@@ -438,7 +483,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
     ap.add_argument("--c4-n0", type=int, default=4096)
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -448,7 +493,8 @@ def main():
         line = run_reference_arm(args, dist)
     else:
         dist = Dist(args.gpus)
-        line = run_ours_c2(args, dist) if args.config == "c2" else run_ours_c4(args, dist)
+        line = (run_ours_c4(args, dist) if args.config == "c4"
+                else run_ours_c2(args, dist, args.config))
     if line is not None:
         print(json.dumps(line), flush=True)
     dist.close()
