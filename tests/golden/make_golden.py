@@ -289,13 +289,40 @@ def verify_goldens():
         print(f"{path}: {rep.outer_iterations} steps, true residual {trn:.6e}, gap {gap:.6e}")
 
 
+def ritz_goldens():
+    """The reference's pencil_ritz_sets (shifts.py:101-129, splu-based) for the
+    configs whose shifts are pinned; values go to tests/golden/ref_ritz.npz so
+    the device Ritz generator and the host greedy picker can be checked
+    against them (and against configs/shifts_<name>.json)."""
+    out = {}
+    to = lambda X: None if X is None else sv.SparseMatrix(X)
+    for name in ("c1", "c2", "c3s", "c5s"):
+        A, B, M, C, f, g = cfgs.build_problem(name)
+        for side, (base, mass) in (("A", (A, M)), ("B", (B, C))):
+            d, inv = sv.pencil_ritz_sets(to(base), to(mass))
+            out[f"{name}_{side}_direct"] = d.values
+            out[f"{name}_{side}_inverse"] = inv.values
+        seq = sv.ShiftSequence.from_json(os.path.join(REPO, "configs", f"shifts_{name}.json"))
+        al = [a for a, _ in seq.pairs]
+        be = [b for _, b in seq.pairs]
+        ra = np.concatenate([out[f"{name}_A_direct"], out[f"{name}_A_inverse"]])
+        rb = np.concatenate([out[f"{name}_B_direct"], out[f"{name}_B_inverse"]])
+        out[f"{name}_objective"] = sv.shift_objective(al, be, ra, rb)
+        print(name, "ritz sets done")
+    np.savez_compressed(os.path.join(GOLD, "ref_ritz.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-c2", action="store_true")
     ap.add_argument("--small", action="store_true", help="only the reduced configs 3/5")
     ap.add_argument("--c3-shifts", action="store_true", help="full-size config-3 shifts")
     ap.add_argument("--verify", action="store_true", help="true_residual_norm goldens")
+    ap.add_argument("--ritz", action="store_true", help="reference Ritz-set goldens")
     args = ap.parse_args()
+    if args.ritz:
+        ritz_goldens()
+        return
     if args.verify:
         verify_goldens()
         return
