@@ -569,13 +569,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                                     ? make_double2(0.0, 0.0)
                                     : make_double2(si * sjj * graw.x, si * sjj * graw.y);
             s_gc[o] = gij;
-            double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1);
-            Gc[(size_t)ii * (m + 1) + j] = gij;          // G[i][j]
-            Gc[(size_t)j * (m + 1) + ii] = cconj(gij);   // G[j][i]
             const double2 hr = s_red[o];
             s_h1[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * hr.x, si * hr.y);
           }
-          if (threadIdx.x < R) gs.wpre2[threadIdx.x] = s_red[2 * J * R + threadIdx.x].x;
           __syncthreads();
           // c = 2 h1 - G h1 (old G entries, column/row j from smem); coef = S c.
           // The old G block is staged in smem with one parallel load when it
@@ -608,7 +604,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             const double si = s_S[o];
             st.coef[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * cv.x, si * cv.y);
           }
-          __syncthreads();
+          if (prof && threadIdx.x == 0) atomicAdd(st.stats + 10, (double)(gtimer() - tfin));
+          // Every block needs only coef for phase C: release now and do this
+          // step's bookkeeping off the critical path.  Its global writes (Gram
+          // column, ||w_pre||^2, rotated Hessenberg column) are read by later
+          // finishers only, which run after this block's next arrive (release).
+          bar_release(st);
+          for (int o = threadIdx.x; o < J * R; o += kThreads) {
+            const int ii = o / R, cc = o - ii * R;
+            double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1);
+            Gc[(size_t)ii * (m + 1) + j] = s_gc[o];          // G[i][j]
+            Gc[(size_t)j * (m + 1) + ii] = cconj(s_gc[o]);   // G[j][i]
+          }
+          if (threadIdx.x < R) gs.wpre2[threadIdx.x] = s_red[2 * J * R + threadIdx.x].x;
           // Apply the previous Givens rotations to the new Hessenberg column now
           // (they do not depend on h_{j+1,j}), so the phase-C finisher only has to
           // form the new rotation.
@@ -630,9 +638,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               const int ii = o / R, cc = o - ii * R;
               if (s_act[cc]) gs.H[((size_t)cc * m + j) * (m + 1) + ii] = s_red[o];
             }
+            __syncthreads();   // finisher smem is reused by phase C
           }
-          if (prof && threadIdx.x == 0) atomicAdd(st.stats + 10, (double)(gtimer() - tfin));
-          bar_release(st);
         } else {
           bar_wait(st, gen);
         }

@@ -60,10 +60,14 @@ INF = float("inf")
 
 @dataclass
 class RitzSet:
-    """shifts.py:18-28."""
+    """shifts.py:18-28, plus ``bounds``: the Arnoldi residual norm
+    |h_{k+1,k} e_k^T y| of each Ritz pair (None when unknown).  Only pairs with
+    small bounds are determined by the operator; the others depend on rounding
+    (and, for the inverse sets, on the solver), in the reference as here."""
     values: np.ndarray
     source: str
     kind: str
+    bounds: np.ndarray = None
 
     def __post_init__(self):
         self.values = np.asarray(self.values, dtype=np.complex128).ravel()
@@ -110,7 +114,9 @@ def arnoldi_ritz(apply, start, steps, source="A-side", kind="direct", device=0):
         V.append(nv)
     else:
         j += 1
-    return RitzSet(values=np.linalg.eigvals(H[:j, :j]), source=source, kind=kind)
+    theta, Yv = np.linalg.eig(H[:j, :j])
+    bounds = np.abs(H[j, j - 1] * Yv[j - 1, :]) / np.linalg.norm(Yv, axis=0)
+    return RitzSet(values=theta, source=source, kind=kind, bounds=bounds)
 
 
 class _DeviceSolve:
@@ -163,12 +169,15 @@ def pencil_ritz_sets(base, mass=None, n_direct=10, n_inverse=20, source="A-side"
 
     direct = arnoldi_ritz(direct_action, start, n_direct, source, "direct", device)
     inv = arnoldi_ritz(inverse_action, start, n_inverse, source, "inverse", device)
-    inv_values = 1.0 / inv.values[np.abs(inv.values) > 0]
+    keep = np.abs(inv.values) > 0
+    inv_values = 1.0 / inv.values[keep]
+    # relative bound of the reciprocal: |d(1/theta)| / |1/theta| = |d theta| / |theta|
+    inv_bounds = inv.bounds[keep] / np.abs(inv.values[keep]) * np.abs(inv_values)
     if stats is not None:
         stats[source] = {"base_solve_iterations": base_inv.iterations,
                          "base_solve_unconverged": base_inv.unconverged,
                          "mass_solve_iterations": mass_inv.iterations if mass_inv else 0}
-    return direct, RitzSet(values=inv_values, source=source, kind="inverse")
+    return direct, RitzSet(values=inv_values, source=source, kind="inverse", bounds=inv_bounds)
 
 
 def _merge(ritz):

@@ -30,8 +30,8 @@ def main():
                        precond_kind_B="jacobi")
     seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
     warnings.simplefilter("ignore")
-    for engine, conc, mepth, direct in itertools.product(["persistent"], [True, False], [1, 2],
-                                                         [0, 1]):
+    for engine, conc, mepth, direct in itertools.product(["persistent"], [True, False],
+                                                         [1, 2, 4, 8], [1]):
         eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                            concurrent=conc, engine=engine)
         eng.warm()
