@@ -159,7 +159,11 @@ WORKLOADS = {
           "Jacobi-FGMRES(30), dynamic_mid_bl",
     "c3": "config 3: ADI to 1e-8, generalised 2-D Q1-FEM pencils 1000^2/700^2 (A+sM, B+sC), "
           "r=3, complex128, Jacobi-GMRES(40), dynamic_mid_bl",
+    "c5": "config 5: ADI to 1e-8, 3-D conv-diff 200^3/160^3 (n=8M, m=4.1M), r=4, complex128, "
+          "Jacobi-GMRES(30), dynamic_mid_bl, shifts generated on the GPU (device Ritz values)",
 }
+#: inner-iteration cap per column of the bounded CPU sample (first outer step)
+CPU_SAMPLE_CAP = {"c3": 10, "c5": 1}
 
 
 def build_c2(name="c2"):
@@ -210,14 +214,14 @@ def cpu_reference_solve(kmax=None):
     return time.perf_counter() - t0, run.outer_iterations, bool(run.converged)
 
 
-def cpu_reference_sample_c3(max_inner=10):
-    """Bounded CPU sample for config 3 (a full reference solve would take hours
-    on one core): the first outer step of the reference's Jacobi-BiCGstab ADI
-    (oracle/ restatement) with the inner iterations capped per column."""
+def cpu_reference_sample(name, max_inner):
+    """Bounded CPU sample for configs 3/5 (a full reference solve would take
+    hours on one core): the first outer step of the reference's Jacobi-BiCGstab
+    ADI (oracle/ restatement) with the inner iterations capped per column."""
     from oracle import sylvadi_oracle as orc
     from paper_2312_02891_b200 import configs as cfgs
-    spec = cfgs.CONFIGS["c3"]
-    A, B, M, C, f, g = cfgs.build_problem("c3")
+    spec = cfgs.CONFIGS[name]
+    A, B, M, C, f, g = cfgs.build_problem(name)
     pairs, cyclic = spec.load_shift_pairs()
     cfg = orc.Config(strategy=spec.strategy, kmax=1, outer_tolerance=spec.outer_tolerance)
     bA = orc.Binding("A", A, M, solver="bicgstab", max_iterations=max_inner)
@@ -376,18 +380,19 @@ def run_ours_c2(args, dist, name="c2"):
         "gpu_launches": int(launches),
         "clocks": ck,
     }
-    if name == "c3":
+    if name in ("c3", "c5"):
         from paper_2312_02891_b200.verify import true_residual_norm
         sol, _, _ = eng.run()
         trn = true_residual_norm(prob, sol)
         line["config"]["true_scaled_residual"] = trn / rep.rhs_norm
         line["config"]["true_residual"] = "GPU power iteration (verify.true_residual_norm)"
-    if name == "c3" and dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        secs, its = cpu_reference_sample_c3()
+    if name in CPU_SAMPLE_CAP and dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cap = CPU_SAMPLE_CAP[name]
+        secs, its = cpu_reference_sample(name, cap)
         line["cpu_baseline"] = {"value": secs, "unit": "s", "cores": 1, "kind": "port",
                                 "sample": f"NOT a full solve: first outer step of the "
                                           f"reference's Jacobi-BiCGstab ADI (oracle/ "
-                                          f"restatement) with inner iterations capped at 10 "
+                                          f"restatement) with inner iterations capped at {cap} "
                                           f"per column ({its} inner iterations in total)"}
     elif dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         secs, steps_cpu, conv = cpu_reference_solve()
@@ -483,7 +488,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--c4-n0", type=int, default=4096)
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
