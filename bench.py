@@ -276,7 +276,7 @@ def profile_pass(eng):
     for ws in wss:
         ws.profile(True)
     sol, rep, _ = eng.run()
-    tot = np.zeros(12)
+    tot = np.zeros(13)
     for ws in wss:
         tot += ws.profile(False)
     return tot, rep

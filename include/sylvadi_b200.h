@@ -45,7 +45,8 @@ enum sad_dtype { SAD_F64 = 0, SAD_C128 = 1 };
 enum sad_engine { SAD_ENGINE_MULTI = 0, SAD_ENGINE_PERSISTENT = 1 };
 /* sad_gmres_set_option keys */
 enum sad_option { SAD_OPT_ENGINE = 0, SAD_OPT_MAX_SMS = 1, SAD_OPT_MIN_ELEMS_PER_THREAD = 2,
-                  SAD_OPT_DIRECT_A = 3 /* persistent phase A: -1 auto, 0 TMA ring, 1 direct */ };
+                  SAD_OPT_DIRECT_A = 3 /* persistent phase A: -1 auto, 0 TMA ring, 1 direct */,
+                  SAD_OPT_RESIDENT_CSR = 4 /* 1 (default): small CSR slabs stay in shared memory */ };
 enum sad_precond { SAD_PRECOND_NONE = 0, SAD_PRECOND_JACOBI = 1 };
 
 typedef struct sad_ctx sad_ctx;
@@ -161,7 +162,7 @@ int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
 
 /*
  * Profiling of sad_gmres_solve: enable=1 resets the counters; enable=0 stops.
- * stats_host[12] (may be NULL) receives the counters accumulated so far.
+ * stats_host[13] (may be NULL) receives the counters accumulated so far.
  * Multi-kernel engine (synchronous stepping with CUDA events):
  *   {spmm_ms, spmm_launches, spmm_algorithmic_bytes, orth_ms, arnoldi_steps,
  *    orth_bytes, cycle_end_ms, cycles}
@@ -170,7 +171,7 @@ int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
  *   {kernel_ms, launches, algorithmic_bytes, phaseA_ms (SpMM + basis dots),
  *    arnoldi_steps, phaseC_ms (basis update), cycle_end_ms, cycles,
  *    workA_ms, workC_ms (block 0 before the barrier), finA_ms, finC_ms (the
- *    reducing block's serial section)}
+ *    reducing block's serial section), spmmA_ms (block 0 inside the phase-A SpMM)}
  */
 int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host);
 

@@ -16,6 +16,7 @@ SAD_F64, SAD_C128 = 0, 1
 SAD_PRECOND_NONE, SAD_PRECOND_JACOBI = 0, 1
 SAD_ENGINE_MULTI, SAD_ENGINE_PERSISTENT = 0, 1
 SAD_OPT_ENGINE, SAD_OPT_MAX_SMS, SAD_OPT_MIN_ELEMS_PER_THREAD, SAD_OPT_DIRECT_A = 0, 1, 2, 3
+SAD_OPT_RESIDENT_CSR = 4
 
 #: every symbol declared in include/sylvadi_b200.h with (restype, argtypes)
 _c = ctypes

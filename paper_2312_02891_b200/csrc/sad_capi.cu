@@ -120,6 +120,7 @@ struct sad_gmres {
   int max_sms = 0;              // 0 = all SMs
   int min_elems_per_thread = 2;
   int direct_a = -1;            // phase-A path: -1 auto, 0 TMA ring, 1 direct loads
+  int resident_csr = 1;         // keep small CSR slabs in shared memory
   PState pst{};
   double* stats_dev = nullptr;
   // profiling (sad_gmres_profile): synchronous stepping with CUDA events
@@ -128,7 +129,7 @@ struct sad_gmres {
   double pending_tol = 0.0;
   int timers = 0;   // phase timers without event profiling (sad_gmres_fixed)
   double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  double prof2[4] = {0, 0, 0, 0};   // work_A, work_C (block 0), fin_A, fin_C (last block), ms
+  double prof2[5] = {0, 0, 0, 0, 0};   // work_A, work_C (block 0), fin_A, fin_C (last block), spmm_A (block 0), ms
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
@@ -910,11 +911,11 @@ extern "C" int sad_gmres_profile(sad_gmres* ws, int enable, double* stats_host) 
   sad_ctx* ctx = ws->ctx;
   if (stats_host) {
     for (int i = 0; i < 8; ++i) stats_host[i] = ws->prof[i];
-    for (int i = 0; i < 4; ++i) stats_host[8 + i] = ws->prof2[i];
+    for (int i = 0; i < 5; ++i) stats_host[8 + i] = ws->prof2[i];
   }
   if (enable) {
     for (int i = 0; i < 8; ++i) ws->prof[i] = 0.0;
-    for (int i = 0; i < 4; ++i) ws->prof2[i] = 0.0;
+    for (int i = 0; i < 5; ++i) ws->prof2[i] = 0.0;
     for (int i = 0; i < 3; ++i)
       if (!ws->ev[i]) CK(ctx, cudaEventCreate(&ws->ev[i]));
   }
@@ -1025,18 +1026,30 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
                           finA + (g_smem ? gblk : 0)});
+  // Resident CSR slab (small slabs only, within two blocks' worth of shared
+  // memory per SM): placed after everything else; the kernel keeps it only
+  // when its own slab fits the budget.
+  const size_t csr_off = (smem + 127) & ~size_t(127);
+  const size_t per_block_cap = 110 * 1024;
+  const size_t csr_budget = (direct && ws->resident_csr && csr_off + 4096 <= per_block_cap)
+                                ? per_block_cap - csr_off : 0;
+  if (csr_budget) smem = csr_off + csr_budget;
   cudaError_t e;
   if (ws->dtype == SAD_F64) {
     PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
+    a.csr_off = (int)csr_off;
+    a.csr_budget = (int)csr_budget;
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
+    a.csr_off = (int)csr_off;
+    a.csr_budget = (int)csr_budget;
     e = coop_dispatch_z(a, ws, op, s, smem);
   }
   if (e != cudaSuccess)
@@ -1054,7 +1067,7 @@ static int persistent_collect(sad_gmres* ws, cudaStream_t s) {
     CK(ctx, cudaEventElapsedTime(&ms, ws->ev[0], ws->ev[1]));
     double st[16];
     CK(ctx, cudaMemcpy(st, ws->stats_dev, sizeof(st), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 4; ++i) ws->prof2[i] += st[8 + i] * 1e-6;
+    for (int i = 0; i < 5; ++i) ws->prof2[i] += st[8 + i] * 1e-6;
     ws->prof[0] += ms;
     ws->prof[1] += 1;
     ws->prof[2] += st[0];
@@ -1082,6 +1095,9 @@ extern "C" int sad_gmres_set_option(sad_gmres* ws, int key, int value) {
     case SAD_OPT_MIN_ELEMS_PER_THREAD:
       if (value < 1) return set_err(ws->ctx, SAD_EINVAL, "min elements per thread must be >= 1");
       ws->min_elems_per_thread = value;
+      return SAD_OK;
+    case SAD_OPT_RESIDENT_CSR:
+      ws->resident_csr = value != 0;
       return SAD_OK;
     case SAD_OPT_DIRECT_A:
       if (value < -1 || value > 1) return set_err(ws->ctx, SAD_EINVAL, "direct-A option must be -1, 0 or 1");

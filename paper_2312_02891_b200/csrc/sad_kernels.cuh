@@ -319,6 +319,63 @@ __device__ __forceinline__ void spmm_rows(const int* __restrict__ rowptr,
   }
 }
 
+// spmm_rows with the block's CSR slab resident in shared memory (rp_s holds
+// rowptr[r0 .. r1], ci_s / vv_s the nonzeros from kb on): only the x gathers
+// touch L2, SL of them per row in flight.  Same summation order as spmm_rows.
+template <typename XT, typename VT, bool PRE, bool SIGMA, int R, int U, int SL>
+__device__ __forceinline__ void spmm_rows_s(const int* rp_s, long long r0, const int* ci_s,
+                                            const VT* vv_s, int kb,
+                                            const XT* __restrict__ dinv, double2 sigma,
+                                            const XT* x, const long long* idx, int c,
+                                            XT* acc, XT* xi) {
+  int k0[U], len[U];
+  int maxlen = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    acc[u] = zero<XT>();
+    xi[u] = zero<XT>();
+    if (idx[u] >= 0) {
+      const int lr = (int)(idx[u] / R - r0);
+      k0[u] = rp_s[lr] - kb;
+      len[u] = rp_s[lr + 1] - rp_s[lr];
+      xi[u] = x[idx[u]];
+    } else {
+      k0[u] = 0;
+      len[u] = 0;
+    }
+    maxlen = max(maxlen, len[u]);
+  }
+  for (int q = 0; q < maxlen; q += SL) {
+    XT xg[U][SL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int t = 0; t < SL; ++t) {
+        xg[u][t] = zero<XT>();
+        if (q + t < len[u]) {
+          const int col = ci_s[k0[u] + q + t];
+          xg[u][t] = x[(long long)col * R + c];
+          if (PRE) xg[u][t] = mul(__ldg(dinv + col), xg[u][t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int t = 0; t < SL; ++t)
+        if (q + t < len[u]) acc[u] = fma_(vv_s[k0[u] + q + t], xg[u][t], acc[u]);
+  }
+  if (SIGMA) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (idx[u] >= 0) {
+        const XT xs = PRE ? mul(__ldg(dinv + idx[u] / R), xi[u]) : xi[u];
+        acc[u] = fma_(from_c<XT>(sigma), xs, acc[u]);
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------
 // Kernel 1: fused shifted SpMM
 //   y = scale_c * [ A * (D^-1 x) + sigma * D^-1 x_row ]   (ARNOLDI, PRE)

@@ -22,6 +22,8 @@
 // with ld.cg.
 #pragma once
 
+#include <type_traits>
+
 #include "sad_kernels.cuh"
 #include "sad_spmm_bulk.cuh"
 
@@ -64,6 +66,8 @@ struct PArgs {
   int g_smem;            // stage the Gram block in shared memory (fits)
   int stage_bytes;       // bytes of one phase-A TMA stage (128-aligned)
   int direct_a;          // phase A with direct loads and per-warp sums (small slabs)
+  int csr_off;           // dynamic-smem byte offset of the resident CSR slab
+  int csr_budget;        // bytes available there (0 = CSR read from global)
   PState st;
 };
 
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   const bool prof = a.prof != 0;                                  // phase timers (profiling)
   unsigned long long tphase = 0;
   double acc_bytes = 0.0, acc_steps = 0.0, acc_cycles = 1.0;
-  double t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // A, C, X, R, workA, workC (ns, block 0)
+  double t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // A, C, X, R, workA, workC, spmmA (ns, block 0)
 
   __shared__ double s_w2[kWarps][8];
   __shared__ int s_any;
@@ -261,7 +265,49 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
     for (int q = 0; q < kStages; ++q) mbar_init(s_full + q, 1);
     fence_mbar_init();
   }
+  // The block's CSR slab stays in shared memory for the whole solve when it
+  // fits (the operator is constant): every SpMM then reads rowptr / colidx /
+  // values from shared memory and only gathers x from L2.
+  const int* rp_s = nullptr;
+  const int* ci_s = nullptr;
+  const VT* vv_s = nullptr;
+  int kb_s = 0;
+  bool csr_s = false;
+  if (a.csr_budget > 0 && r1 > r0) {
+    kb_s = __ldg(a.rowptr + r0);
+    const int nz = __ldg(a.rowptr + r1) - kb_s;
+    const size_t rp_b = ((size_t)(r1 - r0 + 1) * 4 + 15) & ~size_t(15);
+    const size_t ci_b = ((size_t)nz * 4 + 15) & ~size_t(15);
+    if (rp_b + ci_b + (size_t)nz * sizeof(VT) <= (size_t)a.csr_budget) {
+      unsigned char* base = reinterpret_cast<unsigned char*>(smem_p) + a.csr_off;
+      int* rp_w = reinterpret_cast<int*>(base);
+      int* ci_w = reinterpret_cast<int*>(base + rp_b);
+      VT* vv_w = reinterpret_cast<VT*>(base + rp_b + ci_b);
+      const VT* vals_g = reinterpret_cast<const VT*>(a.vals);
+      for (long long i = threadIdx.x; i <= r1 - r0; i += kThreads) rp_w[i] = __ldg(a.rowptr + r0 + i);
+      for (int i = threadIdx.x; i < nz; i += kThreads) {
+        ci_w[i] = __ldg(a.colidx + kb_s + i);
+        vv_w[i] = __ldg(vals_g + kb_s + i);
+      }
+      rp_s = rp_w;
+      ci_s = ci_w;
+      vv_s = vv_w;
+      csr_s = true;
+    }
+  }
   __syncthreads();
+  // SpMM rows of this block from the resident slab, or from global memory
+  auto spmm = [&](auto pre_tag, auto u_tag, const XT* xin, const long long* idx, XT* acc, XT* xi) {
+    constexpr bool P = decltype(pre_tag)::value;
+    constexpr int U = decltype(u_tag)::value;
+    constexpr int SL = (32 / (U * (int)(sizeof(XT) / 8))) < 2 ? 2 : 32 / (U * (int)(sizeof(XT) / 8));
+    if (csr_s)
+      spmm_rows_s<XT, VT, P, SIGMA, R, U, SL>(rp_s, r0, ci_s, vv_s, kb_s, a.dinv, a.sigma, xin,
+                                              idx, c, acc, xi);
+    else
+      spmm_rows<XT, VT, P, SIGMA, R, U>(a.rowptr, a.colidx, reinterpret_cast<const VT*>(a.vals),
+                                        a.dinv, a.sigma, xin, idx, c, acc, xi);
+  };
 
   // ---- init: x = 0, V_0 = b, ||b||^2 -> restart decision --------------------
   {
@@ -361,9 +407,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               const int lr = (u * kWarps + warp) * GPW + grp;
               idx[u] = (lane_ok && lr < nrows) ? (base + lr) * R + c : -1;
             }
-            spmm_rows<XT, VT, PRE, SIGMA, R, UD>(a.rowptr, a.colidx,
-                                                 reinterpret_cast<const VT*>(a.vals), a.dinv,
-                                                 a.sigma, vj, idx, c, wv, xv);
+            const unsigned long long tsp = (timing && prof) ? gtimer() : 0ull;
+            spmm(std::integral_constant<bool, PRE>{}, std::integral_constant<int, UD>{}, vj, idx,
+                 wv, xv);
+            if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
 #pragma unroll
             for (int u = 0; u < UD; ++u) {
               if (idx[u] >= 0) {
@@ -442,9 +489,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               const long long row = base + lr[u];
               idx[u] = (lane_ok && lr[u] < nrows) ? row * R + c : -1;
             }
-            spmm_rows<XT, VT, PRE, SIGMA, R, UA>(a.rowptr, a.colidx,
-                                                 reinterpret_cast<const VT*>(a.vals), a.dinv,
-                                                 a.sigma, vj, idx, c, wv, xv);
+            const unsigned long long tsp = (timing && prof) ? gtimer() : 0ull;
+            spmm(std::integral_constant<bool, PRE>{}, std::integral_constant<int, UA>{}, vj, idx,
+                 wv, xv);
+            if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
   #pragma unroll
             for (int u = 0; u < UA; ++u) {
               if (idx[u] >= 0) {
@@ -833,9 +881,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           const long long row = base + ((long long)u * kWarps + warp) * GPW + grp;
           idx[u] = (lane_ok && row < r1) ? row * R + c : -1;
         }
-        spmm_rows<XT, VT, false, SIGMA, R, UA>(a.rowptr, a.colidx,
-                                               reinterpret_cast<const VT*>(a.vals), a.dinv,
-                                               a.sigma, a.x, idx, c, acc, xi);
+        spmm(std::integral_constant<bool, false>{}, std::integral_constant<int, UA>{}, a.x, idx,
+             acc, xi);
 #pragma unroll
         for (int u = 0; u < UA; ++u) {
           if (idx[u] < 0) continue;
@@ -898,6 +945,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
     st.stats[6] += t_acc[3];
     st.stats[8] += t_acc[4];
     st.stats[9] += t_acc[5];
+    st.stats[12] += t_acc[6];
   }
 }
 

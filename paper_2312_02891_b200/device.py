@@ -185,8 +185,8 @@ class GmresWorkspace:
                    self._ctx)
 
     def profile(self, enable):
-        """Enable/disable profiling; returns the 12 counters accumulated so far."""
-        out = np.zeros(12, dtype=np.float64)
+        """Enable/disable profiling; returns the 13 counters accumulated so far."""
+        out = np.zeros(13, dtype=np.float64)
         _lib.check(_lib.load().sad_gmres_profile(self.handle, 1 if enable else 0,
                                                  out.ctypes.data), self._ctx)
         return out

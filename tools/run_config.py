@@ -68,7 +68,7 @@ def main():
         for ws in wss:
             ws.profile(True)
         eng.run()
-        tot = np.zeros(12)
+        tot = np.zeros(13)
         for ws in wss:
             tot += ws.profile(False)
         out["profile"] = {"kernel_ms": tot[0], "launches": int(tot[1]),
@@ -76,7 +76,7 @@ def main():
                           "phaseA_ms": tot[3], "arnoldi_steps": int(tot[4]),
                           "phaseC_ms": tot[5], "cycle_end_ms": tot[6], "cycles": int(tot[7]),
                           "workA_ms": tot[8], "workC_ms": tot[9], "finA_ms": tot[10],
-                          "finC_ms": tot[11]}
+                          "finC_ms": tot[11], "spmmA_ms": tot[12]}
     if not args.no_verify:
         t0 = time.perf_counter()
         trn = true_residual_norm(prob, sol)

@@ -31,14 +31,14 @@ def main():
     seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
     warnings.simplefilter("ignore")
     for engine, conc, mepth, direct in itertools.product(["persistent"], [True, False],
-                                                         [1, 2, 4, 8], [1]):
+                                                         [2], [0, 1]):
         eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                            concurrent=conc, engine=engine)
         eng.warm()
         eng.run()
         for b in (eng.bA, eng.bB):
-            b.phase_a = "direct" if direct else "tma"
             for ws in b._workspaces.values():
+                ws.set_option(_lib.SAD_OPT_RESIDENT_CSR, direct)
                 ws.set_option(_lib.SAD_OPT_MIN_ELEMS_PER_THREAD, mepth)
         ts = []
         for _ in range(args.reps):
@@ -51,7 +51,7 @@ def main():
             ws.profile(True)
         eng.run()
         prof = sum(ws.profile(False) for ws in wss)
-        print(f"engine={engine} concurrent={conc} min_elems={mepth} direct={direct}: solve {min(ts)*1e3:.1f} ms "
+        print(f"engine={engine} concurrent={conc} min_elems={mepth} resident_csr={direct}: solve {min(ts)*1e3:.1f} ms "
               f"(steps {rep.outer_iterations}, inner {rep.sum_inner_A}/{rep.sum_inner_B}) "
               f"kernel {prof[0]:.1f} ms, {prof[2]/prof[0]/1e6:.0f} GB/s, phaseA {prof[3]:.1f} "
               f"phaseC {prof[5]:.1f} cycle-end {prof[6]:.1f} ms, steps {int(prof[4])} | "
