@@ -1022,7 +1022,11 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
                                         : (size_t)ws->n <= 2 * tile_rows * (size_t)sms;
   const size_t stage = direct ? 0 : ((tile_rows * R * ws->esz + 32 + 127) & ~size_t(127));
   const size_t sums = 2 * m1 * R * ws->esz * (direct ? 1 + kWarps : 1);
-  size_t smem = std::max({(size_t)kStages * stage + sums,                 // ring + sums
+  // TMA path: the basis ring and the A1 CSR ring share one region
+  const size_t vsz = op->vals_complex ? 16 : 8;
+  const size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
+                                                  (size_t)kStagesA1 * a1_stage_bytes((int)R, vsz));
+  size_t smem = std::max({ring_bytes + sums,                              // rings + sums
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
                           finA + (g_smem ? gblk : 0)});
@@ -1040,6 +1044,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
+    a.ring_bytes = (int)ring_bytes;
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
     e = coop_dispatch_d(a, ws, op, s, smem);
@@ -1048,6 +1053,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
+    a.ring_bytes = (int)ring_bytes;
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
     e = coop_dispatch_z(a, ws, op, s, smem);

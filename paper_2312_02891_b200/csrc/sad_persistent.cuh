@@ -31,6 +31,19 @@ namespace sad {
 
 constexpr int kStages = 4;   // phase-A TMA ring depth
 constexpr int kGroup = 2;    // basis blocks reduced per __syncthreads (kStages = 2 * kGroup)
+constexpr int kStagesA1 = 3; // staged-SpMM (sub-phase A1) CSR ring depth
+
+// Sub-phase A1 (large slabs): CSR tiles of kWarps * (32 / R) rows -- one row per
+// lane group -- staged by TMA; up to 12 nonzeros per row are staged, denser
+// tiles read their nonzeros from global memory.
+__host__ __device__ constexpr int a1_tile_rows(int R) { return kWarps * (32 / R); }
+__host__ __device__ constexpr size_t a1_al16(size_t b) { return (b + 15) & ~size_t(15); }
+__host__ __device__ constexpr size_t a1_rp_bytes(int R) { return a1_al16((size_t)(a1_tile_rows(R) + 1) * 4 + 64); }
+__host__ __device__ constexpr size_t a1_ci_bytes(int R) { return a1_al16((size_t)12 * a1_tile_rows(R) * 4 + 64); }
+__host__ __device__ constexpr size_t a1_vv_bytes(int R, size_t vsz) { return a1_al16((size_t)12 * a1_tile_rows(R) * vsz + 64); }
+__host__ __device__ constexpr size_t a1_stage_bytes(int R, size_t vsz) {
+  return (a1_rp_bytes(R) + a1_ci_bytes(R) + a1_vv_bytes(R, vsz) + 127) & ~size_t(127);
+}
 
 struct PState {
   GState g;              // j, any_active, active, done, kdim, iters, S, H, cs, sn, g, ycoef, ...
@@ -66,6 +79,7 @@ struct PArgs {
   int g_smem;            // stage the Gram block in shared memory (fits)
   int stage_bytes;       // bytes of one phase-A TMA stage (128-aligned)
   int direct_a;          // phase A with direct loads and per-warp sums (small slabs)
+  int ring_bytes;        // dynamic-smem bytes of the phase-A rings (basis / A1 CSR)
   int csr_off;           // dynamic-smem byte offset of the resident CSR slab
   int csr_budget;        // bytes available there (0 = CSR read from global)
   PState st;
@@ -261,8 +275,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   __shared__ int s_soff[kStages];
   __shared__ XT s_ph[kGroup][kWarps][R], s_pg[kGroup][kWarps][R];
   unsigned long long ring = 0;   // basis-tile copies issued so far (block-uniform)
+  // sub-phase A1 CSR ring
+  __shared__ __align__(8) unsigned long long s_full1[kStagesA1];
+  __shared__ int s_off1[kStagesA1][3], s_kb1[kStagesA1], s_st1[kStagesA1];
+  unsigned long long ring1 = 0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kStages; ++q) mbar_init(s_full + q, 1);
+    for (int q = 0; q < kStagesA1; ++q) mbar_init(s_full1 + q, 1);
     fence_mbar_init();
   }
   // The block's CSR slab stays in shared memory for the whole solve when it
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         // tile's rows of one basis block); per basis block the block reduces its
         // h / g contributions through shared memory in a fixed order.
         unsigned char* const smem_c = reinterpret_cast<unsigned char*>(smem_p);
-        XT* s_blk = reinterpret_cast<XT*>(smem_c + (size_t)kStages * a.stage_bytes);  // [2J][R]
+        XT* s_blk = reinterpret_cast<XT*>(smem_c + (size_t)a.ring_bytes);  // [2J][R]
         for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) s_blk[o] = zero<XT>();
         double w2 = 0.0;
         __syncthreads();
@@ -463,6 +482,101 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             s_blk[o] = t;
           }
         } else {
+          // ---- sub-phase A1: w = Op(D^-1 v_j) for the whole slab, CSR tiles
+          // staged by TMA (kStagesA1 deep), one row per lane group, 5 gathers of
+          // x in flight; w (and Z) written once, read back below from L2 ----
+          {
+            const unsigned long long tsp = (timing && prof) ? gtimer() : 0ull;
+            constexpr int T1 = a1_tile_rows(R);
+            constexpr int CAP1 = 12 * T1;
+            constexpr size_t CI1 = a1_ci_bytes(R), VV1 = a1_vv_bytes(R, sizeof(VT));
+            constexpr size_t SB1 = a1_stage_bytes(R, sizeof(VT));
+            const VT* vals_g = reinterpret_cast<const VT*>(a.vals);
+            const long long ntile = (r1 - r0 + T1 - 1) / T1;
+            auto issue1 = [&](long long t, int q) {
+              const long long row0 = r0 + t * T1;
+              const int rows = (int)min((long long)T1, r1 - row0);
+              const int kb = __ldg(a.rowptr + row0), ke = __ldg(a.rowptr + row0 + rows);
+              const int nz = ke - kb;
+              unsigned long long p0, p1, c0 = 0, c1 = 0, v0 = 0, v1 = 0;
+              aligned_range(a.rowptr, row0, rows + 1, 4, p0, p1);
+              const bool stg = nz + 8 <= CAP1;
+              unsigned bytes = (unsigned)(p1 - p0);
+              if (stg) {
+                aligned_range(a.colidx, kb, nz, 4, c0, c1);
+                aligned_range(vals_g, kb, nz, (int)sizeof(VT), v0, v1);
+                bytes += (unsigned)((c1 - c0) + (v1 - v0));
+              }
+              unsigned char* sb = smem_c + (size_t)q * SB1;
+              s_kb1[q] = kb;
+              s_st1[q] = stg ? 1 : 0;
+              s_off1[q][2] = (int)((reinterpret_cast<unsigned long long>(a.rowptr + row0) - p0) / 4);
+              if (stg) {
+                s_off1[q][0] = (int)((reinterpret_cast<unsigned long long>(a.colidx + kb) - c0) / 4);
+                s_off1[q][1] = (int)((reinterpret_cast<unsigned long long>(vals_g + kb) - v0) / sizeof(VT));
+              }
+              mbar_expect_tx(s_full1 + q, bytes);
+              bulk_g2s(sb + CI1 + VV1, reinterpret_cast<const void*>(p0), (unsigned)(p1 - p0), s_full1 + q);
+              if (stg) {
+                if (c1 > c0) bulk_g2s(sb, reinterpret_cast<const void*>(c0), (unsigned)(c1 - c0), s_full1 + q);
+                if (v1 > v0) bulk_g2s(sb + CI1, reinterpret_cast<const void*>(v0), (unsigned)(v1 - v0), s_full1 + q);
+              }
+            };
+            if (threadIdx.x == 0) {
+              fence_proxy_async();
+              for (long long t = 0; t < min((long long)kStagesA1, ntile); ++t)
+                issue1(t, (int)((ring1 + t) % kStagesA1));
+            }
+            for (long long t = 0; t < ntile; ++t) {
+              const unsigned long long kk = ring1 + t;
+              const int q = (int)(kk % kStagesA1);
+              mbar_wait(s_full1 + q, (unsigned)((kk / kStagesA1) & 1));
+              const long long row0 = r0 + t * T1;
+              const int lr = warp * GPW + grp;
+              if (lane_ok && row0 + lr < r1) {
+                const unsigned char* sb = smem_c + (size_t)q * SB1;
+                const int* rp = reinterpret_cast<const int*>(sb + CI1 + VV1) + s_off1[q][2];
+                const bool stg = s_st1[q] != 0;
+                const int kb = s_kb1[q];
+                const int* ci = stg ? reinterpret_cast<const int*>(sb) + s_off1[q][0] - kb : a.colidx;
+                const VT* vv = stg ? reinterpret_cast<const VT*>(sb + CI1) + s_off1[q][1] - kb : vals_g;
+                const long long row = row0 + lr;
+                const long long id = row * R + c;
+                const int k0 = rp[lr], k1 = rp[lr + 1];
+                XT acc = zero<XT>();
+                constexpr int KB1 = 5;
+                for (int k = k0; k < k1; k += KB1) {
+                  XT xg[KB1];
+#pragma unroll
+                  for (int tt = 0; tt < KB1; ++tt) {
+                    xg[tt] = zero<XT>();
+                    if (k + tt < k1) {
+                      const int col = ci[k + tt];
+                      xg[tt] = vj[(long long)col * R + c];
+                      if (PRE) xg[tt] = mul(__ldg(a.dinv + col), xg[tt]);
+                    }
+                  }
+#pragma unroll
+                  for (int tt = 0; tt < KB1; ++tt)
+                    if (k + tt < k1) acc = fma_(vv[k + tt], xg[tt], acc);
+                }
+                const XT xi = vj[id];
+                const XT xs = PRE ? mul(__ldg(a.dinv + row), xi) : xi;
+                if (SIGMA) acc = fma_(from_c<XT>(a.sigma), xs, acc);
+                const XT wv1 = sscal(sj, acc);
+                w[id] = wv1;
+                if (FLEX) a.Z[(long long)j * a.stride + id] = sscal(sj, xs);
+                w2 += abs2(wv1);
+              }
+              __syncthreads();   // stage q consumed
+              if (threadIdx.x == 0 && t + kStagesA1 < ntile) {
+                fence_proxy_async();
+                issue1(t + kStagesA1, q);
+              }
+            }
+            ring1 += (unsigned long long)ntile;
+            if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
+          }
           for (long long base = r0; base < r1; base += T) {
             const long long nrows = min((long long)T, r1 - base);
             auto issue = [&](int i, int q) {
@@ -479,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               fence_proxy_async();
               for (int i = 0; i < min(kStages, J); ++i) issue(i, (int)((ring + i) % kStages));
             }
-            // the tile's SpMM (overlaps with the first basis copies)
+            // the tile's rows of w (from A1) and v_j (overlaps with the first basis copies)
             XT wv[UA], xv[UA];
             long long idx[UA];
             int lr[UA];
@@ -488,22 +602,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               lr[u] = (u * kWarps + warp) * GPW + grp;
               const long long row = base + lr[u];
               idx[u] = (lane_ok && lr[u] < nrows) ? row * R + c : -1;
-            }
-            const unsigned long long tsp = (timing && prof) ? gtimer() : 0ull;
-            spmm(std::integral_constant<bool, PRE>{}, std::integral_constant<int, UA>{}, vj, idx,
-                 wv, xv);
-            if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
-  #pragma unroll
-            for (int u = 0; u < UA; ++u) {
-              if (idx[u] >= 0) {
-                wv[u] = sscal(sj, wv[u]);
-                w[idx[u]] = wv[u];
-                if (FLEX) {
-                  XT zi = PRE ? mul(__ldg(a.dinv + idx[u] / R), xv[u]) : xv[u];
-                  a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
-                }
-                w2 += abs2(wv[u]);
-              }
+              wv[u] = idx[u] >= 0 ? w[idx[u]] : zero<XT>();
+              xv[u] = idx[u] >= 0 ? vj[idx[u]] : zero<XT>();
             }
             // basis blocks in groups of kGroup per __syncthreads (the other half of
             // the ring is in flight meanwhile)
