@@ -274,6 +274,10 @@ class LowRankSolution:
     """X ~= Z diag(gamma_k I_r) Y^* (adi.py:248-272).  Factors may stay on the
     device (``device_blocks``); ``Z``/``Y`` materialise host arrays lazily."""
 
+    #: factors up to this size are concatenated on the device and downloaded in
+    #: one copy; larger ones in chunks of this size
+    CONCAT_BYTES = 4 << 30
+
     def __init__(self, Z=None, gammas=(), Y=None, r=1, z_blocks=None, y_blocks=None,
                  n=None, m=None):
         self._Z, self._Y = Z, Y
@@ -290,13 +294,28 @@ class LowRankSolution:
             return np.zeros((rows, 0), dtype=complex)
         import torch
         k = len(blocks)
-        dev = torch.cat(blocks, dim=1)            # (rows, k*r) contiguous on the device
-        if dev.dtype != torch.complex128:
-            dev = dev.to(torch.complex128)
-        host = torch.empty((rows, k * r), dtype=torch.complex128, pin_memory=True)
-        host.copy_(dev, non_blocking=True)        # one contiguous D2H copy
-        torch.cuda.synchronize(dev.device)
-        return host.numpy()
+        total = rows * k * r * 16
+        if total <= LowRankSolution.CONCAT_BYTES:
+            dev = torch.cat(blocks, dim=1)            # (rows, k*r) contiguous on the device
+            if dev.dtype != torch.complex128:
+                dev = dev.to(torch.complex128)
+            host = torch.empty((rows, k * r), dtype=torch.complex128, pin_memory=True)
+            host.copy_(dev, non_blocking=True)        # one contiguous D2H copy
+            torch.cuda.synchronize(dev.device)
+            return host.numpy()
+        # large factors (configs 3-5): bounded device staging, chunk by chunk
+        out = np.empty((rows, k * r), dtype=np.complex128)
+        group = max(1, LowRankSolution.CONCAT_BYTES // (rows * r * 16))
+        stage = None
+        for i0 in range(0, k, group):
+            i1 = min(k, i0 + group)
+            dev = torch.cat(blocks[i0:i1], dim=1).to(torch.complex128)
+            if stage is None or stage.shape != dev.shape:
+                stage = torch.empty(dev.shape, dtype=torch.complex128, pin_memory=True)
+            stage.copy_(dev)
+            out[:, i0 * r:i1 * r] = stage.numpy()
+            del dev
+        return out
 
     @property
     def Z(self):
