@@ -35,7 +35,7 @@ enum sad_status {
   SAD_EINVAL = 1,      /* ValueError / DimensionMismatch (krylov.py:29-35, sparse.py:112-114) */
   SAD_EBREAKDOWN = 2,  /* FactorizationBreakdown: zero Jacobi diagonal (precond.py:274-275) */
   SAD_ECUDA = 3,       /* CUDA runtime failure */
-  SAD_ENCCL = 4,       /* reserved for the multi-GPU path */
+  SAD_ENCCL = 4,       /* NCCL missing or a collective failed (row-partitioned solves) */
   SAD_ENOMEM = 5       /* device allocation failed */
 };
 
@@ -53,6 +53,8 @@ typedef struct sad_ctx sad_ctx;
 typedef struct sad_csr sad_csr;
 typedef struct sad_op sad_op;
 typedef struct sad_gmres sad_gmres;
+typedef struct sad_comm sad_comm;
+typedef struct sad_halo sad_halo;
 
 /* ABI version (bumped on any signature change). */
 int sad_version(void);
@@ -212,6 +214,66 @@ int sad_ts_hgemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int xdtype, co
                  int nvec, const void* v_dev, double* out_host, void* stream);
 int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int xdtype, const void* x_dev,
                 int nvec, const double* c_host, void* y_dev, int accumulate, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Row-partitioned inner solves (one operator split into
+ * contiguous row slabs, halo exchange before every SpMM, all-reduce of every
+ * block dot; Hessenberg, Givens and masks replicated on every rank).  The
+ * reference has no multi-process path: these extend SolverBinding.solve
+ * (adi.py:473-488) to a slab of the operator; the Python mirror is
+ * paper_2312_02891_b200/rowpart.py.
+ *
+ * Communicators: NCCL (one process per GPU; sad_comm_unique_id on rank 0, the
+ * 128 bytes broadcast by the caller, sad_comm_create_nccl on every rank;
+ * libnccl.so.2 is bound with dlopen), or an in-process group of `nranks` ranks
+ * on one device (sad_comm_create_local) whose kernels run in rank order with
+ * a device sum for the all-reduce and device copies for send/recv.
+ * Every sad_dist_* call takes `nl` local ranks: 1 for NCCL, nranks for a group;
+ * per-rank arguments are arrays of length nl.
+ * ------------------------------------------------------------------------- */
+int sad_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+const char* sad_comm_nccl_error(void);
+int sad_comm_create_nccl(sad_ctx* ctx, int nranks, int rank, const uint8_t* id, sad_comm** out);
+int sad_comm_create_local(sad_ctx* ctx, int nranks, sad_comm** out);
+int sad_comm_destroy(sad_comm* comm);
+int sad_comm_size(const sad_comm* comm);
+int sad_comm_local_ranks(const sad_comm* comm);
+
+/* Halo plan of one rank: rows [0, n_loc) are local, [n_loc, n_loc + n_halo)
+ * the halo, grouped by owning rank q at recv_off[q] .. recv_off[q+1];
+ * send_rows[send_off[q] .. send_off[q+1]) are the local rows rank q needs. */
+int sad_halo_create(sad_ctx* ctx, int nranks, int rank, int64_t n_loc, int64_t n_halo,
+                    const int64_t* send_off, const int32_t* send_rows, const int64_t* recv_off,
+                    sad_halo** out);
+int sad_halo_destroy(sad_halo* halo);
+
+/* Local slab CSR, columns remapped to [local | halo] in the global matrix's
+ * per-row order (not increasing after the remap; no transpose is built). */
+int sad_local_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz,
+                         const int32_t* rowptr, const int32_t* colidx, const double* vals,
+                         sad_csr** out);
+/* Op = slab + sigma I (the B side passes the slab of B^T and conj(sigma));
+ * Jacobi dinv over [local | halo], the halo part filled by sad_dist_op_setup. */
+int sad_local_op_create(sad_ctx* ctx, const sad_csr* slab, double sre, double sim,
+                        int precond_kind, sad_op** out);
+int sad_dist_op_setup(sad_comm* comm, int nl, sad_op* const* ops, sad_halo* const* halos,
+                      void* stream);
+/* halo rows of n_ext-row blocks; y = Op x (x_ext's halo rows are overwritten) */
+int sad_dist_halo_exchange(sad_comm* comm, int nl, sad_halo* const* halos, void* const* blocks,
+                           int r, int dtype, void* stream);
+int sad_dist_op_apply(sad_comm* comm, int nl, sad_op* const* ops, sad_halo* const* halos, int r,
+                      int dtype, void* const* x_ext, void* const* y, void* stream);
+/* in-place sum over the ranks of `count` doubles per rank buffer */
+int sad_dist_allreduce(sad_comm* comm, int nl, double* const* bufs, int64_t count, void* stream);
+/* workspace of one rank: basis blocks of n_ext rows (the halo travels with them) */
+int sad_dist_gmres_create(sad_ctx* ctx, int64_t n_loc, int64_t n_ext, int r, int dtype,
+                          int restart, int flexible, sad_gmres** out);
+/* sad_gmres_solve on a row-partitioned operator: rhs/x/res are n_loc x r
+ * slabs per local rank; iters/resnorm/conv are replicated (filled once). */
+int sad_dist_gmres_solve(sad_comm* comm, int nl, sad_gmres* const* ws, sad_op* const* ops,
+                         sad_halo* const* halos, const void* const* rhs_dev, void* const* x_dev,
+                         void* const* res_dev, double tol_col, int maxit, void* stream,
+                         int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
 
 #ifdef __cplusplus
 }

@@ -82,7 +82,7 @@ def build(force=False, verbose=False, jobs=None):
     if bad:
         raise RuntimeError(f"nvcc failed for {[os.path.basename(o) for o, _, _ in bad]}; "
                            f"see {log_path}\n" + bad[0][2][-4000:])
-    cmd = [nv] + ARCH + ["-shared", "-o", OUT] + [o for o, _, _ in results]
+    cmd = [nv] + ARCH + ["-shared", "-o", OUT] + [o for o, _, _ in results] + ["-ldl"]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError("link failed:\n" + proc.stderr[-4000:])

@@ -60,6 +60,30 @@ SIGNATURES = {
                                 _vp]),
     "sad_ts_gemv": (_c.c_int, [_vp, _i64, _i64, _i64, _c.c_int, _vp, _c.c_int, _vp, _vp,
                                _c.c_int, _vp]),
+    # row-partitioned solves (per-rank arguments are arrays of nl pointers)
+    "sad_comm_unique_id": (_c.c_int, [_vp]),
+    "sad_comm_nccl_error": (_c.c_char_p, []),
+    "sad_comm_create_nccl": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _c.POINTER(_vp)]),
+    "sad_comm_create_local": (_c.c_int, [_vp, _c.c_int, _c.POINTER(_vp)]),
+    "sad_comm_destroy": (_c.c_int, [_vp]),
+    "sad_comm_size": (_c.c_int, [_vp]),
+    "sad_comm_local_ranks": (_c.c_int, [_vp]),
+    "sad_halo_create": (_c.c_int, [_vp, _c.c_int, _c.c_int, _i64, _i64, _vp, _vp, _vp,
+                                   _c.POINTER(_vp)]),
+    "sad_halo_destroy": (_c.c_int, [_vp]),
+    "sad_local_csr_create": (_c.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp,
+                                        _c.POINTER(_vp)]),
+    "sad_local_op_create": (_c.c_int, [_vp, _vp, _c.c_double, _c.c_double, _c.c_int,
+                                       _c.POINTER(_vp)]),
+    "sad_dist_op_setup": (_c.c_int, [_vp, _c.c_int, _vp, _vp, _vp]),
+    "sad_dist_halo_exchange": (_c.c_int, [_vp, _c.c_int, _vp, _vp, _c.c_int, _c.c_int, _vp]),
+    "sad_dist_op_apply": (_c.c_int, [_vp, _c.c_int, _vp, _vp, _c.c_int, _c.c_int, _vp, _vp,
+                                     _vp]),
+    "sad_dist_allreduce": (_c.c_int, [_vp, _c.c_int, _vp, _i64, _vp]),
+    "sad_dist_gmres_create": (_c.c_int, [_vp, _i64, _i64, _c.c_int, _c.c_int, _c.c_int,
+                                         _c.c_int, _c.POINTER(_vp)]),
+    "sad_dist_gmres_solve": (_c.c_int, [_vp, _c.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        _c.c_double, _c.c_int, _vp, _vp, _vp, _vp]),
 }
 
 

@@ -546,7 +546,8 @@ class DeviceAdi:
     (the bench times repeated runs with the inputs already in HBM)."""
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
-                 device=0, concurrent="auto", engine="persistent", phase_a="auto"):
+                 device=0, concurrent="auto", engine="persistent", phase_a="auto",
+                 row_ranks=1):
         import torch
         if not isinstance(problem, SylvesterProblem):
             problem = SylvesterProblem.from_reference(problem)
@@ -578,6 +579,18 @@ class DeviceAdi:
         na, nb = problem.n, problem.m
         sm_a = max(1, min(nsm - 1, int(round(nsm * na / (na + nb))))) if concurrent else 0
         sm_b = max(1, nsm - sm_a) if concurrent else 0
+        if row_ranks > 1:
+            # each side row-partitioned over `row_ranks` slabs, all ranks in this
+            # process on one device (rowpart.py; the one-GPU test vehicle)
+            from .rowpart import RowPartitionedGmres
+            self.concurrent = False
+            self._pool = None
+            mk = dict(max_iterations=config.max_inner_iterations, restart=restart,
+                      flexible=flexible, device=device, nranks=row_ranks, comm="local")
+            self.bA = RowPartitionedGmres("A", problem.A, problem.M, "iterative", kind_a, **mk)
+            self.bB = RowPartitionedGmres("B", problem.B, problem.C, "iterative", kind_b, **mk)
+            self._init_tail(problem)
+            return
         self.bA = GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
@@ -586,13 +599,17 @@ class DeviceAdi:
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
                                   max_sms=sm_b, phase_a=phase_a)
+        self._pool = ThreadPoolExecutor(max_workers=2) if concurrent else None
+        self._init_tail(problem)
+
+    def _init_tail(self, problem):
+        import torch
         self.Md = self.bA.mass      # M (for M z)
         self.Cd = self.bB.mass      # C with transpose (for C^T y)
         self.f = torch.from_numpy(np.ascontiguousarray(problem.f)).to(self.dev, self.tdtype)
         self.g = torch.from_numpy(np.ascontiguousarray(problem.g)).to(self.dev, self.tdtype)
         self.sA = torch.cuda.Stream(device=self.dev)
         self.sB = torch.cuda.Stream(device=self.dev)
-        self._pool = ThreadPoolExecutor(max_workers=2) if concurrent else None
         self.h2d_bytes = (problem.f.nbytes + problem.g.nbytes)
 
     def warm(self):
@@ -712,11 +729,16 @@ def _seq_len(seq):
 
 def _run_device(problem, config, shifts, restart, flexible, device, concurrent,
                 keep_on_device, engine="persistent"):
+    t0 = time.perf_counter()
     eng = DeviceAdi(problem, config, shifts, restart=restart, flexible=flexible,
                     device=device, concurrent=concurrent, engine=engine)
+    t1 = time.perf_counter()
     sol, rep, state = eng.run()
+    t2 = time.perf_counter()
     if not keep_on_device:
         state.Z, state.Y = sol.Z, sol.Y
         state.w = state.w.cpu().numpy().astype(complex)
         state.t = state.t.cpu().numpy().astype(complex)
+    rep.device_timing.update(construct_ms=1e3 * (t1 - t0), run_ms=1e3 * (t2 - t1),
+                             download_ms=1e3 * (time.perf_counter() - t2))
     return sol, rep, state

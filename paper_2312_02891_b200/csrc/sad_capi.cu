@@ -81,6 +81,7 @@ struct sad_op {
   sad_ctx* ctx = nullptr;
   unsigned long long uid = 0;
   long long n = 0;
+  long long ncols = 0;          // columns (n; n_loc + n_halo for a row slab)
   const int* rowptr = nullptr;
   const int* colidx = nullptr;
   const void* vals = nullptr;
@@ -101,6 +102,11 @@ struct sad_op {
 struct sad_gmres {
   sad_ctx* ctx = nullptr;
   long long n = 0;
+  long long n_ext = 0;          // rows per basis block incl. halo (row-partitioned solves)
+  void* xext = nullptr;         // row-partitioned: solution [local | halo]
+  double* rsum = nullptr;       // row-partitioned: rank sums (pstride doubles)
+  long long* hist_host = nullptr;   // row-partitioned: per-step progress history
+  long long* hist_dev = nullptr;
   int R = 1, dtype = 0, m = 1, flexible = 0;
   size_t esz = 8;
   void* V = nullptr;
@@ -337,6 +343,7 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   op->ctx = ctx;
   op->uid = g_op_uid.fetch_add(1);
   op->n = base->nrows;
+  op->ncols = base->nrows;
   op->precond = precond_kind;
   const double2 sig = adjoint ? make_double2(sre, -sim) : make_double2(sre, sim);
   op->sigma_eff = sig;
@@ -565,24 +572,27 @@ static int set_smem_all(int R, size_t dsm, size_t usm) {
   return 1;
 }
 
-extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int restart, int flexible,
-                                sad_gmres** out) {
+static int gmres_create(sad_ctx* ctx, int64_t n, int64_t n_ext, int r, int dtype, int restart,
+                        int flexible, sad_gmres** out) {
   if (!ctx || !out) return SAD_EINVAL;
   *out = nullptr;
   int rc = check_block(ctx, r, dtype);
   if (rc) return rc;
   if (n < 1) return set_err(ctx, SAD_EINVAL, "n must be >= 1");
+  if (n_ext < n) return set_err(ctx, SAD_EINVAL, "extended rows %lld < local rows %lld",
+                                (long long)n_ext, (long long)n);
   if (restart < 1 || restart > 400) return set_err(ctx, SAD_EINVAL, "restart %d outside 1..400", restart);
   sad_gmres* ws = new sad_gmres();
   ws->ctx = ctx;
   ws->n = n;
+  ws->n_ext = n_ext;
   ws->R = r;
   ws->dtype = dtype;
   ws->m = restart;
   ws->flexible = flexible ? 1 : 0;
   ws->esz = dtype == SAD_F64 ? 8 : 16;
   const int m = restart;
-  const size_t blk = (size_t)n * r * ws->esz;
+  const size_t blk = (size_t)n_ext * r * ws->esz;
   size_t dsm = dot_smem(m + 1, r, ws->esz), usm = upd_smem(m + 1, r, ws->esz);
   if (dsm > 220 * 1024) {
     delete ws;
@@ -678,8 +688,16 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
   return SAD_OK;
 }
 
+extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int restart, int flexible,
+                                sad_gmres** out) {
+  return gmres_create(ctx, n, n, r, dtype, restart, flexible, out);
+}
+
 extern "C" int sad_gmres_destroy(sad_gmres* ws) {
   if (!ws) return SAD_OK;
+  cudaFree(ws->xext);
+  cudaFree(ws->rsum);
+  if (ws->hist_host) cudaFreeHost(ws->hist_host);
   for (int i = 0; i < 3; ++i)
     if (ws->ev[i]) cudaEventDestroy(ws->ev[i]);
   cudaFree(ws->V);
@@ -757,7 +775,7 @@ struct Launcher {
     a.colidx = op->colidx;
     a.vals = op->vals;
     a.sigma = op->sigma_eff;
-    a.stride = ws->n * ws->R;
+    a.stride = ws->n_ext * ws->R;
     a.st = ws->st;
     a.dinv = reinterpret_cast<const XT*>(sizeof(XT) == 8 ? (const void*)op->dinv_r
                                                          : (const void*)op->dinv_c);
@@ -779,7 +797,7 @@ struct Launcher {
     a.Z = ws->Z;
     a.x = x;
     a.dinv = ws->dtype == SAD_F64 ? (const void*)op->dinv_r : (const void*)op->dinv_c;
-    a.stride = ws->n * ws->R;
+    a.stride = ws->n_ext * ws->R;
     a.st = ws->st;
     return a;
   }
@@ -1117,6 +1135,8 @@ extern "C" int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs, void*
                                double tol_col, int maxit, void* stream, int64_t* iters_host,
                                double* resnorm_host, uint8_t* conv_host) {
   if (!ws) return SAD_EINVAL;
+  if (ws->rsum)
+    return set_err(ws->ctx, SAD_EINVAL, "row-partitioned workspace: use sad_dist_gmres_solve");
   sad_ctx* ctx = ws->ctx;
   if (!(tol_col > 0.0)) return set_err(ctx, SAD_EINVAL, "abs_tolerance must be positive");
   if (maxit < 0) return set_err(ctx, SAD_EINVAL, "maxit must be >= 0");
@@ -1205,6 +1225,8 @@ extern "C" int sad_gmres_solve(sad_gmres* ws, sad_op* op, const void* rhs, void*
 extern "C" int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs, void* x, void* res,
                                int steps, void* stream, double* resnorm_host, double* timing_ms) {
   if (!ws) return SAD_EINVAL;
+  if (ws->rsum)
+    return set_err(ws->ctx, SAD_EINVAL, "row-partitioned workspace: use sad_dist_gmres_solve");
   sad_ctx* ctx = ws->ctx;
   if (steps < 1 || steps > ws->m)
     return set_err(ctx, SAD_EINVAL, "steps %d outside 1..restart(%d)", steps, ws->m);
@@ -1417,6 +1439,8 @@ extern "C" int sad_adi_epilogue(sad_ctx* ctx, int64_t nA, int64_t nB, int r, int
 extern "C" int sad_gmres_launch(sad_gmres* ws, sad_op* op, const void* rhs, void* x, double tol_col,
                                 int maxit, void* stream) {
   if (!ws) return SAD_EINVAL;
+  if (ws->rsum)
+    return set_err(ws->ctx, SAD_EINVAL, "row-partitioned workspace: use sad_dist_gmres_solve");
   sad_ctx* ctx = ws->ctx;
   if (!(tol_col > 0.0)) return set_err(ctx, SAD_EINVAL, "abs_tolerance must be positive");
   if (maxit < 0) return set_err(ctx, SAD_EINVAL, "maxit must be >= 0");
@@ -1547,3 +1571,5 @@ extern "C" int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int 
   if (e != cudaSuccess) return set_err(ctx, SAD_ECUDA, "ts_gemv launch failed: %s", cudaGetErrorString(e));
   return SAD_OK;
 }
+
+#include "sad_dist.cuh"

@@ -140,6 +140,11 @@ struct GState {
   unsigned long long* stepseq;  // Givens steps executed
   unsigned long long* cycleseq; // cycles finished
   volatile long long* hflag;    // host-mapped: [0]=stepseq [1]=any_active [2]=cycleseq [3]=any_active
+  // row-partitioned (multi-rank) solves: the last block of a reducing kernel
+  // writes this rank's sums to `rsum` instead of finishing; the sums are
+  // all-reduced over the ranks and k_dist_fin finishes on every rank.
+  double* rsum;                 // [pstride] rank sums (null: single-rank finishers)
+  volatile long long* hist;     // host-mapped [m+1]: (cycleseq << 1 | any_active) per step
   double tol;
   int maxit;
   int m;
@@ -257,6 +262,7 @@ static __device__ void fin_givens(const GState& st, const double* n2) {
     *st.any_active = any;
     *st.j = j + 1;
     unsigned long long s = ++(*st.stepseq);
+    if (st.hist) st.hist[j + 1] = (long long)((*st.cycleseq) << 1) | any;
     st.hflag[1] = any;
     __threadfence_system();
     st.hflag[0] = (long long)s;
@@ -470,7 +476,11 @@ __global__ void __launch_bounds__(kThreads) k_spmm(SpmmArgs<XT> a) {
         if (threadIdx.x == 0) s_tot[cc] = t;
       }
       __syncthreads();
-      fin_cycle(a.st, s_tot);
+      if (a.st.rsum) {
+        if (threadIdx.x < R) a.st.rsum[threadIdx.x] = s_tot[threadIdx.x];
+      } else {
+        fin_cycle(a.st, s_tot);
+      }
       if (threadIdx.x == 0) *a.st.ticket = 0u;
     }
   }
@@ -579,7 +589,27 @@ __global__ void __launch_bounds__(kThreads) k_dot(OrthArgs a) {
     for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq * R + threadIdx.x];
     part[2 * (a.st.m + 1) * R + threadIdx.x] = t;
   }
-  if (last_block(a.st.ticket)) {
+  if (a.st.rsum && last_block(a.st.ticket)) {
+    // this rank's sums, unscaled; k_dist_fin scales the all-reduced values
+    for (int o = threadIdx.x; o < J * R; o += kThreads) {
+      double sx = 0.0, sy = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const double* pb = a.st.part + (size_t)b * a.st.pstride;
+        sx += __ldcg(pb + 2 * o);
+        sy += __ldcg(pb + 2 * o + 1);
+      }
+      a.st.rsum[2 * o] = sx;
+      a.st.rsum[2 * o + 1] = sy;
+    }
+    if (PASS1 && threadIdx.x < R) {
+      double t = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b)
+        t += __ldcg(a.st.part + (size_t)b * a.st.pstride + 2 * (a.st.m + 1) * R + threadIdx.x);
+      a.st.rsum[2 * (a.st.m + 1) * R + threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *a.st.ticket = 0u;
+  } else if (!a.st.rsum && last_block(a.st.ticket)) {
     double2* hout = PASS1 ? a.st.h : a.st.h2;
     for (int o = threadIdx.x; o < J * R; o += kThreads) {
       double sx = 0.0, sy = 0.0;
@@ -700,9 +730,67 @@ __global__ void __launch_bounds__(kThreads) k_update(OrthArgs a) {
         if (threadIdx.x == 0) s_tot[cc] = t;
       }
       __syncthreads();
-      fin_givens(a.st, s_tot);
+      if (a.st.rsum) {
+        if (threadIdx.x < R) a.st.rsum[threadIdx.x] = s_tot[threadIdx.x];
+      } else {
+        fin_givens(a.st, s_tot);
+      }
       if (threadIdx.x == 0) *a.st.ticket = 0u;
     }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Row-partitioned solves.  Every reduction of the Arnoldi
+// step is a rank-local sum (above, into st.rsum), an all-reduce over the ranks
+// (NCCL, or the in-process group sum below), then this finisher, replicated on
+// every rank so the Hessenberg, Givens and masks stay identical everywhere.
+// ----------------------------------------------------------------------------
+enum DistFin { FIN_DOT1 = 0, FIN_DOT2 = 1, FIN_GIVENS = 2, FIN_CYCLE = 3 };
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_dist_fin(GState st) {
+  // inactive steps after the stop: the reducing kernels returned early and rsum
+  // holds stale sums; nothing to finish (the cycle-end residual always runs)
+  if (MODE != FIN_CYCLE && *st.any_active == 0) return;
+  const int R = st.R;
+  if (MODE == FIN_DOT1 || MODE == FIN_DOT2) {
+    const int J = *st.j + 1;
+    double2* hout = MODE == FIN_DOT1 ? st.h : st.h2;
+    for (int o = threadIdx.x; o < J * R; o += kThreads) {
+      const double s = st.S[o];
+      hout[o] = s == 0.0 ? make_double2(0.0, 0.0)
+                         : make_double2(s * st.rsum[2 * o], s * st.rsum[2 * o + 1]);
+    }
+    if (MODE == FIN_DOT1 && threadIdx.x < R) st.wpre2[threadIdx.x] = st.rsum[2 * (st.m + 1) * R + threadIdx.x];
+  } else {
+    __shared__ double s_tot[8];
+    if (threadIdx.x < R) s_tot[threadIdx.x] = st.rsum[threadIdx.x];
+    __syncthreads();
+    if (MODE == FIN_GIVENS) fin_givens(st, s_tot);
+    else fin_cycle(st, s_tot);
+  }
+}
+
+// Sum `count` doubles over the P rank buffers of an in-process rank group (rank
+// order, the same on every rank) and write the result back to every buffer.
+static __global__ void k_group_sum(double* const* bufs, int P, int count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int p = 0; p < P; ++p) t += bufs[p][i];
+    for (int p = 0; p < P; ++p) bufs[p][i] = t;
+  }
+}
+
+// Halo send buffer: rows `rows[0..count)` of an (n x wd doubles) block, packed.
+static __global__ void k_halo_pack(const double* __restrict__ src, int wd, const int* __restrict__ rows,
+                                   long long count, double* __restrict__ dst) {
+  const long long total = count * wd;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / wd;
+    const int k = (int)(e - i * wd);
+    dst[e] = src[(long long)rows[i] * wd + k];
   }
 }
 

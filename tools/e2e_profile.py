@@ -38,3 +38,21 @@ pr.enable()
 once()
 pr.disable()
 pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
+
+# phase breakdown (wall clock, synchronised)
+for _ in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
+    eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    sol, rep, st = eng.run()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    Z = sol.Z
+    t3 = time.perf_counter()
+    Y = sol.Y
+    t4 = time.perf_counter()
+    print(f"phases: construct {1e3*(t1-t0):.1f} ms, run {1e3*(t2-t1):.1f} ms, "
+          f"Z {1e3*(t3-t2):.1f} ms ({Z.nbytes/1e6:.0f} MB), Y {1e3*(t4-t3):.1f} ms")
