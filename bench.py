@@ -19,6 +19,10 @@ with the paper's dynamic inner tolerance (dynamic_mid_bl), outer tolerance
 `--config c4` runs the inner-solve microbenchmark (SpMM/orthogonalisation GB/s).
 Multi-GPU (torchrun): config 2 is single-GPU in BASELINE.json, so N ranks run
 N independent replicas ("replicas only", weak scaling); value = max over ranks.
+Configs 3/5 at N GPUs: A side on ranks [0, N/2), B side on [N/2, N), a side on
+several GPUs row-partitioned (NCCL halo exchange + all-reduce); config 4 at N
+GPUs: the operator row-partitioned over all N (strong scaling).  `--rowpart`
+forces the row-partitioned path at N = 1.
 """
 
 import argparse
@@ -69,14 +73,25 @@ def ncu_traffic(key):
 # -- distributed plumbing --------------------------------------------------------
 
 class Dist:
-    def __init__(self, want_gpus):
+    def __init__(self, want_gpus, force_pg=False):
         self.rank = int(os.environ.get("RANK", 0))
         self.world = int(os.environ.get("WORLD_SIZE", 1))
         self.local = int(os.environ.get("LOCAL_RANK", 0))
         self.pg = None
-        if self.world > 1:
+        if self.world > 1 or force_pg:
             import torch
             import torch.distributed as dist
+            if self.world == 1:
+                # a one-rank process group without torchrun (row-partitioned
+                # path at N = 1)
+                import socket
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    port = sk.getsockname()[1]
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", str(port))
+                os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
             torch.cuda.set_device(self.local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
@@ -181,7 +196,7 @@ def build_c2(name="c2"):
 
 
 def c2_config_json(spec, prob, extra=None):
-    out = {"workload": WORKLOADS[spec.name],
+    out = {"workload": WORKLOADS.get(spec.name, f"reduced {spec.name}"),
            "n": prob.n, "m": prob.m, "r": prob.r, "nnz_A": int(prob.A.nnz),
            "nnz_B": int(prob.B.nnz), "kmax": spec.kmax, "restart": spec.restart,
            "flexible": spec.flexible, "strategy": spec.strategy,
@@ -340,7 +355,7 @@ def run_ours_c2(args, dist, name="c2"):
         torch.cuda.empty_cache()
         eng = None
     # e2e through the public API with host inputs
-    e2e_times, e2e_solve, e2e_down = [], [], []
+    e2e_times, e2e_solve = [], []
     A, B, M, C, f, g, pairs, cyclic = raw
     Zh = Yh = None
     for i in range(args.warmup + args.steps):
@@ -499,24 +514,193 @@ def run_ours_c4(args, dist):
     return line if dist.rank == 0 else None
 
 
+def run_ours_sharded(args, dist, name):
+    """Configs 3/5 on N GPUs (one process per GPU): A side on ranks [0, N/2),
+    B side on [N/2, N) (multigpu.ShardedAdi); a side on several GPUs is
+    row-partitioned with NCCL halo exchange + all-reduce, a side on one GPU
+    runs the persistent engine.  value = wall time to 1e-8 (max over ranks,
+    total work fixed: strong scaling)."""
+    import torch
+    from paper_2312_02891_b200 import _lib
+    from paper_2312_02891_b200.multigpu import make_sharded, side_groups
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    spec, prob, cfg, seq, raw = build_c2(name)
+    run = make_sharded(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
+                       device=dev, force_rowpart=args.rowpart)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for _ in range(args.warmup):
+            run.run()
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        clocks = Clocks(dev)
+        times = []
+        dist.barrier()
+        torch.cuda.synchronize()
+        l0 = lib.sad_kernel_launches()
+        clocks.start()
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            factors, gammas, rep = run.run()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            del factors
+        torch.cuda.synchronize()
+        dist.barrier()
+        ck = clocks.stop()
+    launches = lib.sad_kernel_launches() - l0
+    ms_max = dist.max(statistics.mean(times))
+    a_ranks, b_ranks = side_groups(dist.world)
+    how = lambda rk: (f"row-partitioned over {len(rk)} GPUs (NCCL halo + all-reduce)"
+                      if len(rk) > 1 or args.rowpart else "persistent engine on one GPU")
+    line = {
+        "metric": "wall time to 1e-8 ADI residual", "value": ms_max / 1000.0, "unit": "s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded reference generators)",
+        "config": c2_config_json(spec, prob, {
+            "outer_steps": rep.outer_iterations, "converged": rep.converged,
+            "final_scaled_residual": rep.final_scaled_residual,
+            "sum_inner_A": rep.sum_inner_A, "sum_inner_B": rep.sum_inner_B,
+            "parallelism": f"A side on ranks {a_ranks}: {how(a_ranks)}; B side on ranks "
+                           f"{b_ranks}: {how(b_ranks)}; one all_gather of partial Grams "
+                           f"per outer step"}),
+        "gpu_launches": int(launches), "clocks": ck,
+    }
+    return line if dist.rank == 0 else None
+
+
+def run_ours_c4_rowpart(args, dist):
+    """Config 4 under row partition (N GPUs, or N = 1 with --rowpart): the
+    shifted SpMM with its halo exchange on every rank's slab, and the fixed
+    GMRES steps through the row-partitioned engine (halo + all-reduce per
+    reduction).  value = aggregate SpMM GB/s = global algorithmic bytes / max
+    over ranks of the per-launch time (strong scaling: the matrix is fixed)."""
+    import torch
+    from paper_2312_02891_b200 import _lib
+    from paper_2312_02891_b200 import configs as cfgs
+    from paper_2312_02891_b200.rowpart import RowPartitionedGmres, _ptrs
+    from paper_2312_02891_b200.device import current_stream_handle
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    n0, steps = args.c4_n0, args.c4_steps
+    A, X = cfgs.build_c4(n0=n0, r=8, seed=0)
+    shift = 0.1 * (-abs(A.diagonal()).max() * 2.0)
+    n, r = A.shape[0], 8
+    rp = RowPartitionedGmres("A", A, None, precond_kind="jacobi", restart=steps,
+                             max_iterations=steps, nranks=dist.world, comm="nccl", device=dev)
+    pl = rp.plans[0]
+    ops = rp.operator(shift)
+    xl = torch.from_numpy(np.ascontiguousarray(X[pl.r0:pl.r1])).cuda()
+    xe = torch.zeros((pl.n_loc + pl.n_halo, r), dtype=torch.float64, device="cuda")
+    xe[:pl.n_loc] = xl
+    y = torch.empty_like(xl)
+    blk = n * r * 8
+    spmm_b = A.nnz * 12 + 4 * (n + 1) + 2 * blk        # global algorithmic bytes
+    halo_b = sum(p.n_halo for p in rp.all_plans) * r * 8
+
+    def apply():
+        rc = lib.sad_dist_op_apply(rp.comm.h, 1, _ptrs([ops[0].h]), _ptrs([rp._halos[0].h]), r,
+                                   _lib.SAD_F64, _ptrs([xe.data_ptr()]), _ptrs([y.data_ptr()]),
+                                   current_stream_handle())
+        _lib.check(rc, rp._ctx)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        apply()
+    clocks = Clocks(dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.sad_kernel_launches()
+    clocks.start()
+    ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        apply()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    dist.barrier()
+    launches = lib.sad_kernel_launches() - l0
+    spmm_ms = dist.max(statistics.mean(ms))
+    value = spmm_b / (spmm_ms * 1e-3) / 1e9
+    # the fixed-step inner solve: `steps` Arnoldi steps (maxit = restart = steps)
+    delta = 1e-300
+    rp.solve_device(shift, xl, delta)          # warm
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = rp.solve_device(shift, xl, delta)
+    e1.record()
+    torch.cuda.synchronize()
+    solve_ms = dist.max(e0.elapsed_time(e1))
+    ck = clocks.stop()
+    its = int(out.iterations[0])
+    # CGS2 (multi-kernel engine): (4J + 6) N bytes per Arnoldi step j, J = j + 1
+    N = blk
+    orth_b = sum((4 * (j + 1) + 6) * N for j in range(its))
+    spmm_arn = spmm_b + n * 8                    # + Jacobi gather
+    solve_b = orth_b + its * spmm_arn + 2 * spmm_b
+    peak, peak_kind = hbm_peak()
+    line = {"metric": "inner SpMM GB/s", "value": value, "unit": "GB/s",
+            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": spmm_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 4: {n0}^2 conv-diff, r=8, shifted SpMM + {steps} "
+                                   f"GMRES steps, row-partitioned over {dist.world} GPU(s)",
+                       "n": n, "nnz": int(A.nnz), "parallelism": f"row{dist.world}",
+                       "halo_bytes_per_spmm": halo_b, "l2": "flushed between timed SpMMs"},
+            "roofline": {"bound": "hbm", "achieved": value / dist.world, "peak": peak,
+                         "unit": "GB/s", "frac": value / dist.world / peak, "traffic": None,
+                         "kernel": "k_spmm (+ halo pack/exchange)", "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": spmm_b / dist.world},
+            "inner_solve": {"engine": "row-partitioned multi-kernel CGS2", "steps": its,
+                            "ms": solve_ms, "algorithmic_bytes": solve_b,
+                            "gbs": solve_b / (solve_ms * 1e-3) / 1e9,
+                            "frac_per_gpu": solve_b / (solve_ms * 1e-3) / 1e9 / dist.world / peak,
+                            "iterations_per_s": its * r / (solve_ms * 1e-3)},
+            "gpu_launches": int(launches), "clocks": ck}
+    return line if dist.rank == 0 else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5", "c3s", "c5s"])
     ap.add_argument("--c4-n0", type=int, default=4096)
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rowpart", action="store_true",
+                    help="configs 3-5: row-partitioned path even at N = 1 (NCCL world of 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         dist = Dist(0)
         line = run_reference_arm(args, dist)
     else:
-        dist = Dist(args.gpus)
-        line = (run_ours_c4(args, dist) if args.config == "c4"
-                else run_ours_c2(args, dist, args.config))
+        sharded = args.config in ("c3", "c4", "c5", "c3s", "c5s") and (
+            args.rowpart or int(os.environ.get("WORLD_SIZE", 1)) > 1)
+        dist = Dist(args.gpus, force_pg=sharded)
+        if args.config == "c4":
+            line = run_ours_c4_rowpart(args, dist) if sharded else run_ours_c4(args, dist)
+        elif sharded:
+            line = run_ours_sharded(args, dist, args.config)
+        else:
+            line = run_ours_c2(args, dist, args.config)
     if line is not None:
         print(json.dumps(line), flush=True)
     dist.close()

@@ -188,3 +188,39 @@ def test_rowpart_nccl_world1(c1, rng):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("force", [False, True])
+def test_sharded_adi_world1_c1(force):
+    """multigpu.make_sharded at world size 1 (both sides on rank 0, NCCL
+    communicators of size 1): the one-process-per-GPU driver end to end."""
+    import torch.distributed as dist
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200.multigpu import make_sharded
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{_free_port()}",
+                                rank=0, world_size=1)
+    try:
+        spec = cfgs.CONFIGS["c1"]
+        A, B, M, C, f, g = cfgs.build_problem("c1")
+        pairs, cyclic = spec.load_shift_pairs()
+        prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
+        cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax,
+                           outer_tolerance=spec.outer_tolerance,
+                           precond_kind_A="jacobi", precond_kind_B="jacobi")
+        seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
+        run = make_sharded(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
+                           force_rowpart=force)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            factors, gammas, rep = run.run()
+        gold = read_steps_csv(os.path.join(GOLD, "oracle_c1_gmres.csv"))
+        assert rep.converged and rep.outer_iterations == len(gold)
+        for rec, gd in zip(rep.records, gold):
+            assert abs(rec.inner_it_A - gd["inner_it_A"]) <= 2
+            assert abs(rec.inner_it_B - gd["inner_it_B"]) <= 2
+        assert len(factors["A"]) == len(factors["B"]) == rep.outer_iterations
+    finally:
+        if own:
+            dist.destroy_process_group()

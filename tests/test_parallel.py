@@ -257,3 +257,108 @@ def test_row_partitioned_gmres_matches_oracle(tmp_path):
     assert abs(int(got["it"]) - int(ref.iterations[0])) <= 2
     rel = np.linalg.norm(got["x"] - ref.solution[:, 0]) / np.linalg.norm(ref.solution[:, 0])
     assert rel < 1e-7
+
+
+# -- sharded ADI: row-partitioned side groups (multigpu.ShardedAdi) -----------------------
+
+class _GroupOracleSolver:
+    """Test-side stand-in for the row-partitioned device solver: gathers the
+    group's rhs slabs, solves with the oracle, returns this rank's slabs
+    (counts replicated over the group, as the device solver's are)."""
+
+    def __init__(self, side, mat, group, ranks, bounds):
+        from oracle import sylvadi_oracle as orc
+        self.bind = orc.Binding(side, mat, None, restart=50, orth="dcgs2")
+        self.group, self.ranks, self.bounds = group, ranks, bounds
+        self.me = ranks.index(dist.get_rank())
+
+    def solve_device(self, shift, rhs, delta):
+        from types import SimpleNamespace
+        n = self.bounds[-1]
+        pad = np.zeros((n, rhs.shape[1]), complex)
+        r0, r1 = self.bounds[self.me], self.bounds[self.me + 1]
+        pad[:r1 - r0] = rhs
+        outs = [torch.empty((n, rhs.shape[1]), dtype=torch.complex128)
+                for _ in self.ranks]
+        dist.all_gather(outs, torch.from_numpy(pad), group=self.group)
+        full = np.concatenate([outs[i].numpy()[:self.bounds[i + 1] - self.bounds[i]]
+                               for i in range(len(self.ranks))])
+        res = self.bind.solve(shift, full, delta)
+        return SimpleNamespace(solution=res.solution[r0:r1].copy(),
+                               residual=res.residual[r0:r1].copy(),
+                               iterations=res.iterations, converged=res.converged)
+
+
+class _NumpyBackend:
+    def copy(self, b):
+        return np.array(b, dtype=complex)
+
+    def clone(self, b):
+        return b.copy()
+
+    def gram(self, x):
+        return x.conj().T @ x
+
+    def axpy(self, a, x, y):
+        y += a * x
+
+
+def _sharded_worker(rank, world, port, out_path):
+    _init(rank, world, port)
+    try:
+        from paper_2312_02891_b200 import configs as cfgs
+        from paper_2312_02891_b200.adi import AdiConfig
+        from paper_2312_02891_b200.multigpu import ShardedAdi, side_groups
+        from paper_2312_02891_b200.parallel import Comm, RowPartition
+        from paper_2312_02891_b200.shifts import ShiftSequence
+        spec = cfgs.CONFIGS["c1"]
+        A, B, M, C, f, g = cfgs.build_problem("c1")
+        pairs, cyclic = spec.load_shift_pairs()
+        a_ranks, b_ranks = side_groups(world)
+        ga = dist.new_group(a_ranks) if world > 1 else None
+        gb = dist.new_group(b_ranks) if world > 1 else None
+        solvers, slabs = {}, {}
+        for side, mat, ranks, grp in (("A", A, a_ranks, ga), ("B", B.T.tocsr(), b_ranks, gb)):
+            if rank not in ranks:
+                continue
+            part = RowPartition(mat.indptr, len(ranks))
+            bounds = list(part.bounds)
+            solvers[side] = _GroupOracleSolver(side, A if side == "A" else B, grp, ranks, bounds)
+            i = ranks.index(rank)
+            slabs[side] = (bounds[i], bounds[i + 1])
+        cfg = AdiConfig(strategy=spec.strategy, kmax=spec.kmax)
+        run = ShardedAdi(Comm(), rank, a_ranks, b_ranks, solvers, slabs, _NumpyBackend(),
+                         f, g, cfg, ShiftSequence(pairs=pairs, cyclic=cyclic))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            factors, gammas, rep = run.run()
+        np.savez(f"{out_path}.{rank}.npz", it_a=[r.inner_it_A for r in rep.records],
+                 it_b=[r.inner_it_B for r in rep.records],
+                 res=[r.scaled_res for r in rep.records], steps=rep.outer_iterations)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4])
+def test_sharded_adi_matches_single_process(tmp_path, world):
+    """A on ranks [0, N/2), B on [N/2, N), each side's rows split over its
+    group; one all_gather of partial Grams per step: every rank reproduces the
+    single-process oracle driver's steps and inner counts."""
+    from oracle import sylvadi_oracle as orc
+    from paper_2312_02891_b200 import configs as cfgs
+    out = str(tmp_path / "sh")
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    spec = cfgs.CONFIGS["c1"]
+    A, B, M, C, f, g = cfgs.build_problem("c1")
+    pairs, cyclic = spec.load_shift_pairs()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = orc.run_adi(A, B, f, g, orc.Config(strategy=spec.strategy, kmax=spec.kmax), pairs,
+                          orc.Binding("A", A, None, restart=50, orth="dcgs2"),
+                          orc.Binding("B", B, None, restart=50, orth="dcgs2"), cyclic=cyclic)
+    for rank in range(world):
+        got = np.load(f"{out}.{rank}.npz")
+        assert int(got["steps"]) == ref.outer_iterations
+        assert list(got["it_a"]) == [r.inner_it_A for r in ref.records]
+        assert list(got["it_b"]) == [r.inner_it_B for r in ref.records]
+        np.testing.assert_allclose(got["res"], [r.scaled_res for r in ref.records], rtol=1e-8)
