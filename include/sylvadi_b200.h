@@ -55,6 +55,7 @@ typedef struct sad_op sad_op;
 typedef struct sad_gmres sad_gmres;
 typedef struct sad_comm sad_comm;
 typedef struct sad_halo sad_halo;
+typedef struct sad_bicg sad_bicg;
 
 /* ABI version (bumped on any signature change). */
 int sad_version(void);
@@ -274,6 +275,23 @@ int sad_dist_gmres_solve(sad_comm* comm, int nl, sad_gmres* const* ws, sad_op* c
                          sad_halo* const* halos, const void* const* rhs_dev, void* const* x_dev,
                          void* const* res_dev, double tol_col, int maxit, void* stream,
                          int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
+
+/* ---------------------------------------------------------------------------
+ * The reference's own inner solver on the device: right-preconditioned
+ * BiCGstab per column with the drift-resume loop (krylov.py:82-184), batched
+ * over the r columns of a block (each column an independent run, advancing in
+ * lock step; scalars, breakdown restarts and stopping on the device).
+ * Replaces bicgstab(InnerSolveRequest(op, rhs, tol, maxit, precond))
+ * (krylov.py:160) behind SolverBinding.solve (adi.py:473-488): same stopping
+ * rule (recurrence residual <= tol_col, then the true residual with resume),
+ * iteration counts per column, residual = b - Op x.
+ * ------------------------------------------------------------------------- */
+int sad_bicg_create(sad_ctx* ctx, int64_t n, int r, int dtype, sad_bicg** out);
+int sad_bicg_destroy(sad_bicg* ws);
+int64_t sad_bicg_bytes(const sad_bicg* ws);
+int sad_bicg_solve(sad_bicg* ws, sad_op* op, const void* rhs_dev, void* x_dev, void* res_dev,
+                   double tol_col, int maxit, void* stream, int64_t* iters_host,
+                   double* resnorm_host, uint8_t* conv_host);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,12 @@ SIGNATURES = {
                                          _c.c_int, _c.POINTER(_vp)]),
     "sad_dist_gmres_solve": (_c.c_int, [_vp, _c.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
                                         _c.c_double, _c.c_int, _vp, _vp, _vp, _vp]),
+    # device BiCGstab (the reference's own inner solver)
+    "sad_bicg_create": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.POINTER(_vp)]),
+    "sad_bicg_destroy": (_c.c_int, [_vp]),
+    "sad_bicg_bytes": (_i64, [_vp]),
+    "sad_bicg_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp, _vp,
+                                  _vp, _vp]),
 }
 
 

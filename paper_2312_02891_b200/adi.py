@@ -443,7 +443,7 @@ def run(problem, config, shift_sequence, bindings=None, **kw):
 
 def run_with_state(problem, config, shift_sequence, bindings=None, *, restart=50,
                    flexible=False, device=0, concurrent="auto", keep_on_device=False,
-                   engine="persistent"):
+                   engine="persistent", solver="gmres"):
     """adi.py:553-607.  ``bindings=None`` runs the device-resident driver with
     GpuGmresBinding(restart, flexible) on both sides; otherwise the host loop
     drives the given bindings."""
@@ -455,7 +455,7 @@ def run_with_state(problem, config, shift_sequence, bindings=None, *, restart=50
         return _run_host(problem, config, shift_sequence, bindings)
     return _run_device(problem, config, shift_sequence, restart=restart, flexible=flexible,
                        device=device, concurrent=concurrent, keep_on_device=keep_on_device,
-                       engine=engine)
+                       engine=engine, solver=solver)
 
 
 def _adopt_config(cfg):
@@ -547,7 +547,7 @@ class DeviceAdi:
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
                  device=0, concurrent="auto", engine="persistent", phase_a="auto",
-                 row_ranks=1):
+                 row_ranks=1, solver="gmres"):
         import torch
         if not isinstance(problem, SylvesterProblem):
             problem = SylvesterProblem.from_reference(problem)
@@ -560,6 +560,7 @@ class DeviceAdi:
         self.problem, self.config, self.shifts = problem, config, shift_sequence
         self.device = device
         self.engine = engine
+        self.solver = solver
         if concurrent == "auto":
             # Small blocks are latency-bound: the two solves overlap on disjoint
             # SM sets.  Large blocks are HBM-bound: one solve at a time on every
@@ -594,11 +595,11 @@ class DeviceAdi:
         self.bA = GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
-                                  max_sms=sm_a, phase_a=phase_a)
+                                  max_sms=sm_a, phase_a=phase_a, solver=solver)
         self.bB = GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
-                                  max_sms=sm_b, phase_a=phase_a)
+                                  max_sms=sm_b, phase_a=phase_a, solver=solver)
         self._pool = ThreadPoolExecutor(max_workers=2) if concurrent else None
         self._init_tail(problem)
 
@@ -687,7 +688,7 @@ class DeviceAdi:
         cur = torch.cuda.current_stream(self.dev)
         self.sA.wait_stream(cur)
         self.sB.wait_stream(cur)
-        if self.engine == "persistent" and w.shape[1] <= 8:
+        if self.engine == "persistent" and self.solver == "gmres" and w.shape[1] <= 8:
             # both persistent solves in flight from this thread, one wait each
             resA = torch.empty_like(w)
             resB = torch.empty_like(t)
@@ -728,10 +729,10 @@ def _seq_len(seq):
 
 
 def _run_device(problem, config, shifts, restart, flexible, device, concurrent,
-                keep_on_device, engine="persistent"):
+                keep_on_device, engine="persistent", solver="gmres"):
     t0 = time.perf_counter()
     eng = DeviceAdi(problem, config, shifts, restart=restart, flexible=flexible,
-                    device=device, concurrent=concurrent, engine=engine)
+                    device=device, concurrent=concurrent, engine=engine, solver=solver)
     t1 = time.perf_counter()
     sol, rep, state = eng.run()
     t2 = time.perf_counter()

@@ -1573,3 +1573,4 @@ extern "C" int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int 
 }
 
 #include "sad_dist.cuh"
+#include "sad_bicg_host.cuh"

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .device import (DeviceMatrix, DeviceOperator, GmresWorkspace, gram,
+from .device import (BicgWorkspace, DeviceMatrix, DeviceOperator, GmresWorkspace, gram,
                      sigma_max_from_gram)
 
 MAX_BLOCK = 8   # columns per device solve; wider blocks are split (columns are independent)
@@ -130,7 +130,7 @@ class GpuGmresBinding:
 
     def __init__(self, side, base, mass, mode="iterative", precond_kind="jacobi",
                  droptol=0.1, max_iterations=1000, *, restart=50, flexible=False,
-                 device=0, engine="persistent", max_sms=0, phase_a="auto"):
+                 device=0, engine="persistent", max_sms=0, phase_a="auto", solver="gmres"):
         if side not in ("A", "B"):
             raise ValueError("side must be 'A' or 'B'")
         if mode != "iterative":
@@ -140,6 +140,9 @@ class GpuGmresBinding:
         if precond_kind not in ("none", "jacobi"):
             raise ValueError(f"preconditioner {precond_kind!r} is not available on the GPU "
                              "path (supported: none, jacobi)")
+        if solver not in ("gmres", "bicgstab"):
+            raise ValueError("solver must be 'gmres' or 'bicgstab'")
+        self.solver = solver
         self.side = side
         self.mode = mode
         self.precond_kind = precond_kind
@@ -183,15 +186,19 @@ class GpuGmresBinding:
         key = (r, dtype)
         ws = self._workspaces.get(key)
         if ws is None:
-            ws = _POOL.take((self.device, self.n, r, dtype, self.restart, self.flexible,
-                             self.engine, self.max_sms))
+            if self.solver == "bicgstab":
+                ws = BicgWorkspace(self.n, r, dtype, self.device)
+            else:
+                ws = _POOL.take((self.device, self.n, r, dtype, self.restart, self.flexible,
+                                 self.engine, self.max_sms))
             self._workspaces[key] = ws
         ws.set_option(_lib.SAD_OPT_DIRECT_A, PHASE_A[self.phase_a])
         return ws
 
     def __del__(self):
         for ws in getattr(self, "_workspaces", {}).values():
-            _POOL.give(ws)
+            if isinstance(ws, GmresWorkspace):
+                _POOL.give(ws)
         self._workspaces = {}
 
     # -- solves -------------------------------------------------------------
@@ -228,6 +235,8 @@ class GpuGmresBinding:
                 x_ = torch.empty_like(b_)
                 res_ = torch.empty_like(b_)
             ws = self.workspace(width, dtype)
+            if fixed_steps is not None and self.solver != "gmres":
+                raise ValueError("fixed_steps applies to GMRES only")
             if fixed_steps is None:
                 it, nr, cv = ws.solve(op, b_, x_, res_, tol_col, self.max_iterations, stream)
             else:
@@ -249,6 +258,8 @@ class GpuGmresBinding:
         n, r = rhs.shape
         if n != self.n or r > MAX_BLOCK:
             raise ValueError("begin_device needs an (n, r<=8) block")
+        if self.solver != "gmres" or self.engine != "persistent":
+            raise ValueError("begin_device/end_device need the persistent GMRES engine")
         op = self.operator(shift)
         if rhs.dtype == torch.float64 and not op.is_real:
             raise ValueError("complex shift requires a complex128 block")
@@ -289,7 +300,7 @@ class SolverBindings:
 
 
 def make_gpu_bindings(problem, config, restart=50, flexible=False, device=0,
-                      engine="persistent"):
+                      engine="persistent", solver="gmres"):
     """GPU counterpart of make_bindings (adi.py:497-505)."""
     kind_a = getattr(config, "precond_kind_A", "jacobi")
     kind_b = getattr(config, "precond_kind_B", "jacobi")
@@ -297,7 +308,7 @@ def make_gpu_bindings(problem, config, restart=50, flexible=False, device=0,
     return SolverBindings(
         A=GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
                           max_iterations=maxit, restart=restart, flexible=flexible,
-                          device=device, engine=engine),
+                          device=device, engine=engine, solver=solver),
         B=GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
                           max_iterations=maxit, restart=restart, flexible=flexible,
-                          device=device, engine=engine))
+                          device=device, engine=engine, solver=solver))
