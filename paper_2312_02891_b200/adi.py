@@ -114,7 +114,7 @@ class SylvesterProblem:
         if self.f.shape[1] != self.g.shape[1]:
             raise ValueError("f and g must have the same number of columns")
         for name, blk in (("f", self.f), ("g", self.g)):
-            if blk.shape[1] > 0 and np.linalg.norm(blk) > 0:
+            if blk.shape[1] > 0 and np.any(blk != 0):
                 if np.linalg.matrix_rank(blk) < blk.shape[1]:
                     raise ValueError(f"{name} is column rank deficient")
 
@@ -607,8 +607,9 @@ class DeviceAdi:
         import torch
         self.Md = self.bA.mass      # M (for M z)
         self.Cd = self.bB.mass      # C with transpose (for C^T y)
-        self.f = torch.from_numpy(np.ascontiguousarray(problem.f)).to(self.dev, self.tdtype)
-        self.g = torch.from_numpy(np.ascontiguousarray(problem.g)).to(self.dev, self.tdtype)
+        # upload in the host dtype, widen on the device
+        self.f = torch.from_numpy(np.ascontiguousarray(problem.f)).to(self.dev).to(self.tdtype)
+        self.g = torch.from_numpy(np.ascontiguousarray(problem.g)).to(self.dev).to(self.tdtype)
         self.sA = torch.cuda.Stream(device=self.dev)
         self.sB = torch.cuda.Stream(device=self.dev)
         self.h2d_bytes = (problem.f.nbytes + problem.g.nbytes)
