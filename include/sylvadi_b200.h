@@ -46,7 +46,8 @@ enum sad_engine { SAD_ENGINE_MULTI = 0, SAD_ENGINE_PERSISTENT = 1 };
 /* sad_gmres_set_option keys */
 enum sad_option { SAD_OPT_ENGINE = 0, SAD_OPT_MAX_SMS = 1, SAD_OPT_MIN_ELEMS_PER_THREAD = 2,
                   SAD_OPT_DIRECT_A = 3 /* persistent phase A: -1 auto, 0 TMA ring, 1 direct */,
-                  SAD_OPT_RESIDENT_CSR = 4 /* 1 (default): small CSR slabs stay in shared memory */ };
+                  SAD_OPT_RESIDENT_CSR = 4, /* 1 (default): small CSR slabs stay in shared memory */
+                  SAD_OPT_DIST_ORTH = 5 /* row-partitioned: 1 (default) delayed-Gram CGS2, 0 CGS2 */ };
 enum sad_precond { SAD_PRECOND_NONE = 0, SAD_PRECOND_JACOBI = 1 };
 
 typedef struct sad_ctx sad_ctx;

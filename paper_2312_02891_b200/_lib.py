@@ -17,6 +17,7 @@ SAD_PRECOND_NONE, SAD_PRECOND_JACOBI = 0, 1
 SAD_ENGINE_MULTI, SAD_ENGINE_PERSISTENT = 0, 1
 SAD_OPT_ENGINE, SAD_OPT_MAX_SMS, SAD_OPT_MIN_ELEMS_PER_THREAD, SAD_OPT_DIRECT_A = 0, 1, 2, 3
 SAD_OPT_RESIDENT_CSR = 4
+SAD_OPT_DIST_ORTH = 5
 
 #: every symbol declared in include/sylvadi_b200.h with (restype, argtypes)
 _c = ctypes

@@ -107,6 +107,8 @@ struct sad_gmres {
   double* rsum = nullptr;       // row-partitioned: rank sums (pstride doubles)
   long long* hist_host = nullptr;   // row-partitioned: per-step progress history
   long long* hist_dev = nullptr;
+  int dist_dcgs2 = 0;           // row-partitioned: 1 = DCGS2 (default), 0 = CGS2
+  size_t dual_smem = 0;         // row-partitioned DCGS2: dual-dot shared memory
   int R = 1, dtype = 0, m = 1, flexible = 0;
   size_t esz = 8;
   void* V = nullptr;
@@ -1122,6 +1124,12 @@ extern "C" int sad_gmres_set_option(sad_gmres* ws, int key, int value) {
       return SAD_OK;
     case SAD_OPT_RESIDENT_CSR:
       ws->resident_csr = value != 0;
+      return SAD_OK;
+    case SAD_OPT_DIST_ORTH:
+      if (!ws->rsum) return set_err(ws->ctx, SAD_EINVAL, "orthogonalisation option applies to row-partitioned workspaces");
+      if (value == 1 && ws->dual_smem > 220 * 1024)
+        return set_err(ws->ctx, SAD_EINVAL, "restart too long for the DCGS2 dual dot at this r");
+      ws->dist_dcgs2 = value ? 1 : 0;
       return SAD_OK;
     case SAD_OPT_DIRECT_A:
       if (value < -1 || value > 1) return set_err(ws->ctx, SAD_EINVAL, "direct-A option must be -1, 0 or 1");

@@ -76,6 +76,302 @@ NcclApi& nccl_api() {
 
 }  // namespace
 
+// ---- delayed-Gram CGS2 (DCGS2) for row-partitioned solves ------------------------
+// The persistent kernel's Arnoldi step split at its two grid barriers, with an
+// all-reduce at each: one sweep over the basis for h_raw = V^H w, g_raw =
+// V^H v_j and ||w||^2 (k_dot_dual), the finisher A math (k_dist_finA: Gram
+// column, h1 = S h_raw, c = 2 h1 - G h1, previous rotations), the update
+// w -= V S c with ||w||^2 (k_update<UPD_ORTH2>), the new rotation (k_dist_finC).
+// The basis is streamed twice per step and there are two all-reduces per step
+// (classical CGS2: four sweeps, three all-reduces).
+namespace sad {
+
+// rank-sum layout: h_raw [2 J R] at 0, g_raw at 2(m+1)R, ||w||^2 [R] at 4(m+1)R
+template <typename XT, int R>
+__global__ void __launch_bounds__(kThreads) k_dot_dual(OrthArgs a) {
+  constexpr int GPW = 32 / R;
+  constexpr int U = 8;
+  extern __shared__ double smem_d[];
+  if (*a.st.any_active == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / R, c = lane - grp * R;
+  const bool lane_ok = grp < GPW;
+  const int j = *a.st.j;
+  const int J = j + 1;
+  const int m = a.st.m;
+  const XT* V = reinterpret_cast<const XT*>(a.V);
+  const XT* w = V + (long long)J * a.stride;
+  const XT* vj = V + (long long)j * a.stride;
+  XT* s_h = reinterpret_cast<XT*>(smem_d);                       // [J][kWarps][R]
+  XT* s_g = s_h + (size_t)J * kWarps * R;                        // [J][kWarps][R]
+  double* s_w2 = reinterpret_cast<double*>(s_g + (size_t)J * kWarps * R);   // [kWarps][R]
+  for (int o = threadIdx.x; o < J * kWarps * R; o += kThreads) {
+    s_h[o] = zero<XT>();
+    s_g[o] = zero<XT>();
+  }
+  for (int o = threadIdx.x; o < kWarps * R; o += kThreads) s_w2[o] = 0.0;
+  __syncthreads();
+  const long long tile_rows = (long long)GPW * U;
+  const long long ntiles = (a.n + tile_rows - 1) / tile_rows;
+  double w2 = 0.0;
+  for (long long t = (long long)blockIdx.x * kWarps + warp; t < ntiles;
+       t += (long long)gridDim.x * kWarps) {
+    XT wv[U], jv[U];
+    long long idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long row = t * tile_rows + u * GPW + grp;
+      const bool ok = lane_ok && row < a.n;
+      idx[u] = ok ? row * R + c : -1;
+      wv[u] = ok ? w[idx[u]] : zero<XT>();
+      jv[u] = ok ? vj[idx[u]] : zero<XT>();
+      w2 += abs2(wv[u]);
+    }
+    // two basis blocks per pass: 2U independent loads in flight per lane
+    int i = 0;
+    for (; i + 1 < J; i += 2) {
+      const XT* v0 = V + (long long)i * a.stride;
+      const XT* v1 = v0 + a.stride;
+      XT a0[U], a1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a0[u] = idx[u] >= 0 ? v0[idx[u]] : zero<XT>();
+        a1[u] = idx[u] >= 0 ? v1[idx[u]] : zero<XT>();
+      }
+      XT ph0 = zero<XT>(), pg0 = zero<XT>(), ph1 = zero<XT>(), pg1 = zero<XT>();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ph0 = cfma(a0[u], wv[u], ph0);
+        pg0 = cfma(a0[u], jv[u], pg0);
+        ph1 = cfma(a1[u], wv[u], ph1);
+        pg1 = cfma(a1[u], jv[u], pg1);
+      }
+      ph0 = group_reduce<R>(ph0, grp);
+      pg0 = group_reduce<R>(pg0, grp);
+      ph1 = group_reduce<R>(ph1, grp);
+      pg1 = group_reduce<R>(pg1, grp);
+      if (grp == 0 && lane_ok) {
+        XT* sh = s_h + ((size_t)i * kWarps + warp) * R + c;
+        XT* sg = s_g + ((size_t)i * kWarps + warp) * R + c;
+        sh[0] = add(sh[0], ph0);
+        sg[0] = add(sg[0], pg0);
+        sh[kWarps * R] = add(sh[kWarps * R], ph1);
+        sg[kWarps * R] = add(sg[kWarps * R], pg1);
+      }
+    }
+    if (i < J) {
+      const XT* vi = V + (long long)i * a.stride;
+      XT ph = zero<XT>(), pg = zero<XT>();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (idx[u] >= 0) {
+          const XT v = vi[idx[u]];
+          ph = cfma(v, wv[u], ph);
+          pg = cfma(v, jv[u], pg);
+        }
+      }
+      ph = group_reduce<R>(ph, grp);
+      pg = group_reduce<R>(pg, grp);
+      if (grp == 0 && lane_ok) {
+        XT* sh = s_h + ((size_t)i * kWarps + warp) * R + c;
+        XT* sg = s_g + ((size_t)i * kWarps + warp) * R + c;
+        *sh = add(*sh, ph);
+        *sg = add(*sg, pg);
+      }
+    }
+  }
+  w2 = group_reduce<R>(w2, grp);
+  if (grp == 0 && lane_ok) s_w2[warp * R + c] = w2;
+  __syncthreads();
+  double* part = a.st.part + (size_t)blockIdx.x * a.st.pstride;
+  const int og = 2 * (m + 1) * R, ow = 4 * (m + 1) * R;
+  for (int o = threadIdx.x; o < J * R; o += kThreads) {
+    const int ii = o / R, cc = o - ii * R;
+    XT th = zero<XT>(), tg = zero<XT>();
+    for (int wq = 0; wq < kWarps; ++wq) {
+      th = add(th, s_h[((size_t)ii * kWarps + wq) * R + cc]);
+      tg = add(tg, s_g[((size_t)ii * kWarps + wq) * R + cc]);
+    }
+    const double2 h2c = to_c(th), g2c = to_c(tg);
+    part[2 * o] = h2c.x;
+    part[2 * o + 1] = h2c.y;
+    part[og + 2 * o] = g2c.x;
+    part[og + 2 * o + 1] = g2c.y;
+  }
+  if (threadIdx.x < R) {
+    double t = 0.0;
+    for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq * R + threadIdx.x];
+    part[ow + threadIdx.x] = t;
+  }
+  if (last_block(a.st.ticket)) {
+    for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) {
+      double sh = 0.0, sg = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const double* pb = a.st.part + (size_t)b * a.st.pstride;
+        sh += __ldcg(pb + o);
+        sg += __ldcg(pb + og + o);
+      }
+      a.st.rsum[o] = sh;
+      a.st.rsum[og + o] = sg;
+    }
+    if (threadIdx.x < R) {
+      double t = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b)
+        t += __ldcg(a.st.part + (size_t)b * a.st.pstride + ow + threadIdx.x);
+      a.st.rsum[ow + threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *a.st.ticket = 0u;
+  }
+}
+
+// finisher A on the all-reduced sums (the persistent kernel's finisher A math):
+// Gram column, h1, c = 2 h1 - G h1 (into st.h2 for k_update<UPD_ORTH2>, which
+// scales by S), ||w_pre||^2, the previous rotations applied to the new column
+static __global__ void __launch_bounds__(kThreads) k_dist_finA(GState gs, PState ps) {
+  if (*gs.any_active == 0) return;
+  const int R = gs.R, m = gs.m;
+  const int j = *gs.j, J = j + 1;
+  const double* rs = gs.rsum;
+  double2* h1 = ps.red;
+  double2* gc = ps.red + (size_t)(m + 1) * R;
+  double2* cv = ps.coef;
+  const int og = 2 * (m + 1) * R, ow = 4 * (m + 1) * R;
+  for (int o = threadIdx.x; o < J * R; o += kThreads) {
+    const int cc = o - (o / R) * R;
+    const double si = gs.S[o], sjj = gs.S[j * R + cc];
+    const double2 graw = make_double2(rs[og + 2 * o], rs[og + 2 * o + 1]);
+    gc[o] = (si == 0.0 || sjj == 0.0) ? make_double2(0.0, 0.0)
+                                      : make_double2(si * sjj * graw.x, si * sjj * graw.y);
+    h1[o] = si == 0.0 ? make_double2(0.0, 0.0) : make_double2(si * rs[2 * o], si * rs[2 * o + 1]);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < J * R; o += kThreads) {
+    const int ii = o / R, cc = o - ii * R;
+    double2 gh0 = make_double2(0.0, 0.0), gh1 = gh0, gh2 = gh0, gh3 = gh0;
+    if (ii < j) {
+      const double2* Grow = ps.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1);
+      int l = 0;
+      for (; l + 3 < j; l += 4) {
+        gh0 = add(gh0, mul(Grow[l], h1[l * R + cc]));
+        gh1 = add(gh1, mul(Grow[l + 1], h1[(l + 1) * R + cc]));
+        gh2 = add(gh2, mul(Grow[l + 2], h1[(l + 2) * R + cc]));
+        gh3 = add(gh3, mul(Grow[l + 3], h1[(l + 3) * R + cc]));
+      }
+      for (; l < j; ++l) gh0 = add(gh0, mul(Grow[l], h1[l * R + cc]));
+    } else {
+      for (int l = 0; l < j; ++l) gh0 = add(gh0, mul(cconj(gc[l * R + cc]), h1[l * R + cc]));
+    }
+    double2 gh = add(add(gh0, gh1), add(gh2, gh3));
+    gh = add(gh, mul(gc[ii * R + cc], h1[j * R + cc]));
+    const double2 h = h1[o];
+    double2 c2 = make_double2(2.0 * h.x - gh.x, 2.0 * h.y - gh.y);
+    if (!gs.active[cc]) c2 = make_double2(0.0, 0.0);
+    cv[o] = c2;
+    gs.h2[o] = c2;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < J * R; o += kThreads) {
+    const int ii = o / R, cc = o - ii * R;
+    double2* Gc = ps.G + (size_t)cc * (m + 1) * (m + 1);
+    Gc[(size_t)ii * (m + 1) + j] = gc[o];
+    Gc[(size_t)j * (m + 1) + ii] = cconj(gc[o]);
+  }
+  if (threadIdx.x < R) {
+    const int cc = threadIdx.x;
+    gs.wpre2[cc] = rs[ow + cc];
+    if (gs.active[cc]) {
+      double2 x0 = cv[cc];
+      for (int ii = 0; ii < j; ++ii) {
+        const double2 x1 = cv[(ii + 1) * R + cc];
+        const double ci = gs.cs[(size_t)cc * m + ii];
+        const double2 si = gs.sn[(size_t)cc * m + ii];
+        gs.H[((size_t)cc * m + j) * (m + 1) + ii] = add(scal(ci, x0), mul(si, x1));
+        x0 = sub(scal(ci, x1), mul(cconj(si), x0));
+      }
+      ps.hc[j * R + cc] = x0;
+    }
+  }
+}
+
+// finisher C: the new rotation from ||w||, the residual estimate, the stopping
+// test (the persistent kernel's finisher C), the host-visible progress record
+static __global__ void k_dist_finC(GState gs, PState ps) {
+  if (*gs.any_active == 0) return;
+  const int R = gs.R, m = gs.m;
+  const int j = *gs.j;
+  __shared__ int s_actn[8];
+  if (threadIdx.x < R) {
+    const int cc = threadIdx.x;
+    s_actn[cc] = 0;
+    if (gs.active[cc]) {
+      const double hn = sqrt(gs.rsum[cc]);
+      double cj; double2 sjv, rj;
+      givens(ps.hc[j * R + cc], make_double2(hn, 0.0), cj, sjv, rj);
+      gs.cs[(size_t)cc * m + j] = cj;
+      gs.sn[(size_t)cc * m + j] = sjv;
+      double2* col = gs.H + ((size_t)cc * m + j) * (m + 1);
+      col[j] = rj;
+      col[j + 1] = make_double2(0.0, 0.0);
+      double2* gv = gs.g + (size_t)cc * (m + 1);
+      const double2 gj = gv[j];
+      const double2 gn = mul(cconj(sjv), gj);
+      const double2 gnext = make_double2(-gn.x, -gn.y);
+      gv[j + 1] = gnext;
+      gv[j] = scal(cj, gj);
+      const long long it = gs.iters[cc] + 1;
+      gs.iters[cc] = it;
+      gs.kdim[cc] = j + 1;
+      gs.S[(j + 1) * R + cc] = hn > 0.0 ? 1.0 / hn : 0.0;
+      bool end = (j + 1 == m) || it >= gs.maxit;
+      if (!gs.fixed) end = end || cabs_(gnext) <= gs.tol || hn <= kLucky * sqrt(gs.wpre2[cc]);
+      if (end) gs.active[cc] = 0;
+      s_actn[cc] = end ? 0 : 1;
+    } else {
+      gs.S[(j + 1) * R + cc] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int cc = 0; cc < R; ++cc) any |= s_actn[cc];
+    *gs.any_active = any;
+    *gs.j = j + 1;
+    unsigned long long sq = ++(*gs.stepseq);
+    if (gs.hist) gs.hist[j + 1] = (long long)((*gs.cycleseq) << 1) | any;
+    gs.hflag[1] = any;
+    __threadfence_system();
+    gs.hflag[0] = (long long)sq;
+  }
+}
+
+template <typename XT, int R>
+static void dot_dual_launch(const OrthArgs& a, int grid, size_t smem, cudaStream_t s) {
+  static size_t attr = 48 * 1024;   // dynamic shared memory opted in so far
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_dot_dual<XT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) == cudaSuccess)
+      attr = smem;
+  }
+  k_dot_dual<XT, R><<<grid, kThreads, smem, s>>>(a);
+}
+
+template <typename XT>
+static void dot_dual(int R, const OrthArgs& a, int grid, size_t smem, cudaStream_t s) {
+  switch (R) {
+    case 1: dot_dual_launch<XT, 1>(a, grid, smem, s); break;
+    case 2: dot_dual_launch<XT, 2>(a, grid, smem, s); break;
+    case 3: dot_dual_launch<XT, 3>(a, grid, smem, s); break;
+    case 4: dot_dual_launch<XT, 4>(a, grid, smem, s); break;
+    case 5: dot_dual_launch<XT, 5>(a, grid, smem, s); break;
+    case 6: dot_dual_launch<XT, 6>(a, grid, smem, s); break;
+    case 7: dot_dual_launch<XT, 7>(a, grid, smem, s); break;
+    case 8: dot_dual_launch<XT, 8>(a, grid, smem, s); break;
+  }
+}
+
+}  // namespace sad
+
 #define NCK(ctx, call)                                                                  \
   do {                                                                                  \
     ncclResult_t r_ = (call);                                                           \
@@ -452,6 +748,9 @@ extern "C" int sad_dist_gmres_create(sad_ctx* ctx, int64_t n_loc, int64_t n_ext,
   if (rc) return rc;
   sad_gmres* ws = *out;
   ws->engine = SAD_ENGINE_MULTI;
+  ws->dist_dcgs2 = 1;
+  ws->dual_smem = 2 * (size_t)(restart + 1) * kWarps * r * ws->esz + kWarps * r * 8;
+  if (ws->dual_smem > 220 * 1024) ws->dist_dcgs2 = 0;   // CGS2 (single-dot smem) instead
   const size_t xb = (size_t)n_ext * r * ws->esz;
   if (cudaMalloc(&ws->xext, xb) != cudaSuccess ||
       cudaMalloc(&ws->rsum, (size_t)ws->pstride * sizeof(double)) != cudaSuccess ||
@@ -517,6 +816,15 @@ extern "C" int sad_dist_gmres_solve(sad_comm* cm, int nl, sad_gmres* const* W, s
     if (rc) return rc;
   }
   const int cnt_dot = 2 * (m + 1) * R + R;
+  const int cnt_dual = 4 * (m + 1) * R + R;
+  const bool dcgs2 = W[0]->dist_dcgs2 != 0;
+  for (int i = 0; i < nl; ++i)
+    if ((W[i]->dist_dcgs2 != 0) != dcgs2)
+      return set_err(ctx, SAD_EINVAL, "ranks disagree on the orthogonalisation");
+  if (dcgs2) {
+    // the persistent pieces of the workspace must see this solve's state
+    for (int i = 0; i < nl; ++i) W[i]->pst.g = W[i]->st;
+  }
   auto AR = [&](int count) { return allreduce(cm, rs.data(), nl, count, s, true); };
   auto blocks_of = [&](int j, std::vector<char*>& b) {
     b.resize(nl);
@@ -567,6 +875,24 @@ extern "C" int sad_dist_gmres_solve(sad_comm* cm, int nl, sad_gmres* const* W, s
       rc = halo_exchange(cm, H, vb.data(), nl, wd, s);
       if (rc) return rc;
       for (int i = 0; i < nl; ++i) L[i].arnoldi(0);       // SpMM
+      if (dcgs2) {
+        // DCGS2: one dual dot sweep, finisher A, one update sweep, finisher C
+        for (int i = 0; i < nl; ++i) {
+          const OrthArgs oa = L[i].orth_args();
+          if (W[i]->dtype == SAD_F64) dot_dual<double>(R, oa, L[i].grid_dot, W[i]->dual_smem, s);
+          else dot_dual<double2>(R, oa, L[i].grid_dot, W[i]->dual_smem, s);
+        }
+        COUNT_LAUNCH(nl);
+        if ((rc = AR(cnt_dual))) return rc;
+        for (int i = 0; i < nl; ++i) k_dist_finA<<<1, kThreads, 0, s>>>(W[i]->st, W[i]->pst);
+        COUNT_LAUNCH(nl);
+        for (int i = 0; i < nl; ++i) L[i].arnoldi(4);     // w -= V S c, ||w||^2
+        if ((rc = AR(R))) return rc;
+        for (int i = 0; i < nl; ++i) k_dist_finC<<<1, 32, 0, s>>>(W[i]->st, W[i]->pst);
+        COUNT_LAUNCH(nl);
+        CKL(ctx);
+        continue;
+      }
       for (int i = 0; i < nl; ++i) L[i].arnoldi(1);       // pass-1 dots
       if ((rc = AR(cnt_dot))) return rc;
       dist_fin<FIN_DOT1>(W, nl, s);

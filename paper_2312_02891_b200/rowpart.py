@@ -5,7 +5,9 @@ One shifted operator is split into contiguous row slabs balanced by nonzeros
 blocks that belong to it, and a halo plan (the remote rows its SpMM gathers).
 The solve is ``sad_dist_gmres_solve``: the multi-kernel engine's step sequence
 on every rank, halo exchange before each SpMM, every block dot all-reduced
-before its (replicated) finisher.  Same contract as the single-GPU engine
+before its (replicated) finisher -- delayed-Gram CGS2 by default (two basis
+sweeps, two all-reduces per step; ``orth="cgs2"``: four and three).  Same
+contract as the single-GPU engine
 (SURVEY 8a items 1-6); reductions are summed per rank then over ranks, so the
 results agree with one GPU to rounding, not bit for bit.
 
@@ -165,7 +167,7 @@ class RowPartitionedGmres:
 
     def __init__(self, side, base, mass=None, mode="iterative", precond_kind="jacobi",
                  droptol=0.1, max_iterations=1000, *, nranks=2, restart=50, flexible=False,
-                 device=0, comm="local", group=None):
+                 device=0, comm="local", group=None, orth="dcgs2"):
         if side not in ("A", "B"):
             raise ValueError("side must be 'A' or 'B'")
         if mode != "iterative":
@@ -175,6 +177,9 @@ class RowPartitionedGmres:
         if mass is not None:
             raise NotImplementedError("a non-identity mass matrix is not row-partitioned "
                                       "(generalised pencils run A || B, BASELINE config 3)")
+        if orth not in ("dcgs2", "cgs2"):
+            raise ValueError("orth must be 'dcgs2' or 'cgs2'")
+        self.orth = orth
         self.side, self.mode, self.precond_kind = side, mode, precond_kind
         self.droptol = droptol
         self.max_iterations = int(max_iterations)
@@ -257,6 +262,8 @@ class RowPartitionedGmres:
                                                      1 if self.flexible else 0,
                                                      ctypes.byref(h)), self._ctx)
                 ws.append(_Handle(h, "sad_gmres_destroy"))
+                _lib.check(lib.sad_gmres_set_option(h, _lib.SAD_OPT_DIST_ORTH,
+                                                    1 if self.orth == "dcgs2" else 0), self._ctx)
             self._ws[key] = ws
         return ws
 

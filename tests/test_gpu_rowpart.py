@@ -76,9 +76,10 @@ def test_rowpart_dinv_halo(c1, P):
         assert np.allclose(loc, full[pl.r0:pl.r1], rtol=1e-15, atol=0)
 
 
+@pytest.mark.parametrize("orth", ["dcgs2", "cgs2"])
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
 @pytest.mark.parametrize("side,flexible", [("A", False), ("B", False), ("A", True)])
-def test_rowpart_gmres_matches_single_gpu(c1, rng, P, side, flexible):
+def test_rowpart_gmres_matches_single_gpu(c1, rng, P, side, flexible, orth):
     from paper_2312_02891_b200.krylov import GpuGmresBinding
     from paper_2312_02891_b200.rowpart import RowPartitionedGmres
     A, B = c1[0], c1[1]
@@ -87,9 +88,12 @@ def test_rowpart_gmres_matches_single_gpu(c1, rng, P, side, flexible):
     shift = -40.0 + 12.0j
     rhs = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
     delta = 1e-9 * np.linalg.norm(rhs)
-    one = GpuGmresBinding(side, base, None, restart=30, flexible=flexible, engine="multi")
+    # the single-GPU engine with the same orthogonalisation
+    one = GpuGmresBinding(side, base, None, restart=30, flexible=flexible,
+                          engine="persistent" if orth == "dcgs2" else "multi")
     r1 = one.solve(shift, rhs, delta)
-    rp = RowPartitionedGmres(side, base, None, nranks=P, restart=30, flexible=flexible)
+    rp = RowPartitionedGmres(side, base, None, nranks=P, restart=30, flexible=flexible,
+                             orth=orth)
     rP = rp.solve(shift, rhs, delta)
     assert np.all(rP.converged)
     assert np.all(np.abs(rP.iterations - r1.iterations) <= 2), (rP.iterations, r1.iterations)
