@@ -248,9 +248,33 @@ __device__ __forceinline__ bool bi_reduce(const BState& st, const double (&q)[NQ
     st.part[(size_t)blockIdx.x * st.pstride + threadIdx.x] = t;
   }
   if (!last_block(st.ticket)) return false;
-  for (int o = 0; o < NQ * R; ++o) {
-    double t = block_sum_partials(st.part, st.pstride, gridDim.x, o);
-    if (threadIdx.x == 0) tot_s[o] = t;
+  // all outputs together, 8 at a time: each thread sums its strided blocks for
+  // 8 outputs (independent loads in flight), then one shared-memory tree for the
+  // 8 (fixed order: deterministic)
+  __shared__ double s_red[8][kThreads];
+  for (int o0 = 0; o0 < NQ * R; o0 += 8) {
+    const int no = min(8, NQ * R - o0);
+    double acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) {
+      const double* pb = st.part + (size_t)b * st.pstride + o0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < no) acc[k] += __ldcg(pb + k);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_red[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int sh = kThreads / 2; sh > 0; sh >>= 1) {
+      if (threadIdx.x < sh) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s_red[k][threadIdx.x] += s_red[k][threadIdx.x + sh];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < no) tot_s[o0 + threadIdx.x] = s_red[threadIdx.x][0];
+    __syncthreads();
   }
   __syncthreads();
   return true;

@@ -162,7 +162,9 @@ extern "C" int sad_bicg_solve(sad_bicg* w, sad_op* op, const void* rhs, void* x,
   w->st.maxit = maxit;
   a.st = w->st;
   const int gpw = 32 / R;
-  const int grid = grid_for(w->n, kWarps * gpw, w->max_blocks);
+  // grid-stride kernels: a few blocks per SM keep the finisher's partial
+  // reduction short (small blocks are latency-bound)
+  const int grid = grid_for(w->n, kWarps * gpw, std::min(w->max_blocks, ctx->nsm * 4));
   const bool cplx = w->dtype == SAD_C128;
   auto vec = [&](int K) {
     return cplx ? bicg_launch_vec_z(K, a, R, grid, s) : bicg_launch_vec_d(K, a, R, grid, s);

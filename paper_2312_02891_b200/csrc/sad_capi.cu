@@ -1038,10 +1038,18 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   // Direct phase A when every block owns at most two tiles even at one block
   // per SM (latency-bound small slabs); else the TMA ring.
   const int sms = ws->max_sms > 0 ? std::min(ws->max_sms, ctx->nsm) : ctx->nsm;
-  const bool direct = ws->direct_a >= 0 ? ws->direct_a != 0
-                                        : (size_t)ws->n <= 2 * tile_rows * (size_t)sms;
+  // direct phase A stages the block's rows of w and v_j in shared memory: an
+  // upper bound of the rows per block (the launcher's grid is at least
+  // min(n R / (threads * min elems per thread), SMs) blocks)
+  const size_t rows_cap = std::max<size_t>(
+      ((size_t)kThreads * std::max(ws->min_elems_per_thread, 1) + R - 1) / R,
+      ((size_t)ws->n + sms - 1) / sms);
+  const size_t stage_rows_bytes = 2 * rows_cap * R * ws->esz;
+  bool direct = ws->direct_a >= 0 ? ws->direct_a != 0
+                                  : (size_t)ws->n <= 2 * tile_rows * (size_t)sms;
+  if (direct && stage_rows_bytes > 96 * 1024) direct = false;   // rows do not fit: TMA ring
   const size_t stage = direct ? 0 : ((tile_rows * R * ws->esz + 32 + 127) & ~size_t(127));
-  const size_t sums = 2 * m1 * R * ws->esz * (direct ? 1 + kWarps : 1);
+  const size_t sums = 2 * m1 * R * ws->esz + (direct ? stage_rows_bytes : 0);
   // TMA path: the basis ring and the A1 CSR ring share one region
   const size_t vsz = op->vals_complex ? 16 : 8;
   const size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
@@ -1064,6 +1072,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
+    a.direct_rows = (int)rows_cap;
     a.ring_bytes = (int)ring_bytes;
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
@@ -1073,6 +1082,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
+    a.direct_rows = (int)rows_cap;
     a.ring_bytes = (int)ring_bytes;
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;

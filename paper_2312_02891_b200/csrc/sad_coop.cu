@@ -27,6 +27,7 @@ static cudaError_t coop_launch_t(PArgs<XT> a, const CoopCfg& cfg, cudaStream_t s
   if (grid > (long long)cfg.max_blocks) grid = cfg.max_blocks;
   if (grid < 1) grid = 1;
   a.rows_per_block = (a.n + grid - 1) / grid;
+  if (a.direct_a && a.rows_per_block > a.direct_rows) return cudaErrorInvalidConfiguration;
   a.pT = cfg.max_blocks;
   void* args[] = {(void*)&a};
   if (grid_out) *grid_out = (int)grid;

@@ -74,6 +74,7 @@ struct PArgs {
   XT* Z;
   long long stride;      // n*R elements per basis block
   long long rows_per_block;
+  int direct_rows;        // direct phase A: staged rows per block (shared-memory capacity)
   int pT;                // block stride of the output-major partials
   int prof;              // record phase timers
   int g_smem;            // stage the Gram block in shared memory (fits)
@@ -408,15 +409,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         __syncthreads();
         constexpr int T = kWarps * GPW * UA;   // rows per block-tile
         if (a.direct_a) {
-          // Small slabs (one or two tiles per block): every warp sweeps the
-          // basis for its own rows with direct loads (IB blocks in flight) and
-          // keeps its per-basis-block sums in its own shared-memory slots, so
-          // the block synchronises once per phase instead of once per group.
-          XT* s_wp = s_blk + 2 * J * R;   // [2J][kWarps][R]
-          for (int o = threadIdx.x; o < 2 * J * kWarps * R; o += kThreads) s_wp[o] = zero<XT>();
-          __syncthreads();
-          constexpr int UD = UA / 2;                 // rows per lane per direct tile
+          // Small slabs (latency-bound, L2-resident basis): the SpMM writes the
+          // block's rows of w (and keeps them and v_j's rows in shared memory);
+          // then the basis sweep is split over the warps BY BASIS BLOCK: warp
+          // k owns blocks k, k + kWarps, ... and walks all of the block's rows
+          // with 8 loads in flight per lane, reading w / v_j from shared
+          // memory.  One group reduction per basis block and a single writer per
+          // sum (no cross-warp accumulation), so the sweep costs about one L2
+          // round trip per basis block a warp owns instead of one per
+          // (row tile x group of basis blocks).
+          XT* s_wr = s_blk + 2 * J * R;                               // [rows][R]  w
+          XT* s_xr = s_wr + (size_t)a.direct_rows * R;                // [rows][R]  v_j
+          constexpr int UD = UA / 2;                 // rows per lane per SpMM tile
           constexpr int TD = kWarps * GPW * UD;
+          const int nrows_blk = (int)(r1 - r0);
           for (long long base = r0; base < r1; base += TD) {
             const long long nrows = min((long long)TD, r1 - base);
             XT wv[UD], xv[UD];
@@ -440,46 +446,62 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                   a.Z[(long long)j * a.stride + idx[u]] = sscal(sj, zi);
                 }
                 w2 += abs2(wv[u]);
-              }
-            }
-            constexpr int IBD = 4;   // basis blocks in flight
-            for (int i0 = 0; i0 < J; i0 += IBD) {
-              XT vb[IBD][UD];
-#pragma unroll
-              for (int ib = 0; ib < IBD; ++ib) {
-                const XT* Vi = a.V + (long long)min(i0 + ib, J - 1) * a.stride;
-#pragma unroll
-                for (int u = 0; u < UD; ++u)
-                  vb[ib][u] = (idx[u] >= 0 && i0 + ib < J) ? Vi[idx[u]] : zero<XT>();
-              }
-#pragma unroll
-              for (int ib = 0; ib < IBD; ++ib) {
-                if (i0 + ib < J) {
-                  XT ph = zero<XT>(), pg = zero<XT>();
-#pragma unroll
-                  for (int u = 0; u < UD; ++u) {
-                    ph = cfma(vb[ib][u], wv[u], ph);
-                    pg = cfma(vb[ib][u], xv[u], pg);
-                  }
-                  ph = group_reduce<R>(ph, grp);
-                  pg = group_reduce<R>(pg, grp);
-                  if (grp == 0 && lane_ok) {
-                    XT* ph_s = s_wp + ((size_t)(i0 + ib) * kWarps + warp) * R + c;
-                    XT* pg_s = s_wp + ((size_t)(J + i0 + ib) * kWarps + warp) * R + c;
-                    *ph_s = add(*ph_s, ph);
-                    *pg_s = add(*pg_s, pg);
-                  }
-                }
+                const long long lrow = idx[u] - r0 * R;   // (row - r0) * R + c
+                s_wr[lrow] = wv[u];
+                s_xr[lrow] = xv[u];
               }
             }
           }
           __syncthreads();
-          for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) {
-            const int ii = o / R, cc = o - ii * R;
-            XT t = zero<XT>();
+          // two basis blocks per warp pass (i and i + kWarps): 2 x KL loads in flight
+          for (int i = warp; i < J; i += 2 * kWarps) {
+            const int i2 = i + kWarps;
+            const bool two = i2 < J;
+            const XT* Vi = a.V + (long long)i * a.stride + r0 * R;
+            const XT* Vk = a.V + (long long)(two ? i2 : i) * a.stride + r0 * R;
+            XT ph = zero<XT>(), pg = zero<XT>(), ph2 = zero<XT>(), pg2 = zero<XT>();
+            if (lane_ok) {
+              constexpr int KL = 8;
+              int rr = grp;
+              for (; rr + (KL - 1) * GPW < nrows_blk; rr += KL * GPW) {
+                XT vb[KL], vk[KL];
 #pragma unroll
-            for (int wq = 0; wq < kWarps; ++wq) t = add(t, s_wp[((size_t)ii * kWarps + wq) * R + cc]);
-            s_blk[o] = t;
+                for (int k = 0; k < KL; ++k) {
+                  vb[k] = Vi[(rr + k * GPW) * R + c];
+                  vk[k] = two ? Vk[(rr + k * GPW) * R + c] : zero<XT>();
+                }
+#pragma unroll
+                for (int k = 0; k < KL; ++k) {
+                  const int o = (rr + k * GPW) * R + c;
+                  const XT wr = s_wr[o], xr = s_xr[o];
+                  ph = cfma(vb[k], wr, ph);
+                  pg = cfma(vb[k], xr, pg);
+                  ph2 = cfma(vk[k], wr, ph2);
+                  pg2 = cfma(vk[k], xr, pg2);
+                }
+              }
+              for (; rr < nrows_blk; rr += GPW) {
+                const int o = rr * R + c;
+                const XT v = Vi[o];
+                const XT v2 = two ? Vk[o] : zero<XT>();
+                ph = cfma(v, s_wr[o], ph);
+                pg = cfma(v, s_xr[o], pg);
+                ph2 = cfma(v2, s_wr[o], ph2);
+                pg2 = cfma(v2, s_xr[o], pg2);
+              }
+            }
+            ph = group_reduce<R>(ph, grp);
+            pg = group_reduce<R>(pg, grp);
+            ph2 = group_reduce<R>(ph2, grp);
+            pg2 = group_reduce<R>(pg2, grp);
+            if (grp == 0 && lane_ok) {
+              s_blk[i * R + c] = ph;
+              s_blk[(J + i) * R + c] = pg;
+              if (two) {
+                s_blk[i2 * R + c] = ph2;
+                s_blk[(J + i2) * R + c] = pg2;
+              }
+            }
           }
         } else {
           // ---- sub-phase A1: w = Op(D^-1 v_j) for the whole slab, CSR tiles
