@@ -5,6 +5,7 @@ is torch tensors (plumbing only); the arithmetic runs in libsylvadi_b200.so.
 """
 
 import ctypes
+import math
 
 import numpy as np
 import scipy.sparse as sp
@@ -318,16 +319,44 @@ def axpy(a, x, y, device=0, stream=None):
     return y
 
 
+def _lmax_herm2(a, b, d):
+    """Largest eigenvalue of the Hermitian 2 x 2 [[a, b], [conj(b), d]] (a, d real):
+    (a + d)/2 + sqrt(((a - d)/2)^2 + |b|^2) -- no cancellation for the maximum."""
+    h = 0.5 * (a - d)
+    return 0.5 * (a + d) + math.sqrt(h * h + (b.real * b.real + b.imag * b.imag))
+
+
 def sigma_max_from_gram(G):
-    """Largest singular value of a block from its Gram matrix X^H X."""
+    """Largest singular value of a block from its Gram matrix X^H X (closed
+    forms for r <= 2, the per-step host cost of the small configs)."""
     if G.size == 0:
         return 0.0
+    r = G.shape[0]
+    if r == 1:
+        return math.sqrt(max(G[0, 0].real, 0.0))
+    if r == 2:
+        b = 0.5 * (complex(G[0, 1]) + complex(G[1, 0]).conjugate())
+        return math.sqrt(max(_lmax_herm2(G[0, 0].real, b, G[1, 1].real), 0.0))
     ev = np.linalg.eigvalsh(0.5 * (G + G.conj().T))
     return float(np.sqrt(max(ev[-1], 0.0)))
 
 
 def product_norm_from_grams(Gw, Gt):
-    """||w t^*||_2 from Gw = w^H w and Gt = t^H t: sqrt(lambda_max(Gw^1/2 Gt Gw^1/2))."""
+    """||w t^*||_2 from Gw = w^H w and Gt = t^H t: sqrt(lambda_max(Gw^1/2 Gt Gw^1/2))
+    (= sqrt(lambda_max(Gw Gt)); closed forms for r <= 2)."""
+    r = Gw.shape[0]
+    if r == 1:
+        return math.sqrt(max(Gw[0, 0].real * Gt[0, 0].real, 0.0))
+    if r == 2:
+        # eigenvalues of Gw Gt (similar to the Hermitian PSD Gw^1/2 Gt Gw^1/2):
+        # tr/2 + sqrt(tr^2/4 - det), det = det(Gw) det(Gt) >= 0
+        bw = 0.5 * (complex(Gw[0, 1]) + complex(Gw[1, 0]).conjugate())
+        bt = 0.5 * (complex(Gt[0, 1]) + complex(Gt[1, 0]).conjugate())
+        aw, dw, at, dt = Gw[0, 0].real, Gw[1, 1].real, Gt[0, 0].real, Gt[1, 1].real
+        tr = aw * at + dw * dt + 2.0 * (bw * bt.conjugate()).real
+        det = max(aw * dw - abs(bw) ** 2, 0.0) * max(at * dt - abs(bt) ** 2, 0.0)
+        lam = 0.5 * tr + math.sqrt(max(0.25 * tr * tr - det, 0.0))
+        return math.sqrt(max(lam, 0.0))
     Gw = 0.5 * (Gw + Gw.conj().T)
     Gt = 0.5 * (Gt + Gt.conj().T)
     lam, Q = np.linalg.eigh(Gw)
