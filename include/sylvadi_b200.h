@@ -68,6 +68,9 @@ int64_t sad_kernel_launches(void);
 int sad_ctx_create(int device, sad_ctx** out);
 int sad_ctx_destroy(sad_ctx* ctx);
 const char* sad_last_error(const sad_ctx* ctx);
+/* Release the device memory the context caches for reuse (buffers of
+ * destroyed matrices, operators and workspaces; see sad_capi.cu DevCache). */
+int sad_ctx_trim(sad_ctx* ctx);
 /* Number of SMs of the context's device (grid sizing is a multiple of it). */
 int sad_ctx_num_sms(const sad_ctx* ctx);
 

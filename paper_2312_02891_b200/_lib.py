@@ -31,6 +31,7 @@ SIGNATURES = {
     "sad_ctx_destroy": (_c.c_int, [_vp]),
     "sad_last_error": (_c.c_char_p, [_vp]),
     "sad_ctx_num_sms": (_c.c_int, [_vp]),
+    "sad_ctx_trim": (_c.c_int, [_vp]),
     "sad_csr_create": (_c.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _c.c_int,
                                   _c.POINTER(_vp)]),
     "sad_csr_destroy": (_c.c_int, [_vp]),

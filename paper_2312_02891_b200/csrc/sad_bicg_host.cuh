@@ -44,14 +44,14 @@ extern "C" int sad_bicg_create(sad_ctx* ctx, int64_t n, int r, int dtype, sad_bi
   w->max_blocks = ctx->nsm * 8;
   const int pstride = 5 * 8;
   size_t sb = (size_t)r * (5 * 16 + 3 * 8 + 2 * 8 + 8 * 4) + 16 * 8 + 256;
-  if (cudaMalloc(&w->vecs, blk * 7) != cudaSuccess ||
-      cudaMalloc(&w->state, sb) != cudaSuccess ||
-      cudaMalloc(&w->part, (size_t)w->max_blocks * pstride * sizeof(double)) != cudaSuccess ||
+  if (ctx_malloc(ctx, (void**)&w->vecs, blk * 7) != cudaSuccess ||
+      ctx_malloc(ctx, (void**)&w->state, sb) != cudaSuccess ||
+      ctx_malloc(ctx, (void**)&w->part, (size_t)w->max_blocks * pstride * sizeof(double)) != cudaSuccess ||
       cudaHostAlloc(&w->hflag_host, 8 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&w->hflag_dev, w->hflag_host, 0) != cudaSuccess) {
-    cudaFree(w->vecs);
-    cudaFree(w->state);
-    cudaFree(w->part);
+    ctx_free(ctx, w->vecs);
+    ctx_free(ctx, w->state);
+    ctx_free(ctx, w->part);
     if (w->hflag_host) cudaFreeHost(w->hflag_host);
     delete w;
     return set_err(ctx, SAD_ENOMEM, "BiCGstab workspace allocation failed");
@@ -95,9 +95,9 @@ extern "C" int sad_bicg_create(sad_ctx* ctx, int64_t n, int r, int dtype, sad_bi
 
 extern "C" int sad_bicg_destroy(sad_bicg* w) {
   if (!w) return SAD_OK;
-  cudaFree(w->vecs);
-  cudaFree(w->state);
-  cudaFree(w->part);
+  ctx_free(w->ctx, w->vecs);
+  ctx_free(w->ctx, w->state);
+  ctx_free(w->ctx, w->part);
   if (w->hflag_host) cudaFreeHost(w->hflag_host);
   delete w;
   return SAD_OK;

@@ -17,6 +17,8 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <map>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -32,7 +34,23 @@ using namespace sad;
 
 #define SAD_ABI_VERSION 1
 
+// Device allocations of matrices, operators and workspaces go through a
+// per-context cache: a destroyed handle's buffers are kept for reuse instead
+// of cudaFree (which synchronises the device; tearing down an ADI engine's
+// two dozen operators cost ~50 ms of a ~120 ms config-2 call).  A reused
+// buffer may still be in use by kernels launched before its previous owner
+// was destroyed, so the first reuse after any free synchronises the device
+// once (cheap: it happens when a new engine is built, with the device idle).
+struct DevCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;   // size -> pointer
+  std::unordered_map<void*, size_t> live;     // pointer -> size
+  size_t free_bytes = 0;
+  bool pending = false;                       // frees since the last device sync
+};
+
 struct sad_ctx {
+  DevCache cache;
   int device = 0;
   int nsm = 148;
   std::string err;
@@ -172,6 +190,73 @@ static int set_err(sad_ctx* ctx, int code, const char* fmt, ...) {
 
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+static constexpr size_t kCacheLimit = (size_t)8 << 30;   // cached free bytes before a release
+
+static size_t cache_round(size_t n) {
+  const size_t g = n >= ((size_t)2 << 20) ? ((size_t)2 << 20) : 4096;
+  return (n + g - 1) / g * g;
+}
+
+static void cache_release_locked(DevCache& c) {
+  if (c.free_blocks.empty()) return;
+  cudaDeviceSynchronize();
+  for (auto& kv : c.free_blocks) cudaFree(kv.second);
+  c.free_blocks.clear();
+  c.free_bytes = 0;
+  c.pending = false;
+}
+
+// cudaMalloc through the context's cache (best fit within 1/8 + 4 KB slack)
+static cudaError_t ctx_malloc(sad_ctx* ctx, void** p, size_t n) {
+  DevCache& c = ctx->cache;
+  const size_t rn = cache_round(std::max<size_t>(n, 1));
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.free_blocks.lower_bound(rn);
+  if (it != c.free_blocks.end() && it->first <= rn + rn / 8 + 4096) {
+    if (c.pending) {
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) return e;
+      c.pending = false;
+    }
+    *p = it->second;
+    c.live[it->second] = it->first;
+    c.free_bytes -= it->first;
+    c.free_blocks.erase(it);
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc(p, rn);
+  if (e == cudaErrorMemoryAllocation && !c.free_blocks.empty()) {
+    cudaGetLastError();
+    cache_release_locked(c);
+    e = cudaMalloc(p, rn);
+  }
+  if (e == cudaSuccess) c.live[*p] = rn;
+  return e;
+}
+
+static void ctx_free(sad_ctx* ctx, void* p) {
+  if (!p) return;
+  DevCache& c = ctx->cache;
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.live.find(p);
+  if (it == c.live.end()) {   // not from the cache
+    cudaFree(p);
+    return;
+  }
+  c.free_blocks.insert({it->second, p});
+  c.free_bytes += it->second;
+  c.live.erase(it);
+  c.pending = true;
+  if (c.free_bytes > kCacheLimit) cache_release_locked(c);
+}
+
+extern "C" int sad_ctx_trim(sad_ctx* ctx) {
+  if (!ctx) return SAD_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->cache.mu);
+  cache_release_locked(ctx->cache);
+  return SAD_OK;
+}
+
 extern "C" int sad_version(void) { return SAD_ABI_VERSION; }
 extern "C" int64_t sad_kernel_launches(void) { return g_launches.load(); }
 
@@ -203,6 +288,10 @@ extern "C" int sad_ctx_create(int device, sad_ctx** out) {
 
 extern "C" int sad_ctx_destroy(sad_ctx* c) {
   if (!c) return SAD_OK;
+  {
+    std::lock_guard<std::mutex> lk(c->cache.mu);
+    cache_release_locked(c->cache);
+  }
   cudaFree(c->scratch);
   cudaFree(c->ticket);
   cudaFree(c->gram_out);
@@ -246,9 +335,9 @@ static void host_transpose(long long nr, long long nc, const std::vector<int>& r
 static int upload_csr(sad_ctx* ctx, DevCsr& d, const std::vector<int>& rp,
                       const std::vector<int>& ci, const std::vector<double>& v) {
   // +64 bytes: the TMA bulk SpMM widens its source ranges to 16-byte alignment
-  CK(ctx, cudaMalloc(&d.rowptr, rp.size() * sizeof(int) + 64));
-  CK(ctx, cudaMalloc(&d.colidx, std::max<size_t>(ci.size(), 1) * sizeof(int) + 64));
-  CK(ctx, cudaMalloc(&d.vals, std::max<size_t>(v.size(), 1) * sizeof(double) + 64));
+  CK(ctx, ctx_malloc(ctx, (void**)&d.rowptr, rp.size() * sizeof(int) + 64));
+  CK(ctx, ctx_malloc(ctx, (void**)&d.colidx, std::max<size_t>(ci.size(), 1) * sizeof(int) + 64));
+  CK(ctx, ctx_malloc(ctx, (void**)&d.vals, std::max<size_t>(v.size(), 1) * sizeof(double) + 64));
   CK(ctx, cudaMemcpy(d.rowptr, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
   if (!ci.empty()) {
     CK(ctx, cudaMemcpy(d.colidx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -257,10 +346,10 @@ static int upload_csr(sad_ctx* ctx, DevCsr& d, const std::vector<int>& rp,
   return SAD_OK;
 }
 
-static void free_csr(DevCsr& d) {
-  cudaFree(d.rowptr);
-  cudaFree(d.colidx);
-  cudaFree(d.vals);
+static void free_csr(sad_ctx* ctx, DevCsr& d) {
+  ctx_free(ctx, d.rowptr);
+  ctx_free(ctx, d.colidx);
+  ctx_free(ctx, d.vals);
   d = DevCsr();
 }
 
@@ -300,8 +389,8 @@ extern "C" int sad_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_
     c->has_t = true;
   }
   if (rc != SAD_OK) {
-    free_csr(c->d);
-    free_csr(c->dt);
+    free_csr(ctx, c->d);
+    free_csr(ctx, c->dt);
     delete c;
     return rc;
   }
@@ -311,8 +400,8 @@ extern "C" int sad_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_
 
 extern "C" int sad_csr_destroy(sad_csr* c) {
   if (!c) return SAD_OK;
-  free_csr(c->d);
-  free_csr(c->dt);
+  free_csr(c->ctx, c->d);
+  free_csr(c->ctx, c->dt);
   delete c;
   return SAD_OK;
 }
@@ -390,17 +479,17 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
       rp[i + 1] = (int)ci.size();
     }
     size_t nz = ci.size();
-    CK(ctx, cudaMalloc(&op->own_rowptr, (n + 1) * sizeof(int) + 64));
-    CK(ctx, cudaMalloc(&op->own_colidx, std::max<size_t>(nz, 1) * sizeof(int) + 64));
+    CK(ctx, ctx_malloc(ctx, (void**)&op->own_rowptr, (n + 1) * sizeof(int) + 64));
+    CK(ctx, ctx_malloc(ctx, (void**)&op->own_colidx, std::max<size_t>(nz, 1) * sizeof(int) + 64));
     CK(ctx, cudaMemcpy(op->own_rowptr, rp.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
     if (nz) CK(ctx, cudaMemcpy(op->own_colidx, ci.data(), nz * sizeof(int), cudaMemcpyHostToDevice));
     if (cplx) {
       std::vector<double2> vc(nz);
       for (size_t k = 0; k < nz; ++k) vc[k] = make_double2(vr[k], vi[k]);
-      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double2) + 64));
+      CK(ctx, ctx_malloc(ctx, &op->own_vals, std::max<size_t>(nz, 1) * sizeof(double2) + 64));
       if (nz) CK(ctx, cudaMemcpy(op->own_vals, vc.data(), nz * sizeof(double2), cudaMemcpyHostToDevice));
     } else {
-      CK(ctx, cudaMalloc(&op->own_vals, std::max<size_t>(nz, 1) * sizeof(double) + 64));
+      CK(ctx, ctx_malloc(ctx, &op->own_vals, std::max<size_t>(nz, 1) * sizeof(double) + 64));
       if (nz) CK(ctx, cudaMemcpy(op->own_vals, vr.data(), nz * sizeof(double), cudaMemcpyHostToDevice));
     }
     op->rowptr = op->own_rowptr;
@@ -416,7 +505,7 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   // one allocation for both dinv copies; the breakdown flag lives in the ctx
   char* dbuf = nullptr;
   const size_t nn = (size_t)std::max<long long>(n, 1);
-  CK(ctx, cudaMalloc(&dbuf, nn * sizeof(double2) + nn * sizeof(double) + 256));
+  CK(ctx, ctx_malloc(ctx, (void**)&dbuf, nn * sizeof(double2) + nn * sizeof(double) + 256));
   op->dinv_c = reinterpret_cast<double2*>(dbuf);
   op->dinv_r = reinterpret_cast<double*>(dbuf + ((nn * sizeof(double2) + 255) & ~size_t(255)));
   int* d_bd = reinterpret_cast<int*>(ctx->ticket + 8);
@@ -447,10 +536,10 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
 
 extern "C" int sad_op_destroy(sad_op* op) {
   if (!op) return SAD_OK;
-  cudaFree(op->own_rowptr);
-  cudaFree(op->own_colidx);
-  cudaFree(op->own_vals);
-  cudaFree(op->dinv_c);   // dinv_r lives in the same allocation
+  ctx_free(op->ctx, op->own_rowptr);
+  ctx_free(op->ctx, op->own_colidx);
+  ctx_free(op->ctx, op->own_vals);
+  ctx_free(op->ctx, op->dinv_c);   // dinv_r lives in the same allocation
   delete op;
   return SAD_OK;
 }
@@ -606,12 +695,12 @@ static int gmres_create(sad_ctx* ctx, int64_t n, int64_t n_ext, int r, int dtype
     return set_err(ctx, SAD_ECUDA, "cudaFuncSetAttribute failed");
   }
   ws->dot_blocks_per_sm = std::max(1, std::min(8, (int)((200 * 1024) / dsm)));
-  if (cudaMalloc(&ws->V, blk * (m + 1) + 64) != cudaSuccess) {
+  if (ctx_malloc(ctx, &ws->V, blk * (m + 1) + 64) != cudaSuccess) {
     delete ws;
     return set_err(ctx, SAD_ENOMEM, "basis allocation of %zu bytes failed", blk * (m + 1));
   }
-  if (ws->flexible && cudaMalloc(&ws->Z, blk * m) != cudaSuccess) {
-    cudaFree(ws->V);
+  if (ws->flexible && ctx_malloc(ctx, &ws->Z, blk * m) != cudaSuccess) {
+    ctx_free(ctx, ws->V);
     delete ws;
     return set_err(ctx, SAD_ENOMEM, "FGMRES Z allocation failed");
   }
@@ -635,8 +724,8 @@ static int gmres_create(sad_ctx* ctx, int64_t n, int64_t n_ext, int r, int dtype
   sb += 4 * 16 + 16 * 8;                     // barrier, err, stats
   sb += 64 * 16;                             // alignment slack
   ws->state_bytes = sb;
-  if (cudaMalloc(&ws->state, sb) != cudaSuccess ||
-      cudaMalloc(&ws->part, (size_t)ws->max_blocks * ws->pstride * sizeof(double)) != cudaSuccess ||
+  if (ctx_malloc(ctx, (void**)&ws->state, sb) != cudaSuccess ||
+      ctx_malloc(ctx, (void**)&ws->part, (size_t)ws->max_blocks * ws->pstride * sizeof(double)) != cudaSuccess ||
       cudaHostAlloc(&ws->hflag_host, 8 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&ws->hflag_dev, ws->hflag_host, 0) != cudaSuccess) {
     sad_gmres_destroy(ws);
@@ -697,15 +786,15 @@ extern "C" int sad_gmres_create(sad_ctx* ctx, int64_t n, int r, int dtype, int r
 
 extern "C" int sad_gmres_destroy(sad_gmres* ws) {
   if (!ws) return SAD_OK;
-  cudaFree(ws->xext);
-  cudaFree(ws->rsum);
+  ctx_free(ws->ctx, ws->xext);
+  ctx_free(ws->ctx, ws->rsum);
   if (ws->hist_host) cudaFreeHost(ws->hist_host);
   for (int i = 0; i < 3; ++i)
     if (ws->ev[i]) cudaEventDestroy(ws->ev[i]);
-  cudaFree(ws->V);
-  cudaFree(ws->Z);
-  cudaFree(ws->state);
-  cudaFree(ws->part);
+  ctx_free(ws->ctx, ws->V);
+  ctx_free(ws->ctx, ws->Z);
+  ctx_free(ws->ctx, ws->state);
+  ctx_free(ws->ctx, ws->part);
   if (ws->hflag_host) cudaFreeHost(ws->hflag_host);
   delete ws;
   return SAD_OK;

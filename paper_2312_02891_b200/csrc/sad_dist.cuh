@@ -547,7 +547,7 @@ extern "C" int sad_local_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, 
   std::vector<double> v(vals, vals + nnz);
   int rc = upload_csr(ctx, c->d, rp, ci, v);
   if (rc != SAD_OK) {
-    free_csr(c->d);
+    free_csr(ctx, c->d);
     delete c;
     return rc;
   }
@@ -580,7 +580,7 @@ extern "C" int sad_local_op_create(sad_ctx* ctx, const sad_csr* base, double sre
   op->real_ok = (sim == 0.0);
   const size_t nn = (size_t)std::max<long long>(op->ncols, 1);
   char* dbuf = nullptr;
-  CK(ctx, cudaMalloc(&dbuf, nn * sizeof(double2) + nn * sizeof(double) + 256));
+  CK(ctx, ctx_malloc(ctx, (void**)&dbuf, nn * sizeof(double2) + nn * sizeof(double) + 256));
   op->dinv_c = reinterpret_cast<double2*>(dbuf);
   op->dinv_r = reinterpret_cast<double*>(dbuf + ((nn * sizeof(double2) + 255) & ~size_t(255)));
   CK(ctx, cudaMemset(op->dinv_c, 0, nn * sizeof(double2)));
@@ -752,8 +752,8 @@ extern "C" int sad_dist_gmres_create(sad_ctx* ctx, int64_t n_loc, int64_t n_ext,
   ws->dual_smem = 2 * (size_t)(restart + 1) * kWarps * r * ws->esz + kWarps * r * 8;
   if (ws->dual_smem > 220 * 1024) ws->dist_dcgs2 = 0;   // CGS2 (single-dot smem) instead
   const size_t xb = (size_t)n_ext * r * ws->esz;
-  if (cudaMalloc(&ws->xext, xb) != cudaSuccess ||
-      cudaMalloc(&ws->rsum, (size_t)ws->pstride * sizeof(double)) != cudaSuccess ||
+  if (ctx_malloc(ctx, &ws->xext, xb) != cudaSuccess ||
+      ctx_malloc(ctx, (void**)&ws->rsum, (size_t)ws->pstride * sizeof(double)) != cudaSuccess ||
       cudaHostAlloc(&ws->hist_host, (size_t)(restart + 2) * sizeof(long long), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&ws->hist_dev, ws->hist_host, 0) != cudaSuccess) {
     sad_gmres_destroy(ws);
