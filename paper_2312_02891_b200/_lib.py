@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsylvadi_b200.so")
+#: SAD_LIB_PATH selects another build of the library (A/B experiments)
+LIB_PATH = os.environ.get("SAD_LIB_PATH") or os.path.join(_HERE, "libsylvadi_b200.so")
 
 SAD_OK, SAD_EINVAL, SAD_EBREAKDOWN, SAD_ECUDA, SAD_ENCCL, SAD_ENOMEM = range(6)
 SAD_F64, SAD_C128 = 0, 1

@@ -17,11 +17,14 @@ spec = cfgs.CONFIGS[name]
 A, B, M, C, f, g = cfgs.build_problem(name)
 pairs, cyclic = spec.load_shift_pairs()
 prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
-cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax, precond_kind_A="jacobi",
+cfg = pb.AdiConfig(strategy=spec.strategy, kmax=int(os.environ.get("KMAX", spec.kmax)),
+                   precond_kind_A="jacobi",
                    precond_kind_B="jacobi")
 seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
-for conc in (True, False):
-    for phase_a in ("direct", "tma"):
+CONC = [c == "1" for c in os.environ.get("CONC", "1,0").split(",")]
+PHASE = os.environ.get("PHASE", "direct,tma").split(",")
+for conc in CONC:
+    for phase_a in PHASE:
         eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                            concurrent=conc, phase_a=phase_a)
         eng.warm()
