@@ -1,6 +1,8 @@
 // sad_coop.cu -- one variant of the cooperative persistent GMRES launcher
 // (see sad_coop.cuh).  Compiled once per -DSAD_COOP_VARIANT=<n> (0..9) by
 // paper_2312_02891_b200/_build.py.
+#include <mutex>
+
 #include "sad_coop.cuh"
 
 #ifndef SAD_COOP_VARIANT
@@ -13,11 +15,29 @@ template <typename XT, typename VT, int R, bool SIGMA, bool FLEX>
 static cudaError_t coop_launch_t(PArgs<XT> a, const CoopCfg& cfg, cudaStream_t s, size_t smem,
                                  int* grid_out) {
   auto kern = k_gmres_persistent<XT, VT, R, true, SIGMA, FLEX>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // the smem attribute and the occupancy query cost tens of microseconds per
+  // call; both depend only on smem here, so they are cached per variant (the
+  // small configs launch one solve per side per outer step)
+  static std::mutex mu;
+  static size_t attr_smem = 0;
+  static size_t occ_smem = ~size_t(0);
+  static int occ_nb = 0;
   int nb = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (smem > attr_smem) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_smem = smem;
+    }
+    if (smem != occ_smem) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_nb, kern, kThreads, smem);
+      if (e != cudaSuccess) return e;
+      occ_smem = smem;
+    }
+    nb = occ_nb;
+  }
   if (nb < 1) return cudaErrorInvalidConfiguration;
   const int sms = cfg.max_sms > 0 ? (cfg.max_sms < cfg.nsm ? cfg.max_sms : cfg.nsm) : cfg.nsm;
   const long long elems = a.n * R;
