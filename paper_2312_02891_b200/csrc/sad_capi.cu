@@ -138,6 +138,7 @@ struct sad_gmres {
   int pstride = 0;
   long long* hflag_host = nullptr;
   long long* hflag_dev = nullptr;
+  long long* res_host = nullptr;   // pinned: iterations [8] | residual norms [8]
   GState st{};
   int64_t bytes = 0;
   int dot_blocks_per_sm = 1;
@@ -727,6 +728,7 @@ static int gmres_create(sad_ctx* ctx, int64_t n, int64_t n_ext, int r, int dtype
   if (ctx_malloc(ctx, (void**)&ws->state, sb) != cudaSuccess ||
       ctx_malloc(ctx, (void**)&ws->part, (size_t)ws->max_blocks * ws->pstride * sizeof(double)) != cudaSuccess ||
       cudaHostAlloc(&ws->hflag_host, 8 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc(&ws->res_host, 16 * sizeof(long long), cudaHostAllocDefault) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&ws->hflag_dev, ws->hflag_host, 0) != cudaSuccess) {
     sad_gmres_destroy(ws);
     return set_err(ctx, SAD_ENOMEM, "workspace allocation failed");
@@ -796,6 +798,7 @@ extern "C" int sad_gmres_destroy(sad_gmres* ws) {
   ctx_free(ws->ctx, ws->state);
   ctx_free(ws->ctx, ws->part);
   if (ws->hflag_host) cudaFreeHost(ws->hflag_host);
+  if (ws->res_host) cudaFreeHost(ws->res_host);
   delete ws;
   return SAD_OK;
 }
@@ -970,10 +973,11 @@ static int read_results(sad_gmres* ws, void* res, cudaStream_t s, int64_t* iters
   sad_ctx* ctx = ws->ctx;
   const int R = ws->R;
   if (res) CK(ctx, cudaMemcpyAsync(res, ws->V, (size_t)ws->n * R * ws->esz, cudaMemcpyDeviceToDevice, s));
-  std::vector<long long> it(R);
-  std::vector<double> be(R);
-  CK(ctx, cudaMemcpyAsync(it.data(), ws->st.iters, R * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  CK(ctx, cudaMemcpyAsync(be.data(), ws->st.beta, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+  // pinned staging (a pageable destination would make each copy a staged, slower transfer)
+  long long* it = ws->res_host;
+  double* be = reinterpret_cast<double*>(ws->res_host + 8);
+  CK(ctx, cudaMemcpyAsync(it, ws->st.iters, R * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(ctx, cudaMemcpyAsync(be, ws->st.beta, R * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(ctx, cudaStreamSynchronize(s));
   for (int c = 0; c < R; ++c) {
     if (iters) iters[c] = it[c];
@@ -1566,7 +1570,9 @@ extern "C" int sad_gmres_finish(sad_gmres* ws, void* res, void* stream, int64_t*
                                 double* resnorm_host, uint8_t* conv_host) {
   if (!ws) return SAD_EINVAL;
   cudaStream_t s = S_(stream);
-  if (!ws->pending_multi) {
+  // profiling needs the launch's events and counters; otherwise the single
+  // synchronisation inside read_results also reports a failed launch
+  if (!ws->pending_multi && ws->profile) {
     int rc = persistent_collect(ws, s);
     if (rc) return rc;
   }
