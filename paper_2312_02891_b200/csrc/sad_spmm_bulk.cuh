@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
   __shared__ int s_kb[S];
   __shared__ int s_staged[S];
 
+  // Arnoldi mode (multi-kernel and row-partitioned engines): w = S_j Op(D^-1 v_j)
+  // from basis block j into block j + 1 (+ the FGMRES Z_j), nothing once every
+  // column of the cycle has stopped
+  if (MODE == SPMM_ARNOLDI && *a.st.any_active == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const VT* vals = reinterpret_cast<const VT*>(a.vals);
   const long long ntiles = (a.n + TR - 1) / TR;
@@ -173,6 +177,15 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
   const bool lane_ok = grp < GPW;
   const XT* x = a.x;
   XT* y = a.y;
+  XT* zout = nullptr;
+  double scale = 1.0;
+  if (MODE == SPMM_ARNOLDI) {
+    const int j = *a.st.j;
+    x = a.x + (long long)j * a.stride;
+    y = const_cast<XT*>(a.x) + (long long)(j + 1) * a.stride;
+    if (a.zout) zout = a.zout + (long long)j * a.stride;
+    scale = lane_ok ? a.st.S[j * R + c] : 0.0;
+  }
   for (long long k = 0; k < K; ++k) {
     const int st = (int)(k % S);
     mbar_wait(full + st, (unsigned)((k / S) & 1));
@@ -231,11 +244,13 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
       for (int u = 0; u < U; ++u) {
         if (idx[u] < 0) continue;
         XT vres = acc[u];
-        if (SIGMA) {
+        if (SIGMA || (MODE == SPMM_ARNOLDI && zout)) {
           XT xi = x[idx[u]];
           if (PRE) xi = mul(__ldg(a.dinv + idx[u] / R), xi);
-          vres = fma_(from_c<XT>(a.sigma), xi, vres);
+          if (SIGMA) vres = fma_(from_c<XT>(a.sigma), xi, vres);
+          if (MODE == SPMM_ARNOLDI && zout) zout[idx[u]] = sscal(scale, xi);
         }
+        if (MODE == SPMM_ARNOLDI) vres = sscal(scale, vres);
         if (MODE == SPMM_RESID || MODE == SPMM_RESID_CYCLE) vres = sub(a.b[idx[u]], vres);
         y[idx[u]] = vres;
       }

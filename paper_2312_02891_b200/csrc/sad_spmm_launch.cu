@@ -27,7 +27,7 @@ static int grid_for(long long work, int per_block, int cap) {
 // -----------------------------------------------------------------------------
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
 static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
-  if constexpr (MODE == SPMM_APPLY || MODE == SPMM_RESID) {
+  if constexpr (MODE == SPMM_APPLY || MODE == SPMM_RESID || MODE == SPMM_ARNOLDI) {
     // TMA-staged SpMM; grid = resident blocks (persistent over row tiles)
     auto kern = k_spmm_bulk<XT, VT, R, MODE, PRE, SIGMA>;
     constexpr size_t smem = bulk_smem_bytes<VT, R>();
