@@ -120,8 +120,12 @@ class Clocks:
               "clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device):
+    def __init__(self, device, period_ms=1000):
+        # one query per second: each nvidia-smi query takes the driver lock and
+        # can stall a latency-bound solve's launches by ~20 ms (config 2 steps
+        # are ~80 ms), so sample sparsely; long configs still get many samples
         self.device = device
+        self.period_ms = period_ms
         self.proc = None
         self.lines = []
 
@@ -129,7 +133,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -307,15 +311,17 @@ def run_ours_c2(args, dist, name="c2"):
     spec, prob, cfg, seq, raw = build_c2(name)
     eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible, device=dev)
     eng.warm()
+    # the clock sampler starts before the warm-up: nvidia-smi's start-up (NVML
+    # initialisation) stalls CUDA calls of this process for tens of ms
+    clocks = Clocks(dev)
+    clocks.start()
     for _ in range(args.warmup):
         _, rep, _ = eng.run()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    clocks = Clocks(dev)
     times, reps = [], []
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.sad_kernel_launches()
-    clocks.start()
     for _ in range(args.steps):
         flush.fill_(1.0)
         e0 = torch.cuda.Event(enable_timing=True)
@@ -333,6 +339,7 @@ def run_ours_c2(args, dist, name="c2"):
     ms = statistics.mean(times)
     ms_max = dist.max(ms)
     rep = reps[-1]
+    step_ms = [round(x, 2) for x in times]
 
     # the same ADI with the reference's own inner algorithm on the device
     # (Jacobi-BiCGstab, solver="bicgstab"): the apples-to-apples comparison
@@ -441,6 +448,7 @@ def run_ours_c2(args, dist, name="c2"):
                                         "download_ms")}},
         "gpu_launches": int(launches),
         "clocks": ck,
+        "step_ms": step_ms,
     }
     if same_alg is not None:
         line["same_algorithm_as_reference"] = same_alg
@@ -489,13 +497,14 @@ def run_ours_c4(args, dist):
     # --- shifted SpMM (the metric): K timed launches, L2 flushed in between ---
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     y = torch.empty_like(rhs)
+    clocks = Clocks(dev)
+    clocks.start()          # before the warm-up (see run_ours_c2)
     for _ in range(args.warmup):
         op.apply(rhs, y)
-    clocks = Clocks(dev)
+    time.sleep(0.3)         # the sampler's start-up is over before the timed region
     dist.barrier()
     torch.cuda.synchronize()
     l0 = lib.sad_kernel_launches()
-    clocks.start()
     ms = []
     for _ in range(args.steps):
         flush.fill_(1.0)
@@ -560,15 +569,15 @@ def run_ours_sharded(args, dist, name):
                        device=dev, force_rowpart=args.rowpart)
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
+        clocks = Clocks(dev)
+        clocks.start()      # before the warm-up (see run_ours_c2)
         for _ in range(args.warmup):
             run.run()
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-        clocks = Clocks(dev)
         times = []
         dist.barrier()
         torch.cuda.synchronize()
         l0 = lib.sad_kernel_launches()
-        clocks.start()
         for _ in range(args.steps):
             flush.fill_(1.0)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -641,13 +650,14 @@ def run_ours_c4_rowpart(args, dist):
         _lib.check(rc, rp._ctx)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    clocks = Clocks(dev)
+    clocks.start()          # before the warm-up (see run_ours_c2)
     for _ in range(args.warmup):
         apply()
-    clocks = Clocks(dev)
+    time.sleep(0.3)
     dist.barrier()
     torch.cuda.synchronize()
     l0 = lib.sad_kernel_launches()
-    clocks.start()
     ms = []
     for _ in range(args.steps):
         flush.fill_(1.0)

@@ -297,6 +297,40 @@ int sad_bicg_solve(sad_bicg* ws, sad_op* op, const void* rhs_dev, void* x_dev, v
                    double tol_col, int maxit, void* stream, int64_t* iters_host,
                    double* resnorm_host, uint8_t* conv_host);
 
+/* ---------------------------------------------------------------------------
+ * The device-resident ADI outer loop in native code: run_with_state
+ * (adi.py:553-607) with adi_step (adi.py:510-537) for the iterative
+ * strategies, inner solves by the persistent GMRES kernel.  Same loop as
+ * paper_2312_02891_b200/adi.py DeviceAdi.run, without interpreter overhead per
+ * step.  Host scalars as in AdiConfig (adi.py:130-180).
+ * ------------------------------------------------------------------------- */
+enum sad_strategy { SAD_STRAT_FIXED = 0, SAD_STRAT_DYNAMIC_MID = 1, SAD_STRAT_DYNAMIC_MID_BL = 2,
+                    SAD_STRAT_DYNAMIC_B = 3, SAD_STRAT_DYNAMIC_B_BL = 4 };
+typedef struct {
+  int strategy;                /* enum sad_strategy */
+  int kmax;
+  int max_inner_iterations;
+  double outer_tolerance;
+  double xi;
+  double gap_budget;           /* <= 0: outer_tolerance * ||f g^*|| (adi.py:563-565) */
+  double fixed_delta;
+  double delta_min_A, delta_max_A, delta_min_B, delta_max_B;
+} sad_adi_config;
+/* records[k][14] per step: scaled_res, delta_A, delta_B, achieved_rA,
+ * achieved_rB, inner_it_A, inner_it_B, u, v, a_converged, b_converged,
+ * clamped_A_min, clamped_B_min, wall_ms (StepRecord, adi.py:193-210);
+ * summary[5]: ||f g^*||, converged, final scaled residual, u, v.
+ * opsA/opsB/gammas: per step k (kmax entries; gammas complex interleaved);
+ * z_base/y_base: kmax contiguous n x r blocks (z_k, y_k); w, t: f, g in,
+ * updated in place; M, C may be NULL (identity; C applied transposed). */
+#define SAD_ADI_REC 14
+int sad_adi_run(sad_ctx* ctx, const sad_adi_config* cfg, int r, int dtype, int64_t nA, int64_t nB,
+                sad_gmres* wsA, sad_gmres* wsB, sad_op* const* opsA, sad_op* const* opsB,
+                const double* gammas, sad_csr* M, sad_csr* C, void* w_dev, void* t_dev,
+                void* z_base, void* y_base, void* resA_dev, void* resB_dev, void* mz_buf,
+                void* cty_buf, int concurrent, void* stream_main, void* streamA, void* streamB,
+                double* records, int* steps_out, double* summary);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,7 +93,25 @@ SIGNATURES = {
     "sad_bicg_bytes": (_i64, [_vp]),
     "sad_bicg_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp, _vp,
                                   _vp, _vp]),
+    # native ADI outer loop
+    "sad_adi_run": (_c.c_int, [_vp, _vp, _c.c_int, _c.c_int, _i64, _i64, _vp, _vp, _vp, _vp,
+                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _c.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
+
+
+class AdiConfigC(_c.Structure):
+    """sad_adi_config (include/sylvadi_b200.h)."""
+    _fields_ = [("strategy", _c.c_int), ("kmax", _c.c_int), ("max_inner_iterations", _c.c_int),
+                ("outer_tolerance", _c.c_double), ("xi", _c.c_double),
+                ("gap_budget", _c.c_double), ("fixed_delta", _c.c_double),
+                ("delta_min_A", _c.c_double), ("delta_max_A", _c.c_double),
+                ("delta_min_B", _c.c_double), ("delta_max_B", _c.c_double)]
+
+
+SAD_ADI_REC = 14
+STRATEGY_CODES = {"fixed": 0, "dynamic_mid": 1, "dynamic_mid_bl": 2, "dynamic_b": 3,
+                  "dynamic_b_bl": 4}
 
 
 class FactorizationBreakdown(RuntimeError):

@@ -31,6 +31,7 @@ import numpy as np
 
 from .device import (DeviceMatrix, adi_epilogue, as_csr, axpy, gram,
                      product_norm_from_grams, sigma_max_from_gram)
+from . import _lib
 from .krylov import GpuGmresBinding, SolverBindings
 from .shifts import ShiftSequence
 
@@ -547,7 +548,7 @@ class DeviceAdi:
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
                  device=0, concurrent="auto", engine="persistent", phase_a="auto",
-                 row_ranks=1, solver="gmres"):
+                 row_ranks=1, solver="gmres", native="auto"):
         import torch
         if not isinstance(problem, SylvesterProblem):
             problem = SylvesterProblem.from_reference(problem)
@@ -561,6 +562,14 @@ class DeviceAdi:
         self.device = device
         self.engine = engine
         self.solver = solver
+        # the outer loop in native code (sad_adi_run) for the persistent GMRES
+        # engine; the Python loop below stays the reference implementation
+        self.native = (native is True or native == "auto") and engine == "persistent" \
+            and solver == "gmres" and row_ranks == 1 and problem.r <= 8 \
+            and _strategy(config.strategy).value in _lib.STRATEGY_CODES
+        if native is True and not self.native:
+            raise ValueError("native outer loop needs the persistent GMRES engine, r <= 8 and "
+                             "an iterative strategy")
         if concurrent == "auto":
             # Small blocks are latency-bound: the two solves overlap on disjoint
             # SM sets.  Large blocks are HBM-bound: one solve at a time on every
@@ -621,7 +630,95 @@ class DeviceAdi:
             self.bA.operator(b)
             self.bB.operator(a)
 
+    def _native_fits(self):
+        """z_k / y_k of every possible step preallocated as one buffer each:
+        only when kmax steps fit in a quarter of the free device memory."""
+        import torch
+        esz = 16 if self.tdtype == torch.complex128 else 8
+        need = self.config.kmax * (self.problem.n + self.problem.m) * self.problem.r * esz
+        free, _ = torch.cuda.mem_get_info(self.dev)
+        return need <= free // 4
+
+    def _run_native(self, f=None, g=None):
+        """DeviceAdi.run's loop in C++ (sad_adi_run): same steps, records and
+        solution layout; the host does only scalar work between the solves."""
+        import ctypes
+
+        import torch
+        cfg, prob = self.config, self.problem
+        t0 = time.perf_counter()
+        r, K = prob.r, cfg.kmax
+        torch.cuda.synchronize(self.dev)
+        w = (self.f if f is None else f).clone()
+        t = (self.g if g is None else g).clone()
+        dtype = _lib.SAD_F64 if self.tdtype == torch.float64 else _lib.SAD_C128
+        pairs = [tuple(complex(x) for x in self.shifts.at(k)) for k in range(1, K + 1)]
+        opsA = (ctypes.c_void_p * K)(*[self.bA.operator(b).handle.value for a, b in pairs])
+        opsB = (ctypes.c_void_p * K)(*[self.bB.operator(a).handle.value for a, b in pairs])
+        gam = np.array([gamma(a, b) for a, b in pairs], dtype=np.complex128)
+        wsA = self.bA.workspace(r, dtype)
+        wsB = self.bB.workspace(r, dtype)
+        z_all = torch.empty((K, prob.n, r), dtype=self.tdtype, device=self.dev)
+        y_all = torch.empty((K, prob.m, r), dtype=self.tdtype, device=self.dev)
+        resA, resB = torch.empty_like(w), torch.empty_like(t)
+        mz = torch.empty_like(w) if self.Md is not None else None
+        cty = torch.empty_like(t) if self.Cd is not None else None
+        c = _lib.AdiConfigC(
+            strategy=_lib.STRATEGY_CODES[_strategy(cfg.strategy).value], kmax=K,
+            max_inner_iterations=int(cfg.max_inner_iterations),
+            outer_tolerance=cfg.outer_tolerance, xi=cfg.xi,
+            gap_budget=-1.0 if cfg.gap_budget is None else float(cfg.gap_budget),
+            fixed_delta=cfg.fixed_delta, delta_min_A=cfg.delta_min_A, delta_max_A=cfg.delta_max_A,
+            delta_min_B=cfg.delta_min_B, delta_max_B=cfg.delta_max_B)
+        recs = np.zeros((K, _lib.SAD_ADI_REC), dtype=np.float64)
+        summary = np.zeros(5, dtype=np.float64)
+        steps = ctypes.c_int(0)
+        cur = torch.cuda.current_stream(self.dev)
+        self.sA.wait_stream(cur)
+        self.sB.wait_stream(cur)
+        ptr = lambda x: None if x is None else x.data_ptr()   # noqa: E731
+        rc = _lib.load().sad_adi_run(
+            _lib.context(self.device), ctypes.byref(c), r, dtype, prob.n, prob.m, wsA.handle,
+            wsB.handle, opsA, opsB, gam.ctypes.data,
+            None if self.Md is None else self.Md.handle, None if self.Cd is None else self.Cd.handle,
+            w.data_ptr(), t.data_ptr(), z_all.data_ptr(), y_all.data_ptr(), resA.data_ptr(),
+            resB.data_ptr(), ptr(mz), ptr(cty), 1 if self.concurrent else 0,
+            ctypes.c_void_p(cur.cuda_stream), ctypes.c_void_p(self.sA.cuda_stream),
+            ctypes.c_void_p(self.sB.cuda_stream), recs.ctypes.data, ctypes.byref(steps),
+            summary.ctypes.data)
+        _lib.check(rc, _lib.context(self.device))
+        cur.wait_stream(self.sA)
+        cur.wait_stream(self.sB)
+        k_done = steps.value
+        report = SolveReport(rhs_norm=float(summary[0]), strategy=cfg.strategy)
+        for k in range(k_done):
+            q = recs[k]
+            rec = StepRecord(step=k + 1, scaled_res=q[0], delta_A=q[1], delta_B=q[2],
+                             achieved_rA=q[3], achieved_rB=q[4], inner_it_A=int(q[5]),
+                             inner_it_B=int(q[6]), u=q[7], v=q[8], wall_ms=q[13],
+                             a_converged=bool(q[9]), b_converged=bool(q[10]),
+                             clamped_A_min=bool(q[11]), clamped_B_min=bool(q[12]))
+            if not (rec.a_converged and rec.b_converged):
+                warnings.warn(f"inner solver missed its target at step {k + 1}; "
+                              "continuing with the achieved residual")
+            report.records.append(rec)
+        report.converged = bool(summary[1])
+        report.final_scaled_residual = float(summary[2]) if k_done else 0.0
+        zb = [z_all[k] for k in range(k_done)]
+        yb = [y_all[k] for k in range(k_done)]
+        gammas = [complex(x) for x in gam[:k_done]]
+        hist = pairs[:k_done]
+        return self._finish(report, zb, yb, gammas, hist, w, t, float(summary[3]),
+                            float(summary[4]), k_done, t0)
+
     def run(self, f=None, g=None):
+        cyclic_ok = getattr(self.shifts, "cyclic", True) or \
+            _seq_len(self.shifts) >= self.config.kmax
+        if self.native and cyclic_ok and self._native_fits():
+            return self._run_native(f, g)
+        return self._run_python(f, g)
+
+    def _run_python(self, f=None, g=None):
         import torch
         cfg, prob = self.config, self.problem
         t0 = time.perf_counter()

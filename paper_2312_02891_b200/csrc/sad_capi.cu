@@ -191,6 +191,16 @@ static int set_err(sad_ctx* ctx, int code, const char* fmt, ...) {
 
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Wait for a stream by polling it: the small configs' outer loop waits for
+// the solves once per step, and a blocking synchronisation that yields the
+// thread costs tens of microseconds of wake-up latency each time.
+static cudaError_t spin_sync(cudaStream_t s) {
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+  }
+}
+
 static constexpr size_t kCacheLimit = (size_t)8 << 30;   // cached free bytes before a release
 
 static size_t cache_round(size_t n) {
@@ -978,7 +988,7 @@ static int read_results(sad_gmres* ws, void* res, cudaStream_t s, int64_t* iters
   double* be = reinterpret_cast<double*>(ws->res_host + 8);
   CK(ctx, cudaMemcpyAsync(it, ws->st.iters, R * sizeof(long long), cudaMemcpyDeviceToHost, s));
   CK(ctx, cudaMemcpyAsync(be, ws->st.beta, R * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(ctx, cudaStreamSynchronize(s));
+  CK(ctx, spin_sync(s));
   for (int c = 0; c < R; ++c) {
     if (iters) iters[c] = it[c];
     if (resn) resn[c] = be[c];
@@ -1456,7 +1466,7 @@ extern "C" int sad_gram(sad_ctx* ctx, int64_t n, int r, int dtype, const void* x
     gram_launch<double2>(r, n, x, y, ctx->scratch, ctx->ticket, ctx->gram_out, grid, s);
   CKL(ctx);
   CK(ctx, cudaMemcpyAsync(ctx->gram_host, ctx->gram_out, r * r * sizeof(double2), cudaMemcpyDeviceToHost, s));
-  CK(ctx, cudaStreamSynchronize(s));
+  CK(ctx, spin_sync(s));
   std::memcpy(gram_host, ctx->gram_host, r * r * sizeof(double2));
   return SAD_OK;
 }
@@ -1539,7 +1549,7 @@ extern "C" int sad_adi_epilogue(sad_ctx* ctx, int64_t nA, int64_t nB, int r, int
   CKL(ctx);
   const size_t bytes = (size_t)6 * r * r * sizeof(double2);
   CK(ctx, cudaMemcpyAsync(ctx->epi_host, ctx->epi_out, bytes, cudaMemcpyDeviceToHost, s));
-  CK(ctx, cudaStreamSynchronize(s));
+  CK(ctx, spin_sync(s));
   std::memcpy(gram_host, ctx->epi_host, bytes);
   return SAD_OK;
 }
@@ -1687,3 +1697,4 @@ extern "C" int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int 
 
 #include "sad_dist.cuh"
 #include "sad_bicg_host.cuh"
+#include "sad_adi_host.cuh"
