@@ -444,8 +444,7 @@ def run_ours_c2(args, dist, name="c2"):
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "phases_ms": {k: statistics.mean(d.get(k, 0.0) for d in e2e_solve)
-                              for k in ("construct_ms", "run_ms", "inner_solve_ms",
-                                        "download_ms")}},
+                              for k in ("construct_ms", "run_ms", "download_ms")}},
         "gpu_launches": int(launches),
         "clocks": ck,
         "step_ms": step_ms,
