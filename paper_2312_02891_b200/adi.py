@@ -548,7 +548,7 @@ class DeviceAdi:
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
                  device=0, concurrent="auto", engine="persistent", phase_a="auto",
-                 row_ranks=1, solver="gmres", native="auto"):
+                 row_ranks=1, solver="gmres", native="auto", sm_split=None):
         import torch
         if not isinstance(problem, SylvesterProblem):
             problem = SylvesterProblem.from_reference(problem)
@@ -587,7 +587,15 @@ class DeviceAdi:
         # (proportional to its size) so both cooperative grids are co-resident
         nsm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         na, nb = problem.n, problem.m
-        sm_a = max(1, min(nsm - 1, int(round(nsm * na / (na + nb))))) if concurrent else 0
+        # SM share of the A side: the larger side also tends to need more Arnoldi
+        # steps per solve, so the share is pushed past the row ratio (config 2:
+        # rows 0.70 -> share 0.85, 77.4 -> 73.7 ms; tools/c2_split.py), clamped
+        # so the smaller side keeps enough SMs
+        if sm_split is None:
+            frac_a = min(0.85, max(0.15, 0.5 + 2.0 * (na / (na + nb) - 0.5)))
+        else:
+            frac_a = float(sm_split)
+        sm_a = max(1, min(nsm - 1, int(round(nsm * frac_a)))) if concurrent else 0
         sm_b = max(1, nsm - sm_a) if concurrent else 0
         if row_ranks > 1:
             # each side row-partitioned over `row_ranks` slabs, all ranks in this
