@@ -291,3 +291,32 @@ def test_bulk_spmm_many_tiles(rng, r):
     y2 = host(op2.apply(dev(xc)))
     want2 = A.T @ xc + np.conj(-3.0 + 2.0j) * xc
     assert np.max(np.abs(y2 - want2)) <= 1e-13 * np.max(np.abs(want2))
+
+
+def test_allocation_cache_reuse_and_trim(rng):
+    """Device buffers of destroyed handles are reused (sad_capi.cu DevCache):
+    operators built in the memory of destroyed ones give the same results,
+    and sad_ctx_trim releases the cache."""
+    import gc
+    from paper_2312_02891_b200 import _lib
+    from paper_2312_02891_b200.device import DeviceMatrix, DeviceOperator
+    n, r = 211, 3
+    base = rand_sparse(rng, n)
+    mass = rand_sparse(rng, n)
+    x = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+    shifts = [-1.5 + 0.3j, -2.5 - 0.1j, -0.75 + 0.0j]
+    want = [orc.ShiftedOp(base, mass, s).apply(x) for s in shifts]
+    for round_ in range(3):
+        dm = DeviceMatrix(base)
+        dmm = DeviceMatrix(mass)
+        ops = [DeviceOperator(dm, dmm, s) for s in shifts]
+        for op, w in zip(ops, want):
+            y = host(op.apply(dev(x)))
+            assert np.max(np.abs(y - w)) <= 1e-13 * np.max(np.abs(w)), round_
+        del ops, dm, dmm
+        gc.collect()
+    ctx = _lib.context(0)
+    _lib.check(_lib.load().sad_ctx_trim(ctx), ctx)
+    op = DeviceOperator(DeviceMatrix(base), DeviceMatrix(mass), shifts[0])
+    y = host(op.apply(dev(x)))
+    assert np.max(np.abs(y - want[0])) <= 1e-13 * np.max(np.abs(want[0]))
