@@ -57,6 +57,7 @@ typedef struct sad_gmres sad_gmres;
 typedef struct sad_comm sad_comm;
 typedef struct sad_halo sad_halo;
 typedef struct sad_bicg sad_bicg;
+typedef struct sad_minres sad_minres;
 
 /* ABI version (bumped on any signature change). */
 int sad_version(void);
@@ -296,6 +297,26 @@ int64_t sad_bicg_bytes(const sad_bicg* ws);
 int sad_bicg_solve(sad_bicg* ws, sad_op* op, const void* rhs_dev, void* x_dev, void* res_dev,
                    double tol_col, int maxit, void* stream, int64_t* iters_host,
                    double* resnorm_host, uint8_t* conv_host);
+
+/* ---------------------------------------------------------------------------
+ * The reference's inner solver for Hermitian sides on the device: split-
+ * preconditioned MINRES (Paige-Saunders) per column (krylov.py:187-287),
+ * batched over the r columns of a block in lock step, the recurrence scalars,
+ * true-residual checks and stopping on the device.  Replaces
+ * minres(InnerSolveRequest(op, rhs, tol, maxit, precond)) (krylov.py:271)
+ * behind SolverBinding.solve when uses_minres(shift) (adi.py:468-488): real
+ * shift, symmetric base/mass, preconditioner "none" or "jacobi" (SPD split
+ * |dinv|, precond.py:242-256).  Same stopping rule (phibar <= check_at, then
+ * ||b - Op x|| <= tol_col), iteration counts per column, residual = b - Op x.
+ * SAD_EINVAL for a complex shift; SAD_EBREAKDOWN if beta1^2 <= 0
+ * (the reference's RuntimeError, krylov.py:203-205).
+ * ------------------------------------------------------------------------- */
+int sad_minres_create(sad_ctx* ctx, int64_t n, int r, int dtype, sad_minres** out);
+int sad_minres_destroy(sad_minres* ws);
+int64_t sad_minres_bytes(const sad_minres* ws);
+int sad_minres_solve(sad_minres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
+                     void* res_dev, double tol_col, int maxit, void* stream,
+                     int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
 
 /* ---------------------------------------------------------------------------
  * The device-resident ADI outer loop in native code: run_with_state

@@ -346,6 +346,96 @@ def bicgstab(op, rhs, abs_tolerance, max_iterations=1000, dinv=None):
     return _finalize(op, rhs, x, iters, tol_col)
 
 
+# -- MINRES (the reference's inner solver for Hermitian sides) -----------------
+
+def _minres_column(op, dinv, b, tol, maxit):
+    """krylov.py:187-268 -- split-preconditioned MINRES (Paige-Saunders), one
+    column.  The SPD split of Jacobi is |dinv| (precond.py:242-256); dinv None
+    is the identity."""
+    n = b.shape[0]
+    x = np.zeros(n, dtype=np.complex128)
+    if np.linalg.norm(b) <= tol:
+        return x, 0
+    pabs = None if dinv is None else np.abs(dinv)
+    psolve = (lambda v: v.copy()) if pabs is None else (lambda v: v * pabs)
+    r1 = b.astype(np.complex128)
+    y = psolve(r1)
+    beta1_sq = np.vdot(r1, y).real
+    if beta1_sq <= 0.0:
+        raise RuntimeError("MINRES preconditioner is not positive definite")
+    beta1 = np.sqrt(beta1_sq)
+    oldb, beta, dbar, epsln, phibar = 0.0, beta1, 0.0, 0.0, beta1
+    cs, sn = -1.0, 0.0
+    w = np.zeros(n, dtype=np.complex128)
+    w2 = np.zeros(n, dtype=np.complex128)
+    r2 = r1.copy()
+    ratio = np.linalg.norm(b) / beta1
+    check_at = tol / max(ratio, 1e-300)
+    it = 0
+    while it < maxit:
+        it += 1
+        s = 1.0 / beta
+        v = s * y
+        y = op.apply(v[:, None])[:, 0]
+        if it >= 2:
+            y -= (beta / oldb) * r1
+        alfa = np.vdot(v, y).real
+        y -= (alfa / beta) * r2
+        r1 = r2
+        r2 = y
+        y = psolve(r2)
+        oldb = beta
+        beta = np.sqrt(max(np.vdot(r2, y).real, 0.0))
+        oldeps = epsln
+        delta = cs * dbar + sn * alfa
+        gbar = sn * dbar - cs * alfa
+        epsln = sn * beta
+        dbar = -cs * beta
+        gamma = max(np.hypot(gbar, beta), 1e-300)
+        cs = gbar / gamma
+        sn = beta / gamma
+        phi = cs * phibar
+        phibar = sn * phibar
+        w1 = w2
+        w2 = w
+        w = (v - oldeps * w1 - delta * w2) / gamma
+        x = x + phi * w
+        if phibar <= check_at:
+            nr = np.linalg.norm(b - op.apply(x[:, None])[:, 0])
+            if nr <= tol:
+                return x, it
+            if phibar <= 1e-300:
+                break
+            check_at = min(check_at, 0.5 * tol * phibar / nr)
+        if beta <= 1e-300:
+            break
+    return x, it
+
+
+def minres(op, rhs, abs_tolerance, max_iterations=1000, dinv=None):
+    """krylov.py:271-287 (per column, no resume)."""
+    rhs = _check_request(op, rhs, abs_tolerance)
+    r = rhs.shape[1]
+    tol_col = abs_tolerance / r
+    x = np.zeros_like(rhs)
+    iters = np.zeros(r, dtype=np.int64)
+    for c in range(r):
+        xc, it = _minres_column(op, dinv, rhs[:, c], tol_col, max_iterations)
+        x[:, c] = xc
+        iters[c] = it
+    return _finalize(op, rhs, x, iters, tol_col)
+
+
+def is_symmetric(matrix, tol=1e-12):
+    """adi.py:413-419"""
+    csr = sp.csr_matrix(matrix)
+    diff = (csr - csr.T).tocoo()
+    if diff.nnz == 0:
+        return True
+    scale = max(np.abs(csr.data).max(initial=0.0), 1.0)
+    return np.abs(diff.data).max(initial=0.0) <= tol * scale
+
+
 def _check_request(op, rhs, abs_tolerance):
     """krylov.py:25-35 (InnerSolveRequest validation)."""
     rhs = np.asarray(rhs, dtype=np.complex128)
@@ -497,7 +587,9 @@ class Binding:
     """adi.py:422-488 restricted to the iterative Jacobi path.
 
     ``solver`` is "bicgstab" (the reference's own choice for unsymmetric
-    operators, adi.py:486-488) or "gmres"/"fgmres" (the B200 build's solver).
+    operators, adi.py:486-488), "minres", "reference" (the reference's
+    dispatch: MINRES for a symmetric side at a real shift, else BiCGstab,
+    adi.py:468-488) or "gmres"/"fgmres" (the B200 build's solver).
     """
 
     def __init__(self, side, base, mass, solver="gmres", max_iterations=1000,
@@ -522,9 +614,19 @@ class Binding:
             self._ops[shift] = hit
         return hit
 
+    def uses_minres(self, shift):
+        """adi.py:468-472 (iterative mode)."""
+        if self.solver == "minres":
+            return True
+        return (self.solver == "reference" and complex(shift).imag == 0.0
+                and self.precond in ("none", "jacobi") and is_symmetric(self.base)
+                and (self.mass is None or is_symmetric(self.mass)))
+
     def solve(self, shift, rhs, delta):
         op, dinv = self._op(shift)
-        if self.solver == "bicgstab":
+        if self.uses_minres(shift):
+            return minres(op, rhs, delta, self.max_iterations, dinv)
+        if self.solver in ("bicgstab", "reference"):
             return bicgstab(op, rhs, delta, self.max_iterations, dinv)
         return gmres(op, rhs, delta, self.max_iterations, dinv,
                      restart=self.restart, flexible=(self.solver == "fgmres"),

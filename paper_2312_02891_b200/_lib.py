@@ -93,6 +93,12 @@ SIGNATURES = {
     "sad_bicg_bytes": (_i64, [_vp]),
     "sad_bicg_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp, _vp,
                                   _vp, _vp]),
+    # device MINRES (the reference's inner solver for Hermitian sides)
+    "sad_minres_create": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.POINTER(_vp)]),
+    "sad_minres_destroy": (_c.c_int, [_vp]),
+    "sad_minres_bytes": (_i64, [_vp]),
+    "sad_minres_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp, _vp,
+                                    _vp, _vp]),
     # native ADI outer loop
     "sad_adi_run": (_c.c_int, [_vp, _vp, _c.c_int, _c.c_int, _i64, _i64, _vp, _vp, _vp, _vp,
                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -231,8 +231,9 @@ static __device__ void bi_finish_spmm(const BState& st, int K, const double* tot
 // NQ doubles per column; partial layout [block][NQ][R].  Returns true in the
 // last block to arrive, with the totals in tot_s[NQ * R] (block order: fixed).
 template <int R, int NQ>
-__device__ __forceinline__ bool bi_reduce(const BState& st, const double (&q)[NQ], int grp, int c,
-                                          bool lane_ok, double* tot_s) {
+__device__ __forceinline__ bool part_reduce(double* part, int pstride, unsigned* ticket,
+                                            const double (&q)[NQ], int grp, int c, bool lane_ok,
+                                            double* tot_s) {
   __shared__ double s_q[kWarps][NQ][8];
   const int warp = threadIdx.x >> 5;
 #pragma unroll
@@ -245,9 +246,9 @@ __device__ __forceinline__ bool bi_reduce(const BState& st, const double (&q)[NQ
     const int k = threadIdx.x / R, cc = threadIdx.x - k * R;
     double t = 0.0;
     for (int w = 0; w < kWarps; ++w) t += s_q[w][k][cc];
-    st.part[(size_t)blockIdx.x * st.pstride + threadIdx.x] = t;
+    part[(size_t)blockIdx.x * pstride + threadIdx.x] = t;
   }
-  if (!last_block(st.ticket)) return false;
+  if (!last_block(ticket)) return false;
   // all outputs together, 8 at a time: each thread sums its strided blocks for
   // 8 outputs (independent loads in flight), then one shared-memory tree for the
   // 8 (fixed order: deterministic)
@@ -258,7 +259,7 @@ __device__ __forceinline__ bool bi_reduce(const BState& st, const double (&q)[NQ
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.0;
     for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) {
-      const double* pb = st.part + (size_t)b * st.pstride + o0;
+      const double* pb = part + (size_t)b * pstride + o0;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         if (k < no) acc[k] += __ldcg(pb + k);
@@ -278,6 +279,12 @@ __device__ __forceinline__ bool bi_reduce(const BState& st, const double (&q)[NQ
   }
   __syncthreads();
   return true;
+}
+
+template <int R, int NQ>
+__device__ __forceinline__ bool bi_reduce(const BState& st, const double (&q)[NQ], int grp, int c,
+                                          bool lane_ok, double* tot_s) {
+  return part_reduce<R, NQ>(st.part, st.pstride, st.ticket, q, grp, c, lane_ok, tot_s);
 }
 
 // ---- elementwise kernels ------------------------------------------------------

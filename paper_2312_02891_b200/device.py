@@ -293,6 +293,50 @@ class BicgWorkspace:
             self.handle = None
 
 
+class MinresWorkspace:
+    """Device MINRES (the reference's inner solver for Hermitian sides,
+    krylov.py:187-287) on n x r blocks: seven n x r work blocks plus per-column
+    scalars.  Real shifts only (adi.py:468-472)."""
+
+    def __init__(self, n, r, dtype, device=0):
+        self.n, self.r, self.dtype = n, r, dtype
+        self._ctx = _lib.context(device)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().sad_minres_create(self._ctx, n, r, dtype, ctypes.byref(h)),
+                   self._ctx)
+        self.handle = h
+
+    def set_option(self, key, value):
+        """GMRES engine options do not apply."""
+
+    @property
+    def nbytes(self):
+        return int(_lib.load().sad_minres_bytes(self.handle))
+
+    def solve(self, op, rhs, x, res, tol_col, maxit, stream=None):
+        """Returns (iterations int64[r], residual norms float64[r], converged bool[r])."""
+        r = self.r
+        iters = np.zeros(r, dtype=np.int64)
+        norms = np.zeros(r, dtype=np.float64)
+        conv = np.zeros(r, dtype=np.uint8)
+        rc = _lib.load().sad_minres_solve(
+            self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
+            None if res is None else res.data_ptr(), float(tol_col), int(maxit),
+            current_stream_handle(stream), iters.ctypes.data, norms.ctypes.data,
+            conv.ctypes.data)
+        _lib.check(rc, self._ctx)
+        return iters, norms, conv.astype(bool)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.load().sad_minres_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
 def gram(x, y=None, device=0, stream=None):
     """X^H Y (r x r complex numpy) of two device blocks."""
     import torch

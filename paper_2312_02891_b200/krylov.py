@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .device import (BicgWorkspace, DeviceMatrix, DeviceOperator, GmresWorkspace, gram,
+from .device import (BicgWorkspace, DeviceMatrix, MinresWorkspace, DeviceOperator, GmresWorkspace, gram,
                      sigma_max_from_gram)
 
 MAX_BLOCK = 8   # columns per device solve; wider blocks are split (columns are independent)
@@ -119,6 +119,22 @@ def validate_request(n, rhs, abs_tolerance):
 PHASE_A = {"auto": -1, "tma": 0, "direct": 1}
 
 
+SOLVERS = ("gmres", "bicgstab", "minres", "reference")
+
+
+def _side_symmetric(mat, tol=1e-12):
+    """adi.py:413-419 on a host matrix (DeviceMatrix: its recorded flag)."""
+    if isinstance(mat, DeviceMatrix):
+        return bool(getattr(mat, "symmetric", False))
+    import scipy.sparse as sp
+    csr = sp.csr_matrix(mat.scipy() if hasattr(mat, "scipy") else mat)
+    diff = (csr - csr.T).tocoo()
+    if diff.nnz == 0:
+        return True
+    scale = max(np.abs(csr.data).max(initial=0.0), 1.0)
+    return np.abs(diff.data).max(initial=0.0) <= tol * scale
+
+
 class GpuGmresBinding:
     """Per-side GPU inner solver with shift-keyed operator cache (adi.py:422-488).
 
@@ -140,8 +156,8 @@ class GpuGmresBinding:
         if precond_kind not in ("none", "jacobi"):
             raise ValueError(f"preconditioner {precond_kind!r} is not available on the GPU "
                              "path (supported: none, jacobi)")
-        if solver not in ("gmres", "bicgstab"):
-            raise ValueError("solver must be 'gmres' or 'bicgstab'")
+        if solver not in SOLVERS:
+            raise ValueError(f"solver must be one of {SOLVERS}")
         self.solver = solver
         self.side = side
         self.mode = mode
@@ -157,6 +173,11 @@ class GpuGmresBinding:
             raise ValueError(f"phase_a must be one of {sorted(PHASE_A)}")
         self.phase_a = phase_a
         adjoint = (side == "B")
+        # solver="reference": the reference's own dispatch (adi.py:468-488),
+        # MINRES for a symmetric side at a real shift, BiCGstab otherwise
+        self.symmetric = False
+        if solver == "reference":
+            self.symmetric = _side_symmetric(base) and (mass is None or _side_symmetric(mass))
         self.base = base if isinstance(base, DeviceMatrix) else DeviceMatrix(base, adjoint, device)
         self.mass = (None if mass is None else
                      mass if isinstance(mass, DeviceMatrix) else DeviceMatrix(mass, adjoint, device))
@@ -182,12 +203,28 @@ class GpuGmresBinding:
             self._operators[shift] = op
         return op
 
-    def workspace(self, r, dtype):
-        key = (r, dtype)
+    def uses_minres(self, shift):
+        """adi.py:468-472 (mode is always "iterative" here)."""
+        if self.solver == "minres":
+            return True
+        return (self.solver == "reference" and self.symmetric
+                and complex(shift).imag == 0.0 and self.precond_kind in ("none", "jacobi"))
+
+    def kind_for(self, shift):
+        """The inner algorithm a solve at ``shift`` runs."""
+        if self.solver in ("gmres", "bicgstab", "minres"):
+            return self.solver
+        return "minres" if self.uses_minres(shift) else "bicgstab"
+
+    def workspace(self, r, dtype, kind=None):
+        kind = self.solver if kind is None else kind
+        key = (kind, r, dtype)
         ws = self._workspaces.get(key)
         if ws is None:
-            if self.solver == "bicgstab":
+            if kind == "bicgstab":
                 ws = BicgWorkspace(self.n, r, dtype, self.device)
+            elif kind == "minres":
+                ws = MinresWorkspace(self.n, r, dtype, self.device)
             else:
                 ws = _POOL.take((self.device, self.n, r, dtype, self.restart, self.flexible,
                                  self.engine, self.max_sms))
@@ -234,7 +271,7 @@ class GpuGmresBinding:
                 b_ = rhs[:, c0:c1].contiguous()
                 x_ = torch.empty_like(b_)
                 res_ = torch.empty_like(b_)
-            ws = self.workspace(width, dtype)
+            ws = self.workspace(width, dtype, self.kind_for(shift))
             if fixed_steps is not None and self.solver != "gmres":
                 raise ValueError("fixed_steps applies to GMRES only")
             if fixed_steps is None:

@@ -190,3 +190,57 @@ def test_true_residual_norm_matches_reference(name):
     got = orc.true_residual_norm(A, B, f, g, gold["Z"], gold["Y"], gold["gdiag"], M=M, C=C)
     want = float(gold["true_residual_norm"])
     assert abs(got - want) <= 1e-9 * want, (got, want)
+
+
+# -- MINRES (krylov.py:187-287), pinned to the reference's own outputs -----------
+
+MINRES_CASES = [("def_jac", None, False, "jacobi"), ("indef_jac", None, False, "jacobi"),
+                ("def_none_c", None, False, "none"), ("adj_cap", None, True, "jacobi"),
+                ("pencil_jac", "pencil_mass", False, "jacobi")]
+
+
+@pytest.mark.parametrize("name,mass,adjoint,precond", MINRES_CASES)
+def test_oracle_minres_matches_reference(name, mass, adjoint, precond):
+    """The restated MINRES reproduces the reference's krylov.minres on the
+    fixtures of tests/golden/make_golden_minres.py bit for bit: same iteration
+    counts, same solutions."""
+    d = np.load(os.path.join(GOLD, "ref_minres.npz"))
+    A = sp.csr_matrix(d["lap_A24"])
+    M = None if mass is None else sp.csr_matrix(d[mass])
+    op = orc.ShiftedOp(A, M, complex(d[name + "_shift"][0]), adjoint=adjoint)
+    dinv = orc.jacobi_dinv(op) if precond == "jacobi" else None
+    res = orc.minres(op, d[name + "_b"], float(d[name + "_delta"][0]),
+                     int(d[name + "_maxit"][0]), dinv)
+    assert np.array_equal(res.iterations, d[name + "_iters"])
+    assert np.array_equal(res.converged, d[name + "_conv"])
+    assert np.max(np.abs(res.solution - d[name + "_x"])) <= 1e-14 * np.max(np.abs(d[name + "_x"]))
+
+
+def test_oracle_minres_known_answers(rng):
+    """test_krylov.py:58-98: identity in <= 1 iteration, diagonal negative
+    definite against the dense solve, indefinite 2 x 2 in <= 2 iterations, and
+    the reference's own output on the 50 x 50 diagonal case."""
+    d = np.load(os.path.join(GOLD, "ref_minres.npz"))
+    b = rng.standard_normal((4, 1))
+    res = orc.minres(orc.ShiftedOp(sp.eye(4, format="csr"), None, 0.0), b, 1e-12)
+    assert res.total_iterations <= 1 and np.max(np.abs(res.solution - b)) < 1e-12
+    D = np.diag(-np.arange(1.0, 51.0))
+    res = orc.minres(orc.ShiftedOp(sp.csr_matrix(D), None, 0.0), d["kat_diag_b"], 1e-10)
+    assert np.array_equal(res.iterations, d["kat_diag_iters"])
+    assert np.max(np.abs(res.solution - d["kat_diag_x"])) <= 1e-14
+    res = orc.minres(orc.ShiftedOp(sp.csr_matrix(np.diag([-1.0, 1.0])), None, 0.0),
+                     np.array([[1.0], [1.0]]), 1e-12)
+    assert res.total_iterations <= 2
+    assert np.max(np.abs(res.solution[:, 0] - np.array([-1.0, 1.0]))) < 1e-10
+
+
+def test_oracle_reference_dispatch():
+    """Binding(solver="reference") follows SolverBinding.uses_minres
+    (adi.py:468-472): MINRES for a symmetric side at a real shift, BiCGstab for
+    a complex shift or an unsymmetric side."""
+    d = np.load(os.path.join(GOLD, "ref_minres.npz"))
+    A = sp.csr_matrix(d["lap_A24"])
+    b = orc.Binding("A", A, None, solver="reference")
+    assert b.uses_minres(-10.0) and not b.uses_minres(-10.0 + 1j)
+    U = A + sp.diags(np.ones(A.shape[0] - 1), 1, format="csr")
+    assert not orc.Binding("A", U, None, solver="reference").uses_minres(-10.0)
