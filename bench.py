@@ -116,20 +116,42 @@ class Dist:
 # -- clocks during the timed region ------------------------------------------------
 
 class Clocks:
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    Default: NVML queried in-process from a sampler thread (two light queries
+    per sample; an nvidia-smi query takes the driver lock and stalled config-2
+    steps by 20-50 ms).  SAD_CLOCKS=smi uses the recipe's nvidia-smi -lms loop."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device, period_ms=1000):
-        # one query per second: each nvidia-smi query takes the driver lock and
-        # can stall a latency-bound solve's launches by ~20 ms (config 2 steps
-        # are ~80 ms), so sample sparsely; long configs still get many samples
+    def __init__(self, device, period_ms=None):
         self.device = device
-        self.period_ms = period_ms
+        self.mode = os.environ.get("SAD_CLOCKS", "nvml")
+        self.period_ms = period_ms or (200 if self.mode == "nvml" else 1000)
         self.proc = None
+        self.thread = None
         self.lines = []
+        self.samples = []          # (sm_mhz, sm_max_mhz, set(reasons))
+        self._stop = threading.Event()
 
     def start(self):
+        if self.mode == "nvml":
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                idx = self.device
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                if vis:
+                    idx = int(vis.split(",")[self.device])
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+                self._nv = pynvml
+                self.thread = threading.Thread(target=self._poll, daemon=True)
+                self.thread.start()
+                return
+            except Exception:
+                self.mode = "smi"
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -140,11 +162,34 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self._nv, self._h
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+                "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(smax),
+                                     {k for k, b in bits.items() if mask & b}))
+            except Exception:
+                pass
+            self._stop.wait(self.period_ms / 1000.0)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.mode == "nvml" and self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            sm = [x[0] for x in self.samples]
+            reasons = set().union(*[x[2] for x in self.samples]) if self.samples else set()
+            smax = self.samples[-1][1] if self.samples else None
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -154,7 +199,6 @@ class Clocks:
             self.proc.kill()
         self.thread.join(timeout=2)
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
@@ -164,11 +208,11 @@ class Clocks:
                 smax = float(parts[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[2:6]):
+            for nm, v in zip(self.NAMES, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # -- workloads ------------------------------------------------------------------------

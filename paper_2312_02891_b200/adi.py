@@ -841,6 +841,9 @@ def _run_device(problem, config, shifts, restart, flexible, device, concurrent,
                     device=device, concurrent=concurrent, engine=engine, solver=solver)
     t1 = time.perf_counter()
     sol, rep, state = eng.run()
+    for b in (eng.bA, eng.bB):      # workspaces back to the pool before the next run
+        if hasattr(b, "release"):
+            b.release()
     t2 = time.perf_counter()
     if not keep_on_device:
         state.Z, state.Y = sol.Z, sol.Y

@@ -232,11 +232,16 @@ class GpuGmresBinding:
         ws.set_option(_lib.SAD_OPT_DIRECT_A, PHASE_A[self.phase_a])
         return ws
 
-    def __del__(self):
+    def release(self):
+        """Return the Krylov workspaces to the shared pool now (the next
+        binding of the same shape reuses them without a device allocation)."""
         for ws in getattr(self, "_workspaces", {}).values():
             if isinstance(ws, GmresWorkspace):
                 _POOL.give(ws)
         self._workspaces = {}
+
+    def __del__(self):
+        self.release()
 
     # -- solves -------------------------------------------------------------
     def solve_device(self, shift, rhs, delta, x=None, res=None, stream=None,

@@ -30,6 +30,7 @@ BASE = {"problem": {"dimension": 2, "n0_A": 8, "n0_B": 6, "r": 1, "seed": 0},
     {k: v for k, v in BASE.items() if k != "output_dir"},
     {**BASE, "problem": {"files": {"a": "missing.mtx", "b": "x", "f": "y", "g": "z"}}},
     {**BASE, "shifts": {"file": "missing.json"}},
+    {**BASE, "gpu": {"solver": "ilu-gmres"}},           # unknown inner solver
 ])
 def test_manifest_validation_exit_code(tmp_path, bad):
     path = write(tmp_path, "m.json", bad)

@@ -52,3 +52,20 @@ def test_shifts_subcommand(tmp_path):
     assert cli.main(["shifts", "--a", str(gen / "A.mtx"), "--b", str(gen / "B.mtx"),
                      "--pairs", "4", "--out", str(out)]) == cli.EXIT_OK
     assert len(json.loads(out.read_text())["pairs"]) == 4
+
+
+def test_solve_reference_dispatch_symmetric(tmp_path):
+    """gpu.solver = "reference": the reference's own inner-solver dispatch on
+    a symmetric pair (omega = 0: MINRES on the device at every real shift,
+    BiCGstab otherwise) converges to the outer tolerance through the CLI."""
+    man = {"problem": {"dimension": 2, "n0_A": 16, "n0_B": 12, "r": 1, "seed": 2},
+           "strategies": ["dynamic_mid_bl"], "shifts": {"pairs": 6},
+           "config": {"kmax": 100, "precond_kind_A": "jacobi", "precond_kind_B": "jacobi"},
+           "output_dir": "run", "gpu": {"solver": "reference"}}
+    path = tmp_path / "m.json"
+    path.write_text(json.dumps(man))
+    assert cli.main(["solve", "--manifest", str(path)]) == cli.EXIT_OK
+    summ = json.loads((tmp_path / "run" / "summary.json").read_text())
+    assert summ["inner_solver"] == "gpu reference"
+    e = summ["strategies"]["dynamic_mid_bl"]
+    assert e["converged"] and e["scaled_true_residual"] < 2e-8

@@ -56,3 +56,23 @@ for _ in range(3):
     t4 = time.perf_counter()
     print(f"phases: construct {1e3*(t1-t0):.1f} ms, run {1e3*(t2-t1):.1f} ms, "
           f"Z {1e3*(t3-t2):.1f} ms ({Z.nbytes/1e6:.0f} MB), Y {1e3*(t4-t3):.1f} ms")
+
+# first run of a fresh engine vs a second run of the same (warm) engine
+for _ in range(3):
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
+    eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible)
+    ts = []
+    for _k in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sol, rep, st = eng.run()
+        torch.cuda.synchronize()
+        ts.append(1e3 * (time.perf_counter() - t0))
+    print("fresh engine runs (ms):", [round(x, 1) for x in ts])
+pr = cProfile.Profile()
+prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
+eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible)
+pr.enable()
+eng.run()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(15)
