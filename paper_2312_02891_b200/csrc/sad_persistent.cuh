@@ -271,6 +271,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
 
   __shared__ double s_w2[kWarps][8];
   __shared__ int s_any;
+  __shared__ double s_Sj[8];     // S_{j+1} of the step just finished (block copy)
+  const int cbase = 2 * (m + 1) * R;   // phase-C partial slots (after phase A's)
   // phase-A TMA ring
   __shared__ __align__(8) unsigned long long s_full[kStages];
   __shared__ int s_soff[kStages];
@@ -390,15 +392,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
     __syncthreads();
     if (!s_any) break;
     // ---------------- Arnoldi steps ----------------
+    // j and S_j of the first step of a cycle come from global state (written
+    // before a full barrier); later steps use the block's own copies
+    int jl = -1;
     while (true) {
-      const int j = ldcgi(gs.j);
+      const int j = jl >= 0 ? jl : ldcgi(gs.j);
       const int J = j + 1;
       if (timing) tphase = gtimer();
       // ======== phase A: SpMM + h_raw + delayed Gram column ========
       {
         const XT* vj = a.V + (long long)j * a.stride;
         XT* w = a.V + (long long)J * a.stride;
-        const double sj = lane_ok ? ldcg1(gs.S + j * R + c) : 0.0;
+        const double sj = !lane_ok ? 0.0 : (jl >= 0 ? s_Sj[c] : ldcg1(gs.S + j * R + c));
         // The basis is streamed through a ring of TMA stages (one stage = the
         // tile's rows of one basis block); per basis block the block reduces its
         // h / g contributions through shared memory in a fixed order.
@@ -853,13 +858,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         if (threadIdx.x < R) {
           double t = 0.0;
           for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
-          put(threadIdx.x, make_double2(t, 0.0));
+          // phase-C sums in their own slots (cbase..): blocks that run ahead
+          // into the next phase A overwrite slots 0.. only
+          put(cbase + threadIdx.x, make_double2(t, 0.0));
         }
         if (timing && prof) t_acc[5] += (double)(gtimer() - tphase);
-        if (bar_arrive(st, gen)) {
-          const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
-          // per-column scalars, loaded together and before the reduction (one
-          // round trip overlapping it)
+        // Every block waits for all partials and then forms the step's Givens
+        // rotation itself (same fixed-order reduction everywhere, so every block
+        // gets bit-identical values): no serial finisher between the arrival of
+        // the last block and the release.  Block 0 alone writes the global
+        // state; the other blocks keep what the next step needs (j, S_{j+1},
+        // whether the cycle goes on) in shared memory.
+        if (bar_arrive(st, gen)) bar_release(st);
+        else bar_wait(st, gen);
+        {
+          const bool w0 = blockIdx.x == 0;
+          const unsigned long long tfin = (prof && w0 && threadIdx.x == 0) ? gtimer() : 0ull;
           __shared__ int s_actn[8];
           __shared__ double2 s_nrm[8];
           int act_c = 0;
@@ -874,83 +888,92 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             gj_c = ldcg2(gs.g + (size_t)cc * (m + 1) + j);
             hjj = ldcg2(st.hc + j * R + cc);
           }
-          reduce_partials_small(partT, pT, gridDim.x, R, s_nrm);
+          reduce_partials_small(partT + (size_t)cbase * pT, pT, gridDim.x, R, s_nrm);
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
             s_actn[cc] = 0;
+            double snext = 0.0;
             if (act_c) {
               const double hn = sqrt(s_nrm[cc].x);
               double cj; double2 sjv, rj;
               givens(hjj, make_double2(hn, 0.0), cj, sjv, rj);
-              gs.cs[(size_t)cc * m + j] = cj;
-              gs.sn[(size_t)cc * m + j] = sjv;
-              double2* col = gs.H + ((size_t)cc * m + j) * (m + 1);
-              col[j] = rj;
-              col[j + 1] = make_double2(0.0, 0.0);
-              double2* gv = gs.g + (size_t)cc * (m + 1);
               const double2 gn = mul(cconj(sjv), gj_c);
               const double2 gnext = make_double2(-gn.x, -gn.y);
-              gv[j + 1] = gnext;
-              gv[j] = scal(cj, gj_c);
               const long long it = it_c + 1;
-              gs.iters[cc] = it;
-              gs.kdim[cc] = j + 1;
               const double est = cabs_(gnext);
-              gs.S[(j + 1) * R + cc] = hn > 0.0 ? 1.0 / hn : 0.0;
+              snext = hn > 0.0 ? 1.0 / hn : 0.0;
               bool end = (j + 1 == m) || it >= gs.maxit;
               if (!gs.fixed) end = end || est <= gs.tol || hn <= kLucky * sqrt(wpre_c);
-              if (end) gs.active[cc] = 0;
+              if (w0) {
+                gs.cs[(size_t)cc * m + j] = cj;
+                gs.sn[(size_t)cc * m + j] = sjv;
+                double2* col = gs.H + ((size_t)cc * m + j) * (m + 1);
+                col[j] = rj;
+                col[j + 1] = make_double2(0.0, 0.0);
+                double2* gv = gs.g + (size_t)cc * (m + 1);
+                gv[j + 1] = gnext;
+                gv[j] = scal(cj, gj_c);
+                gs.iters[cc] = it;
+                gs.kdim[cc] = j + 1;
+                gs.S[(j + 1) * R + cc] = snext;
+                if (end) gs.active[cc] = 0;
+              }
               s_actn[cc] = end ? 0 : 1;
-            } else {
+            } else if (w0) {
               gs.S[(j + 1) * R + cc] = 0.0;
             }
+            s_Sj[cc] = snext;
           }
           __syncthreads();
           int any_now = 0;
           for (int cc = 0; cc < R; ++cc) any_now |= s_actn[cc];
-          if (threadIdx.x == 0) {
+          if (w0 && threadIdx.x == 0) {
             *gs.any_active = any_now;
             *gs.j = j + 1;
           }
-          __syncthreads();
           if (any_now == 0) {
-            // cycle end: back substitution, one warp per column (lanes split the
-            // inner products; fixed shuffle tree)
-            for (int cc = warp; cc < R; cc += kWarps) {
-              const int k = gs.kdim[cc];
-              const double2* Hc = gs.H + (size_t)cc * m * (m + 1);
-              const double2* gv = gs.g + (size_t)cc * (m + 1);
-              double2* yv = reinterpret_cast<double2*>(smem_p) + (size_t)warp * m;
-              for (int ii = k - 1; ii >= 0; --ii) {
-                double2 part = make_double2(0.0, 0.0);
-                for (int l = ii + 1 + lane; l < k; l += 32)
-                  part = add(part, mul(Hc[(size_t)l * (m + 1) + ii], yv[l]));
+            if (w0) {
+              __syncthreads();   // block 0's state writes above, visible to its own threads
+              // cycle end: back substitution, one warp per column (lanes split the
+              // inner products; fixed shuffle tree)
+              for (int cc = warp; cc < R; cc += kWarps) {
+                const int k = gs.kdim[cc];
+                const double2* Hc = gs.H + (size_t)cc * m * (m + 1);
+                const double2* gv = gs.g + (size_t)cc * (m + 1);
+                double2* yv = reinterpret_cast<double2*>(smem_p) + (size_t)warp * m;
+                for (int ii = k - 1; ii >= 0; --ii) {
+                  double2 part = make_double2(0.0, 0.0);
+                  for (int l = ii + 1 + lane; l < k; l += 32)
+                    part = add(part, mul(Hc[(size_t)l * (m + 1) + ii], yv[l]));
 #pragma unroll
-                for (int sh = 16; sh > 0; sh >>= 1) part = add(part, shfl_down(part, sh));
-                if (lane == 0) yv[ii] = cdiv(sub(gv[ii], part), Hc[(size_t)ii * (m + 1) + ii]);
+                  for (int sh = 16; sh > 0; sh >>= 1) part = add(part, shfl_down(part, sh));
+                  if (lane == 0) yv[ii] = cdiv(sub(gv[ii], part), Hc[(size_t)ii * (m + 1) + ii]);
+                  __syncwarp();
+                }
+                for (int ii = lane; ii < m; ii += 32) {
+                  double2 y = ii < k ? yv[ii] : make_double2(0.0, 0.0);
+                  if (!FLEX && ii < k) {
+                    const double sc = gs.S[ii * R + cc];
+                    y = sc == 0.0 ? make_double2(0.0, 0.0) : make_double2(sc * y.x, sc * y.y);
+                  }
+                  gs.ycoef[ii * R + cc] = y;
+                }
                 __syncwarp();
               }
-              for (int ii = lane; ii < m; ii += 32) {
-                double2 y = ii < k ? yv[ii] : make_double2(0.0, 0.0);
-                if (!FLEX && ii < k) {
-                  const double sc = gs.S[ii * R + cc];
-                  y = sc == 0.0 ? make_double2(0.0, 0.0) : make_double2(sc * y.x, sc * y.y);
-                }
-                gs.ycoef[ii * R + cc] = y;
+              __syncthreads();
+              if (threadIdx.x == 0) {
+                int jx = 0;
+                for (int cc = 0; cc < R; ++cc) jx = max(jx, gs.kdim[cc]);
+                *gs.jx = jx;
               }
-              __syncwarp();
             }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-              int jx = 0;
-              for (int cc = 0; cc < R; ++cc) jx = max(jx, gs.kdim[cc]);
-              *gs.jx = jx;
-            }
+            // everyone waits for block 0's back substitution
+            if (bar_arrive(st, gen)) bar_release(st);
+            else bar_wait(st, gen);
           }
-          if (prof && threadIdx.x == 0) atomicAdd(st.stats + 11, (double)(gtimer() - tfin));
-          bar_release(st);
-        } else {
-          bar_wait(st, gen);
+          if (prof && w0 && threadIdx.x == 0) atomicAdd(st.stats + 11, (double)(gtimer() - tfin));
+          if (threadIdx.x == 0) s_any = any_now;
+          jl = j + 1;
         }
       }
       if (timing) {
@@ -962,7 +985,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         acc_steps += 1.0;
         acc_bytes += st.spmm_bytes_arn + (2.0 * J + 2.0) * (double)a.stride * sizeof(XT);
       }
-      if (threadIdx.x == 0) s_any = ldcgi(gs.any_active);
       __syncthreads();
       if (!s_any) break;
     }
