@@ -1157,6 +1157,16 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t vsz = op->vals_complex ? 16 : 8;
   const size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
                                                   (size_t)kStagesA1 * a1_stage_bytes((int)R, vsz));
+  // large-slab basis sweep: by basis block with direct loads for complex128
+  // blocks (config 3: sweep 228 -> 221 us per A-side step, solve -3 %), through
+  // the TMA ring for fp64 (config 4: the ring is 6 % faster);
+  // SAD_SWEEP=direct|tma overrides (A/B experiments)
+  static const int sweep_env = [] {
+    const char* e = getenv("SAD_SWEEP");
+    if (!e) return -1;
+    return std::string(e) == "tma" ? 0 : 1;
+  }();
+  const int sweep_direct = sweep_env >= 0 ? sweep_env : (ws->dtype == SAD_C128 ? 1 : 0);
   size_t smem = std::max({ring_bytes + sums,                              // rings + sums
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
@@ -1179,6 +1189,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.ring_bytes = (int)ring_bytes;
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
+    a.sweep_direct = sweep_direct;
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
@@ -1189,6 +1200,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.ring_bytes = (int)ring_bytes;
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
+    a.sweep_direct = sweep_direct;
     e = coop_dispatch_z(a, ws, op, s, smem);
   }
   if (e != cudaSuccess)

@@ -83,6 +83,7 @@ struct PArgs {
   int ring_bytes;        // dynamic-smem bytes of the phase-A rings (basis / A1 CSR)
   int csr_off;           // dynamic-smem byte offset of the resident CSR slab
   int csr_budget;        // bytes available there (0 = CSR read from global)
+  int sweep_direct;      // large slabs: basis sweep by basis block with direct loads (no TMA ring)
   PState st;
 };
 
@@ -604,6 +605,68 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             ring1 += (unsigned long long)ntile;
             if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
           }
+          if (a.sweep_direct) {
+            // Basis sweep split over the warps BY BASIS BLOCK (as the direct
+            // path), w and v_j read back from L2 instead of shared memory: warp
+            // k owns blocks k, k + kWarps, ... (two per pass) and walks all of
+            // the block's rows with KL rows of loads in flight per lane -- no
+            // block-wide synchronisation inside the sweep.
+            __syncthreads();   // A1's writes of w visible to the whole block
+            const int nrows_blk = (int)(r1 - r0);
+            const XT* wg = w + r0 * R;
+            const XT* xg = vj + r0 * R;
+            for (int i = warp; i < J; i += 2 * kWarps) {
+              const int i2 = i + kWarps;
+              const bool two = i2 < J;
+              const XT* Vi = a.V + (long long)i * a.stride + r0 * R;
+              const XT* Vk = a.V + (long long)(two ? i2 : i) * a.stride + r0 * R;
+              XT ph = zero<XT>(), pg = zero<XT>(), ph2 = zero<XT>(), pg2 = zero<XT>();
+              if (lane_ok) {
+                constexpr int KL = sizeof(XT) == 8 ? 8 : 4;
+                int rr = grp;
+                for (; rr + (KL - 1) * GPW < nrows_blk; rr += KL * GPW) {
+                  XT vb[KL], vk[KL], wr[KL], xr[KL];
+#pragma unroll
+                  for (int k = 0; k < KL; ++k) {
+                    const int o = (rr + k * GPW) * R + c;
+                    vb[k] = Vi[o];
+                    vk[k] = two ? Vk[o] : zero<XT>();
+                    wr[k] = wg[o];
+                    xr[k] = xg[o];
+                  }
+#pragma unroll
+                  for (int k = 0; k < KL; ++k) {
+                    ph = cfma(vb[k], wr[k], ph);
+                    pg = cfma(vb[k], xr[k], pg);
+                    ph2 = cfma(vk[k], wr[k], ph2);
+                    pg2 = cfma(vk[k], xr[k], pg2);
+                  }
+                }
+                for (; rr < nrows_blk; rr += GPW) {
+                  const int o = rr * R + c;
+                  const XT v = Vi[o];
+                  const XT v2 = two ? Vk[o] : zero<XT>();
+                  const XT wr = wg[o], xr = xg[o];
+                  ph = cfma(v, wr, ph);
+                  pg = cfma(v, xr, pg);
+                  ph2 = cfma(v2, wr, ph2);
+                  pg2 = cfma(v2, xr, pg2);
+                }
+              }
+              ph = group_reduce<R>(ph, grp);
+              pg = group_reduce<R>(pg, grp);
+              ph2 = group_reduce<R>(ph2, grp);
+              pg2 = group_reduce<R>(pg2, grp);
+              if (grp == 0 && lane_ok) {
+                s_blk[i * R + c] = ph;
+                s_blk[(J + i) * R + c] = pg;
+                if (two) {
+                  s_blk[i2 * R + c] = ph2;
+                  s_blk[(J + i2) * R + c] = pg2;
+                }
+              }
+            }
+          } else
           for (long long base = r0; base < r1; base += T) {
             const long long nrows = min((long long)T, r1 - base);
             auto issue = [&](int i, int q) {
