@@ -31,7 +31,13 @@ namespace sad {
 
 constexpr int kStages = 4;   // phase-A TMA ring depth
 constexpr int kGroup = 2;    // basis blocks reduced per __syncthreads (kStages = 2 * kGroup)
-constexpr int kStagesA1 = 3; // staged-SpMM (sub-phase A1) CSR ring depth
+#ifndef SAD_KSTAGES_A1
+#define SAD_KSTAGES_A1 3
+#endif
+#ifndef SAD_KB1
+#define SAD_KB1 5
+#endif
+constexpr int kStagesA1 = SAD_KSTAGES_A1; // staged-SpMM (sub-phase A1) CSR ring depth
 
 // Sub-phase A1 (large slabs): CSR tiles of kWarps * (32 / R) rows -- one row per
 // lane group -- staged by TMA; up to 12 nonzeros per row are staged, denser
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                 const long long id = row * R + c;
                 const int k0 = rp[lr], k1 = rp[lr + 1];
                 XT acc = zero<XT>();
-                constexpr int KB1 = 5;
+                constexpr int KB1 = SAD_KB1;   // gathers in flight per row
                 for (int k = k0; k < k1; k += KB1) {
                   XT xg[KB1];
 #pragma unroll
