@@ -17,7 +17,8 @@ prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g)
 cfg = pb.AdiConfig(strategy=spec.strategy, kmax=spec.kmax, precond_kind_A="jacobi",
                    precond_kind_B="jacobi")
 seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
-for split in (None, 0.85):
+SPLITS = [None if x == "none" else float(x) for x in os.environ.get("SPLITS", "none,0.85").split(",")]
+for split in SPLITS:
     eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                        sm_split=split)
     eng.warm()
