@@ -527,10 +527,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             constexpr size_t SB1 = a1_stage_bytes(R, sizeof(VT));
             const VT* vals_g = reinterpret_cast<const VT*>(a.vals);
             const long long ntile = (r1 - r0 + T1 - 1) / T1;
-            auto issue1 = [&](long long t, int q) {
+            // kb/ke of the tile to issue: loaded by the issuing thread one tile
+            // ahead (pkb/pke) so the issue at the end of a tile does not wait
+            // on a global round trip while the rest of the block is at the
+            // tile's __syncthreads
+            auto issue1 = [&](long long t, int q, int kb, int ke) {
               const long long row0 = r0 + t * T1;
               const int rows = (int)min((long long)T1, r1 - row0);
-              const int kb = __ldg(a.rowptr + row0), ke = __ldg(a.rowptr + row0 + rows);
               const int nz = ke - kb;
               unsigned long long p0, p1, c0 = 0, c1 = 0, v0 = 0, v1 = 0;
               aligned_range(a.rowptr, row0, rows + 1, 4, p0, p1);
@@ -558,12 +561,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             };
             if (threadIdx.x == 0) {
               fence_proxy_async();
-              for (long long t = 0; t < min((long long)kStagesA1, ntile); ++t)
-                issue1(t, (int)((ring1 + t) % kStagesA1));
+              for (long long t = 0; t < min((long long)kStagesA1, ntile); ++t) {
+                const long long row0 = r0 + t * T1;
+                const int rows = (int)min((long long)T1, r1 - row0);
+                issue1(t, (int)((ring1 + t) % kStagesA1), __ldg(a.rowptr + row0),
+                       __ldg(a.rowptr + row0 + rows));
+              }
             }
             for (long long t = 0; t < ntile; ++t) {
               const unsigned long long kk = ring1 + t;
               const int q = (int)(kk % kStagesA1);
+              // (fp64 blocks only: config 4 -2 %; the complex128 variant is at
+              // its register cap and its SpMM got 17 % slower with the prefetch)
+              constexpr bool PF = sizeof(XT) == 8;
+              int pkb = 0, pke = 0;
+              if (PF && threadIdx.x == 0 && t + kStagesA1 < ntile) {
+                const long long row0n = r0 + (t + kStagesA1) * T1;
+                const int rowsn = (int)min((long long)T1, r1 - row0n);
+                pkb = __ldg(a.rowptr + row0n);
+                pke = __ldg(a.rowptr + row0n + rowsn);
+              }
               mbar_wait(s_full1 + q, (unsigned)((kk / kStagesA1) & 1));
               const long long row0 = r0 + t * T1;
               const int lr = warp * GPW + grp;
@@ -605,7 +622,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               __syncthreads();   // stage q consumed
               if (threadIdx.x == 0 && t + kStagesA1 < ntile) {
                 fence_proxy_async();
-                issue1(t + kStagesA1, q);
+                if (!PF) {
+                  const long long row0n = r0 + (t + kStagesA1) * T1;
+                  const int rowsn = (int)min((long long)T1, r1 - row0n);
+                  pkb = __ldg(a.rowptr + row0n);
+                  pke = __ldg(a.rowptr + row0n + rowsn);
+                }
+                issue1(t + kStagesA1, q, pkb, pke);
               }
             }
             ring1 += (unsigned long long)ntile;
