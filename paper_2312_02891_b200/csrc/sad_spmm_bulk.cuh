@@ -138,10 +138,12 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
     if (lane == 0) {
       for (long long k = 0; k < K; ++k) {
         const int st = (int)(k % S);
-        if (k >= S) mbar_wait(empty + st, (unsigned)(((k / S) - 1) & 1));
+        // the tile's row range is loaded before waiting for the free stage, so
+        // its global round trip overlaps the consumers' work
         const long long r0 = (blockIdx.x + k * G) * (long long)TR;
         const int rows = (int)min((long long)TR, a.n - r0);
         const int kb = __ldg(a.rowptr + r0), ke = __ldg(a.rowptr + r0 + rows);
+        if (k >= S) mbar_wait(empty + st, (unsigned)(((k / S) - 1) & 1));
         const int nz = ke - kb;
         unsigned long long p0, p1, c0, c1, v0, v1;
         aligned_range(a.rowptr, r0, rows + 1, 4, p0, p1);
