@@ -491,7 +491,10 @@ def run_ours_c2(args, dist, name="c2"):
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "phases_ms": {k: statistics.mean(d.get(k, 0.0) for d in e2e_solve)
-                              for k in ("construct_ms", "run_ms", "download_ms")}},
+                              for k in ("construct_ms", "run_ms", "download_ms")},
+                "step_s": [round(x, 4) for x in e2e_times],
+                "step_phases_ms": [{k: round(d.get(k, 0.0), 1) for k in
+                                    ("construct_ms", "run_ms", "download_ms")} for d in e2e_solve]},
         "gpu_launches": int(launches),
         "clocks": ck,
         "step_ms": step_ms,
