@@ -433,7 +433,7 @@ def is_symmetric(matrix, tol=1e-12):
     if diff.nnz == 0:
         return True
     scale = max(np.abs(csr.data).max(initial=0.0), 1.0)
-    return np.abs(diff.data).max(initial=0.0) <= tol * scale
+    return bool(np.abs(diff.data).max(initial=0.0) <= tol * scale)
 
 
 def _check_request(op, rhs, abs_tolerance):

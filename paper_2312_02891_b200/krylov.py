@@ -132,7 +132,7 @@ def _side_symmetric(mat, tol=1e-12):
     if diff.nnz == 0:
         return True
     scale = max(np.abs(csr.data).max(initial=0.0), 1.0)
-    return np.abs(diff.data).max(initial=0.0) <= tol * scale
+    return bool(np.abs(diff.data).max(initial=0.0) <= tol * scale)
 
 
 class GpuGmresBinding:
