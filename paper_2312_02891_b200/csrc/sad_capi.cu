@@ -1157,16 +1157,17 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t vsz = op->vals_complex ? 16 : 8;
   const size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
                                                   (size_t)kStagesA1 * a1_stage_bytes((int)R, vsz));
-  // large-slab basis sweep: by basis block with direct loads for complex128
-  // blocks (config 3: sweep 228 -> 221 us per A-side step, solve -3 %), through
-  // the TMA ring for fp64 (config 4: the ring is 6 % faster);
+  // large-slab basis sweep: by basis block with direct loads when the block
+  // width does not divide the warp (R = 3: config 3 sweep 228 -> 221 us per
+  // A-side step, solve -3 %), through the TMA ring otherwise (config 4, R = 8:
+  // the ring is 6 % faster; config 5, R = 4 complex: 48.4 s vs 49.8 s);
   // SAD_SWEEP=direct|tma overrides (A/B experiments)
   static const int sweep_env = [] {
     const char* e = getenv("SAD_SWEEP");
     if (!e) return -1;
     return std::string(e) == "tma" ? 0 : 1;
   }();
-  const int sweep_direct = sweep_env >= 0 ? sweep_env : (ws->dtype == SAD_C128 ? 1 : 0);
+  const int sweep_direct = sweep_env >= 0 ? sweep_env : ((32 % ws->R) != 0 ? 1 : 0);
   size_t smem = std::max({ring_bytes + sums,                              // rings + sums
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
