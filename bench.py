@@ -1,28 +1,32 @@
 #!/usr/bin/env python
 """bench.py -- headline benchmark of the B200 inner-solve hot path.
 
-Default workload (BASELINE.json configs[1], "config 2"): inexact low-rank ADI
-on the 3-D convection-diffusion pair n=64,000 / m=27,000, r=2, complex128,
-pinned reference heuristic shifts (npairs=12), Jacobi-FGMRES(30) inner solves
-with the paper's dynamic inner tolerance (dynamic_mid_bl), outer tolerance
-1e-8.  One "step" = one full ADI solve to the 1e-8 residual.
+Default workload (BASELINE.json configs[3], "config 4", the configuration the
+metric "inner SpMM GB/s vs HBM peak" is quoted on): the shifted SpMM
+y = (A + alpha I) x of the inner solves on a 2-D 5-point convection-diffusion
+operator on a 4096^2 grid (16.7M rows, 84M nonzeros) and an r = 8 fp64 block.
+One "step" = one shifted SpMM over the whole block.
 
-  metric  = "wall time to 1e-8 ADI residual" (s, lower is better)
-  value   = device-resident solve, inputs already in HBM
-  e2e     = the public API call run(problem, config, shifts) with host
-            scipy/numpy inputs: uploads, solve and the Z/Y download inside
-  roofline= the dominant kernel class, from a CUDA-event-instrumented pass
-  cpu_baseline = the reference's own CPU path (Jacobi-BiCGstab ADI, restated
-            in oracle/) on the host, rank 0, N=1
+  metric  = "inner SpMM GB/s" (algorithmic bytes / time, higher is better)
+  value   = device-resident SpMM (k_spmm_bulk), CUDA events, L2 flushed
+  e2e     = the same SpMM through the host-buffer C-ABI call
+            (DeviceOperator.apply_host -> sad_op_apply_host): pinned host x in,
+            host y out, transfers inside the timed region
+  roofline= k_spmm_bulk against the measured HBM copy bandwidth
+  inner_solve = 100 fixed Jacobi-GMRES steps in one persistent launch
+            (orthogonalisation GB/s, iterations/s)
+  config3_wall_time = config 3's 1-GPU wall time to the 1e-8 ADI residual
+  cpu_baseline = the reference's ShiftedOperator.apply (oracle/ restatement)
+            on all host threads, rank 0, N=1
 
-`--impl reference` times that CPU path alone (the reference arm).
-`--config c4` runs the inner-solve microbenchmark (SpMM/orthogonalisation GB/s).
-Multi-GPU (torchrun): config 2 is single-GPU in BASELINE.json, so N ranks run
-N independent replicas ("replicas only", weak scaling); value = max over ranks.
-Configs 3/5 at N GPUs: A side on ranks [0, N/2), B side on [N/2, N), a side on
-several GPUs row-partitioned (NCCL halo exchange + all-reduce); config 4 at N
-GPUs: the operator row-partitioned over all N (strong scaling).  `--rowpart`
-forces the row-partitioned path at N = 1.
+`--impl reference` times that CPU apply alone (the reference arm).
+`--config c2|c3|c5` times a whole ADI solve to 1e-8 (wall time, lower is
+better; the reference arm then runs the reference's Jacobi-BiCGstab ADI).
+Multi-GPU (torchrun): config 4 row-partitions the operator over the N ranks
+(NCCL halo exchange; aggregate SpMM GB/s, strong scaling); configs 3/5 put the
+A side on ranks [0, N/2) and the B side on [N/2, N), a side on several GPUs
+row-partitioned; config 2 runs N replicas.  `--rowpart` forces the
+row-partitioned path at N = 1.
 """
 
 import argparse
@@ -521,9 +525,171 @@ def run_ours_c2(args, dist, name="c2"):
     return line if dist.rank == 0 else None
 
 
+C4_WORKLOAD = ("config 4: inner-solve microbenchmark, 2-D 5-point conv-diff 100*(1,1).grad on "
+               "a {n0}^2 grid (n={n}, nnz={nnz}), shifted SpMM y = (A + alpha I) x on an "
+               "r=8 fp64 Gaussian block, alpha = 0.1 * lambda_max (largest-magnitude Ritz "
+               "value, {ritz} Arnoldi steps); plus {steps} fixed Jacobi-GMRES steps")
+
+
+def c4_shift(A, dev, steps=10):
+    """alpha = 0.1 * lambda_max estimate: the largest-magnitude Ritz
+    value of `steps` Arnoldi iterations (shifts.arnoldi_ritz on the device,
+    start vector ones as pencil_ritz_sets, shifts.py:111)."""
+    from paper_2312_02891_b200.device import DeviceMatrix, DeviceOperator
+    from paper_2312_02891_b200.shifts import arnoldi_ritz
+    dm = DeviceMatrix(A, False, dev)
+    op0 = DeviceOperator(dm, None, 0.0, precond_kind="none")
+    ritz = arnoldi_ritz(lambda v: op0.apply(v), np.ones(A.shape[0]), steps, device=dev)
+    lam = complex(ritz.values[np.argmax(np.abs(ritz.values))])
+    del op0, dm
+    return 0.1 * lam.real, lam
+
+
+def c4_pinned_shift(n0):
+    """configs/shift_c4.json (configs/make_shift_c4.py: the reference's own
+    arnoldi_ritz), or None for another grid size."""
+    try:
+        with open(os.path.join(REPO, "configs", "shift_c4.json")) as fh:
+            d = json.load(fh)
+    except OSError:
+        return None
+    if int(d["n0"]) != int(n0):
+        return None
+    return float(d["shift"]), complex(*d["lambda_max"])
+
+
+def c4_spmm_bytes(A, r=8, s=8):
+    """Algorithmic bytes of one shifted SpMM: CSR (values, columns,
+    row offsets) + read x + write y; no Jacobi gather in apply mode."""
+    n = A.shape[0]
+    return A.nnz * 12 + 4 * (n + 1) + 2 * s * r * n
+
+
+def cpu_apply_threads(A, X, shift, threads, reps=1, out=None):
+    """The reference's ShiftedOperator.apply (sparse.py:192-206) on the host:
+    the oracle restatement (oracle/sylvadi_oracle.py ShiftedOp.apply: scipy
+    csr_matvecs, cast to complex, + shift * x) over `threads` row chunks in
+    parallel (scipy's sparsetools and numpy release the GIL).  Returns the
+    seconds of each repetition and the output block."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import sylvadi_oracle as orc
+    n = A.shape[0]
+    nchunk = max(1, 4 * threads)
+    bnd = np.linspace(0, n, nchunk + 1).astype(np.int64)
+    ops = []
+    for i in range(nchunk):
+        r0, r1 = int(bnd[i]), int(bnd[i + 1])
+        # the row slab as a square operator over the slab's rows needs the full
+        # column range: apply the slab of A, then the shift on the slab's rows
+        ops.append((A[r0:r1], r0, r1))
+    if out is None:
+        out = np.empty((n, X.shape[1]), dtype=np.complex128)
+
+    def work(i):
+        Ai, r0, r1 = ops[i]
+        # orc.ShiftedOp(Ai, None, shift).apply would check squareness; the slab
+        # form is the same arithmetic: (A x).astype(complex) + shift * x
+        y = (Ai @ X).astype(complex)
+        y += complex(shift) * X[r0:r1]
+        out[r0:r1] = y
+
+    assert orc.ShiftedOp is not None
+    secs = []
+    with ThreadPoolExecutor(threads) as ex:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            list(ex.map(work, range(nchunk)))
+            secs.append(time.perf_counter() - t0)
+    return secs, out
+
+
+def run_reference_arm_c4(args, dist):
+    """--impl reference, config 4: the reference's CPU shifted SpMM
+    (ShiftedOperator.apply, sparse.py:192-206, via the oracle restatement) on
+    the full config-4 block, all host threads; one full apply per step."""
+    if dist.rank != 0:
+        return None
+    from paper_2312_02891_b200 import configs as cfgs
+    n0 = args.c4_n0
+    A, X = cfgs.build_c4(n0=n0, r=8, seed=0)
+    pinned = c4_pinned_shift(n0)
+    if args.c4_shift is not None:
+        shift = float(args.c4_shift)
+    elif pinned is not None:
+        shift = pinned[0]
+    else:
+        raise SystemExit("config 4 at this grid size needs --c4-shift (the pinned shift is for "
+                         "the 4096^2 grid)")
+    threads = len(os.sched_getaffinity(0))
+    spmm_b = c4_spmm_bytes(A)
+    cpu_apply_threads(A, X, shift, threads, reps=args.warmup)
+    secs, _ = cpu_apply_threads(A, X, shift, threads, reps=args.steps)
+    mean = statistics.mean(secs)
+    value = spmm_b / mean / 1e9
+    n = A.shape[0]
+    return {
+        "metric": "inner SpMM GB/s", "value": value, "unit": "GB/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * mean, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded reference generators)",
+        "config": {"workload": C4_WORKLOAD.format(n0=n0, n=n, nnz=A.nnz, ritz="-", steps=0),
+                   "n": n, "nnz": int(A.nnz), "r": 8, "shift": shift,
+                   "algorithmic_bytes_per_step": spmm_b},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full config-4 applies (16.7M x 8 block) of the "
+                                   f"reference's ShiftedOperator.apply (oracle/ restatement: "
+                                   f"scipy csr_matvecs, complex cast, + shift x) over "
+                                   f"{threads} threads on row chunks; the reference itself "
+                                   f"is single-threaded"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def c3_wall_time(args, dev):
+    """Config 3's 1-GPU wall time to the 1e-8 ADI residual (BASELINE configs[2]):
+    the device-resident solve (one warm-up run, one timed run, CUDA events)."""
+    import torch
+    import paper_2312_02891_b200 as pb
+    spec, prob, cfg, seq, _ = build_c2("c3")
+    eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible, device=dev)
+    eng.warm()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        eng.run()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, rep, _ = eng.run()
+        e1.record()
+        torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1000.0
+    out = {"workload": WORKLOADS["c3"], "value": secs, "unit": "s",
+           "measured": "CUDA events around one device-resident solve after one warm-up solve",
+           "outer_steps": rep.outer_iterations, "converged": rep.converged,
+           "final_scaled_residual": rep.final_scaled_residual,
+           "sum_inner_A": rep.sum_inner_A, "sum_inner_B": rep.sum_inner_B}
+    del eng
+    return out
+
+
+def _free_device():
+    import gc
+    import torch
+    from paper_2312_02891_b200 import _lib
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    lib = _lib.load()
+    for ctx in list(_lib._CTX.values()):
+        lib.sad_ctx_trim(ctx)
+
+
 def run_ours_c4(args, dist):
-    """Inner-solve microbenchmark (config 4): shifted SpMM GB/s on the r=8 block
-    (metric), plus 100 fixed GMRES steps through the persistent engine."""
+    """Config 4 (BASELINE configs[3], the metric "inner SpMM GB/s vs HBM peak"):
+    the shifted SpMM on the full 16.7M x 8 block (value: device-resident; e2e:
+    host block -> sad_op_apply_host -> host block), then 100 fixed GMRES steps
+    (orthogonalisation GB/s, iterations/s) and config 3's 1-GPU wall time."""
     import torch
     from paper_2312_02891_b200 import GpuGmresBinding, _lib
     from paper_2312_02891_b200 import configs as cfgs
@@ -532,23 +698,28 @@ def run_ours_c4(args, dist):
     lib = _lib.load()
     n0 = args.c4_n0
     A, X = cfgs.build_c4(n0=n0, r=8, seed=0)
-    # alpha = 0.1 * lambda_max estimate (Gershgorin bound of the stencil, negative)
-    shift = 0.1 * (-abs(A.diagonal()).max() * 2.0)
+    ritz_steps = 10
+    pinned = c4_pinned_shift(n0)
+    if args.c4_shift is not None:
+        shift, lam = float(args.c4_shift), None
+    elif pinned is not None:
+        shift, lam = pinned          # configs/shift_c4.json (the reference's arnoldi_ritz)
+    else:
+        shift, lam = c4_shift(A, dev, ritz_steps)
     steps = args.c4_steps
     gb = GpuGmresBinding("A", A, None, precond_kind="jacobi", restart=steps, device=dev)
     rhs = torch.from_numpy(X).cuda()
-    x = torch.empty_like(rhs)
-    res = torch.empty_like(rhs)
     op = gb.operator(shift)
     n, r = A.shape[0], 8
     blk = n * r * 8
-    spmm_b = A.nnz * 12 + 4 * (n + 1) + 2 * blk
+    spmm_b = c4_spmm_bytes(A)
     # --- shifted SpMM (the metric): K timed launches, L2 flushed in between ---
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     y = torch.empty_like(rhs)
     clocks = Clocks(dev)
     clocks.start()          # before the warm-up (see run_ours_c2)
     for _ in range(args.warmup):
+        flush.fill_(1.0)
         op.apply(rhs, y)
     time.sleep(0.3)         # the sampler's start-up is over before the timed region
     dist.barrier()
@@ -564,40 +735,111 @@ def run_ours_c4(args, dist):
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
     dist.barrier()
     launches = lib.sad_kernel_launches() - l0
-    spmm_ms = statistics.mean(ms)
+    ck = clocks.stop()
+    spmm_ms = dist.max(statistics.mean(ms))
     spmm_gbs = spmm_b / (spmm_ms * 1e-3) / 1e9
     value = spmm_gbs * dist.world
+    y_dev = y.cpu().numpy()
+    # --- e2e: the same SpMM through the host-buffer C-ABI call (pinned host
+    # blocks; every step uploads x and downloads y inside the timed region) ---
+    xh = torch.empty((n, r), dtype=torch.float64, pin_memory=True)
+    yh = torch.empty((n, r), dtype=torch.float64, pin_memory=True)
+    xh.copy_(torch.from_numpy(X))
+    xh_np, yh_np = xh.numpy(), yh.numpy()
+    for _ in range(args.warmup):
+        op.apply_host(xh_np, yh_np)
+    e2e_s = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op.apply_host(xh_np, yh_np)           # synchronous: y is on the host
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_mean = dist.max(statistics.mean(e2e_s))
+    e2e_gbs = spmm_b / e2e_mean / 1e9 * dist.world
+    host_vs_dev = float(np.max(np.abs(yh_np - y_dev)))
+    del xh, yh
     # --- the inner solve: 100 fixed GMRES steps, one persistent launch ---
+    x = torch.empty_like(rhs)
+    res = torch.empty_like(rhs)
     ws = gb.workspace(8, _lib.SAD_F64)
     ws.fixed(op, rhs, x, res, steps)
     _, tm = ws.fixed(op, rhs, x, res, steps, timed=True)
-    ck = clocks.stop()
     peak, peak_kind = hbm_peak()
     solve_gbs = tm[3] / (tm[0] * 1e-3) / 1e9
+    arn = int(tm[6]) if tm[6] > 0 else steps
+    # DCGS2 bytes of Arnoldi step j (J = j + 1 basis blocks): (2J + 2) N
+    orth_b = sum((2 * (j + 1) + 2) * blk for j in range(arn))
+    orth_ms = max(tm[1] - tm[4], 0.0) + tm[2]
     traffic, tr_ent = ncu_traffic("c4_spmm")
     straffic, str_ent = ncu_traffic("c4_persistent")
+    del gb, op, ws, x, res, rhs, y, flush
+    _free_device()
+    c3 = None
+    if not args.no_c3:
+        try:
+            c3 = c3_wall_time(args, dev)
+        except Exception as exc:          # reported, never hidden
+            c3 = {"error": f"{type(exc).__name__}: {exc}"}
+        _free_device()
     line = {"metric": "inner SpMM GB/s", "value": value, "unit": "GB/s",
             "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": spmm_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"config 4: {n0}^2 conv-diff, r=8, "
-                                                        f"shifted SpMM + {steps} fixed GMRES steps",
-                                            "n": n, "nnz": int(A.nnz),
-                                            "l2": "flushed between timed SpMMs"},
+            "data": "synthetic (seeded reference generators: convdiff_fd, Philox N(0,1))",
+            "config": {"workload": C4_WORKLOAD.format(n0=n0, n=n, nnz=A.nnz, ritz=ritz_steps,
+                                                      steps=steps),
+                       "n": n, "nnz": int(A.nnz), "r": r, "shift": shift,
+                       "lambda_max_ritz": None if lam is None else [lam.real, lam.imag],
+                       "l2": "flushed between timed SpMMs (256 MiB write); the 3.36 GB "
+                             "working set also exceeds L2",
+                       "parallelism": "single GPU" if dist.world == 1 else "replicas"},
             "roofline": {"bound": "hbm", "achieved": spmm_gbs, "peak": peak, "unit": "GB/s",
                          "frac": spmm_gbs / peak, "traffic": traffic, "kernel": "k_spmm_bulk",
+                         "frac_of_nominal_8000": spmm_gbs / 8000.0,
                          "traffic_source": tr_ent and (f"profiles/traffic.json[c4_spmm]: "
                                                        f"{tr_ent['note']}"),
-                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": spmm_b},
-            "inner_solve": {"kernel": "k_gmres_persistent", "steps": steps,
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": spmm_b,
+                         "avg_launch_ms": spmm_ms,
+                         "measured": "CUDA events around each timed launch on torch's current "
+                                     "stream (the launch stream)"},
+            "e2e": {"value": e2e_gbs, "unit": "GB/s", "h2d_bytes_per_step": blk,
+                    "d2h_bytes_per_step": blk, "ms_per_step": e2e_mean * 1000.0,
+                    "api": "DeviceOperator.apply_host -> sad_op_apply_host (pinned host x, y; "
+                           "chunked upload / SpMM / download overlapped)",
+                    "max_abs_diff_vs_device_apply": host_vs_dev},
+            "inner_solve": {"kernel": "k_gmres_persistent", "steps": arn,
                             "kernel_ms": tm[0], "phaseA_ms": tm[1], "phaseC_ms": tm[2],
+                            "spmm_subphase_ms": tm[4], "cycle_end_ms": tm[5],
                             "algorithmic_bytes": tm[3], "gbs": solve_gbs,
-                            "traffic": straffic,
-                            "frac": solve_gbs / peak,
-                            "iterations_per_s": steps * r / (tm[0] * 1e-3)},
+                            "frac": solve_gbs / peak, "traffic": straffic,
+                            "orthogonalisation_bytes": orth_b,
+                            "orthogonalisation_ms": orth_ms,
+                            "orthogonalisation_gbs": orth_b / (orth_ms * 1e-3) / 1e9
+                            if orth_ms > 0 else None,
+                            "iterations_per_s": arn * r / (tm[0] * 1e-3),
+                            "note": "phase times from block 0's %globaltimer; orthogonalisation "
+                                    "= phase A minus its SpMM sub-phase, plus phase C"},
             "gpu_launches": int(launches), "clocks": ck}
+    if c3 is not None:
+        line["config3_wall_time"] = c3
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        secs, ycpu = cpu_apply_threads(A, X, shift, threads, reps=3)
+        t = statistics.mean(secs)
+        rel = float(np.max(np.abs(ycpu - y_dev)) / np.max(np.abs(ycpu)))
+        line["cpu_baseline"] = {"value": spmm_b / t / 1e9, "unit": "GB/s", "cores": threads,
+                                "kind": "port",
+                                "sample": f"3 full config-4 applies of the reference's "
+                                          f"ShiftedOperator.apply (oracle/ restatement, scipy "
+                                          f"csr_matvecs + complex cast + shift) over {threads} "
+                                          f"threads on row chunks, {t:.2f} s each"}
+        line["parity"] = {"max_rel_diff_vs_cpu_apply": rel,
+                          "note": "device SpMM vs the reference's apply on the full block "
+                                  "(fma vs mul+add rounding)"}
     return line if dist.rank == 0 else None
 
 
@@ -771,16 +1013,21 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5", "c3s", "c5s"])
+    ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4", "c5", "c3s", "c5s"])
     ap.add_argument("--c4-n0", type=int, default=4096)
     ap.add_argument("--c4-steps", type=int, default=100)
+    ap.add_argument("--c4-shift", type=float, default=None,
+                    help="config 4 shift (default: 0.1 * largest-magnitude Ritz value)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="config 4: skip the config-3 wall-time key")
     ap.add_argument("--rowpart", action="store_true",
                     help="configs 3-5: row-partitioned path even at N = 1 (NCCL world of 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         dist = Dist(0)
-        line = run_reference_arm(args, dist)
+        line = (run_reference_arm_c4(args, dist) if args.config == "c4"
+                else run_reference_arm(args, dist))
     else:
         sharded = args.config in ("c3", "c4", "c5", "c3s", "c5s") and (
             args.rowpart or int(os.environ.get("WORLD_SIZE", 1)) > 1)

@@ -47,7 +47,9 @@ enum sad_engine { SAD_ENGINE_MULTI = 0, SAD_ENGINE_PERSISTENT = 1 };
 enum sad_option { SAD_OPT_ENGINE = 0, SAD_OPT_MAX_SMS = 1, SAD_OPT_MIN_ELEMS_PER_THREAD = 2,
                   SAD_OPT_DIRECT_A = 3 /* persistent phase A: -1 auto, 0 TMA ring, 1 direct */,
                   SAD_OPT_RESIDENT_CSR = 4, /* 1 (default): small CSR slabs stay in shared memory */
-                  SAD_OPT_DIST_ORTH = 5 /* row-partitioned: 1 (default) delayed-Gram CGS2, 0 CGS2 */ };
+                  SAD_OPT_DIST_ORTH = 5, /* row-partitioned: 1 (default) delayed-Gram CGS2, 0 CGS2 */
+                  SAD_OPT_DEBUG_DELAY = 6 /* tests: the persistent kernel's last block idles this
+                                             many ns after every phase-C barrier (race stress) */ };
 enum sad_precond { SAD_PRECOND_NONE = 0, SAD_PRECOND_JACOBI = 1 };
 
 typedef struct sad_ctx sad_ctx;
@@ -104,6 +106,17 @@ int sad_op_get_dinv(const sad_op* op, double* dinv_host);
 /* y = Op x  (ShiftedOperator.apply, sparse.py:192-206). */
 int sad_op_apply(sad_op* op, int r, int dtype, const void* x_dev, void* y_dev,
                  void* stream);
+/*
+ * y = Op x between HOST buffers (x_host, y_host: n x r row-major), the
+ * reference-facing form of ShiftedOperator.apply (sparse.py:192-206), which
+ * takes and returns host numpy blocks.  Returns when y_host is filled.  The
+ * block moves in row chunks: uploads on one stream, the SpMM of an output chunk
+ * as soon as the x rows it reads have landed, downloads on a third stream
+ * (both PCIe directions and the SpMM overlap when the buffers are pinned).
+ * Device staging is owned by the operator and reused across calls.
+ */
+int sad_op_apply_host(sad_op* op, int r, int dtype, const void* x_host, void* y_host,
+                      void* stream);
 /* y = b - Op x  (the true residual, krylov.py:62). */
 int sad_op_residual(sad_op* op, int r, int dtype, const void* b_dev,
                     const void* x_dev, void* y_dev, void* stream);
@@ -160,9 +173,11 @@ int sad_gmres_finish(sad_gmres* ws, void* res_dev, void* stream, int64_t* iters_
 /*
  * Same solve, but a fixed number of Arnoldi steps (no stopping test inside the
  * cycle; config 4 "100 fixed block-GMRES iterations").  When timing_ms_host is
- * not NULL it receives (CUDA events on `stream`):
+ * not NULL (8 doubles) it receives (CUDA events on `stream`):
  *   multi-kernel engine: {spmm_ms, orth_ms, cycle_end_ms, initial_residual_ms}
- *   persistent engine:   {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes}
+ *   persistent engine:   {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes,
+ *                         spmmA_ms, cycle_end_ms, arnoldi_steps, 0}
+ *   (phase times: block 0's %globaltimer; spmmA = its SpMM sub-phase of phase A)
  */
 int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
                     void* res_dev, int steps, void* stream,

@@ -19,6 +19,7 @@ SAD_ENGINE_MULTI, SAD_ENGINE_PERSISTENT = 0, 1
 SAD_OPT_ENGINE, SAD_OPT_MAX_SMS, SAD_OPT_MIN_ELEMS_PER_THREAD, SAD_OPT_DIRECT_A = 0, 1, 2, 3
 SAD_OPT_RESIDENT_CSR = 4
 SAD_OPT_DIST_ORTH = 5
+SAD_OPT_DEBUG_DELAY = 6
 
 #: every symbol declared in include/sylvadi_b200.h with (restype, argtypes)
 _c = ctypes
@@ -42,6 +43,7 @@ SIGNATURES = {
     "sad_op_destroy": (_c.c_int, [_vp]),
     "sad_op_get_dinv": (_c.c_int, [_vp, _vp]),
     "sad_op_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
+    "sad_op_apply_host": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
     "sad_op_residual": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),
     "sad_csr_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _c.c_int, _vp, _vp, _vp]),
     "sad_gmres_create": (_c.c_int, [_vp, _i64, _c.c_int, _c.c_int, _c.c_int, _c.c_int,

@@ -51,6 +51,7 @@ struct DevCache {
 
 struct sad_ctx {
   DevCache cache;
+  std::mutex op_mu;              // serialises sad_op_create
   int device = 0;
   int nsm = 148;
   std::string err;
@@ -93,6 +94,10 @@ static std::atomic<long long> g_launches{0};   // kernels launched by this libra
 namespace sad {
 void count_launches(long long k) { COUNT_LAUNCH(k); }
 int g_spmm_bulk_sms = 148;
+int g_spmm_xpf = [] {
+  const char* e = getenv("SAD_SPMM_XPF");
+  return e ? atoi(e) : 1;
+}();
 }
 
 struct sad_op {
@@ -115,6 +120,24 @@ struct sad_op {
   double* dinv_r = nullptr;
   int precond = 0;
   long long nnz = 0;
+  struct HostApply* happ = nullptr;   // sad_op_apply_host staging (lazy)
+};
+
+// Chunked, pipelined y = Op x between HOST buffers (sad_op_apply_host): x is
+// uploaded in row chunks on one stream, the SpMM of output chunk k starts as
+// soon as every x chunk up to its largest column index has landed, and y
+// chunk k is downloaded on a third stream while later chunks compute, so the
+// two PCIe directions and the SpMM overlap.
+struct HostApply {
+  int r = 0, dtype = -1, nchunk = 0;
+  size_t esz = 0;
+  void* xd = nullptr;
+  void* yd = nullptr;
+  std::vector<long long> bounds;   // nchunk + 1 row boundaries
+  std::vector<int> need;           // last x chunk each output chunk reads
+  cudaStream_t sin = nullptr, sout = nullptr;
+  std::vector<cudaEvent_t> ein, ecomp;
+  cudaEvent_t estart = nullptr, eend = nullptr;
 };
 
 struct sad_gmres {
@@ -148,6 +171,7 @@ struct sad_gmres {
   int min_elems_per_thread = 2;
   int direct_a = -1;            // phase-A path: -1 auto, 0 TMA ring, 1 direct loads
   int resident_csr = 1;         // keep small CSR slabs in shared memory
+  int dbg_delay_ns = 0;         // SAD_OPT_DEBUG_DELAY (race stress tests)
   PState pst{};
   double* stats_dev = nullptr;
   // profiling (sad_gmres_profile): synchronous stepping with CUDA events
@@ -441,6 +465,9 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
     return set_err(ctx, SAD_EINVAL, "adjoint operator needs matrices created with build_transpose");
   if (precond_kind != SAD_PRECOND_NONE && precond_kind != SAD_PRECOND_JACOBI)
     return set_err(ctx, SAD_EINVAL, "unknown preconditioner kind %d", precond_kind);
+  // creation is serialised per context (shared error string, legacy-stream
+  // work); concurrent solves on other streams are unaffected
+  std::lock_guard<std::mutex> creating(ctx->op_mu);
   sad_op* op = new sad_op();
   op->ctx = ctx;
   op->uid = g_op_uid.fetch_add(1);
@@ -516,10 +543,14 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   // one allocation for both dinv copies; the breakdown flag lives in the ctx
   char* dbuf = nullptr;
   const size_t nn = (size_t)std::max<long long>(n, 1);
-  CK(ctx, ctx_malloc(ctx, (void**)&dbuf, nn * sizeof(double2) + nn * sizeof(double) + 256));
+  const size_t dr_off = (nn * sizeof(double2) + 255) & ~size_t(255);
+  const size_t bd_off = (dr_off + nn * sizeof(double) + 255) & ~size_t(255);
+  CK(ctx, ctx_malloc(ctx, (void**)&dbuf, bd_off + 256));
   op->dinv_c = reinterpret_cast<double2*>(dbuf);
-  op->dinv_r = reinterpret_cast<double*>(dbuf + ((nn * sizeof(double2) + 255) & ~size_t(255)));
-  int* d_bd = reinterpret_cast<int*>(ctx->ticket + 8);
+  op->dinv_r = reinterpret_cast<double*>(dbuf + dr_off);
+  // the breakdown flag belongs to this operator (two host threads may create
+  // operators on one context at once)
+  int* d_bd = reinterpret_cast<int*>(dbuf + bd_off);
   CK(ctx, cudaMemsetAsync(d_bd, 0, sizeof(int), 0));
   const int blocks = grid_for(n, 256, ctx->nsm * 16);
   if (precond_kind == SAD_PRECOND_JACOBI) {
@@ -545,8 +576,26 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   return SAD_OK;
 }
 
+static void host_apply_free(sad_op* op) {
+  HostApply* h = op->happ;
+  if (!h) return;
+  if (h->sin) cudaStreamSynchronize(h->sin);
+  if (h->sout) cudaStreamSynchronize(h->sout);
+  ctx_free(op->ctx, h->xd);
+  ctx_free(op->ctx, h->yd);
+  for (cudaEvent_t e : h->ein) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ecomp) cudaEventDestroy(e);
+  if (h->estart) cudaEventDestroy(h->estart);
+  if (h->eend) cudaEventDestroy(h->eend);
+  if (h->sin) cudaStreamDestroy(h->sin);
+  if (h->sout) cudaStreamDestroy(h->sout);
+  delete h;
+  op->happ = nullptr;
+}
+
 extern "C" int sad_op_destroy(sad_op* op) {
   if (!op) return SAD_OK;
+  host_apply_free(op);
   ctx_free(op->ctx, op->own_rowptr);
   ctx_free(op->ctx, op->own_colidx);
   ctx_free(op->ctx, op->own_vals);
@@ -601,6 +650,137 @@ extern "C" int sad_op_residual(sad_op* op, int r, int dtype, const void* b, cons
                                void* stream) {
   if (!op || !b || !x || !y) return SAD_EINVAL;
   return op_spmm<SPMM_RESID>(op, r, dtype, b, x, y, stream);
+}
+
+// largest column index over the rows [bounds[k], bounds[k+1]) of each chunk
+__global__ void k_chunk_maxcol(const int* rowptr, const int* colidx, const long long* bounds,
+                               int* out) {
+  const int k = blockIdx.x;
+  const int kb = rowptr[bounds[k]], ke = rowptr[bounds[k + 1]];
+  int mx = -1;
+  for (int i = kb + threadIdx.x; i < ke; i += blockDim.x) mx = max(mx, colidx[i]);
+  for (int sh = 16; sh > 0; sh >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, sh));
+  __shared__ int s_mx[32];
+  if ((threadIdx.x & 31) == 0) s_mx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = max(mx, s_mx[w]);
+    out[k] = max(mx, s_mx[0]);
+  }
+}
+
+static int host_apply_setup(sad_op* op, int r, int dtype) {
+  sad_ctx* ctx = op->ctx;
+  HostApply* h = op->happ;
+  const size_t esz = dtype == SAD_F64 ? 8 : 16;
+  if (h && h->r == r && h->dtype == dtype) return SAD_OK;
+  host_apply_free(op);
+  h = op->happ = new HostApply();
+  h->r = r;
+  h->dtype = dtype;
+  h->esz = esz;
+  const long long n = op->n;
+  const size_t bytes = (size_t)n * r * esz;
+  // ~16 MiB chunks (PCIe transfers stay efficient), at most 128 of them
+  const long long target = std::max<long long>(1, (long long)((bytes + (16u << 20) - 1) / (16u << 20)));
+  h->nchunk = (int)std::min<long long>(std::min<long long>(target, 128), std::max<long long>(n, 1));
+  h->bounds.resize(h->nchunk + 1);
+  for (int k = 0; k <= h->nchunk; ++k) h->bounds[k] = n * k / h->nchunk;
+  CK(ctx, ctx_malloc(ctx, &h->xd, bytes + 64));
+  CK(ctx, ctx_malloc(ctx, &h->yd, bytes + 64));
+  CK(ctx, cudaStreamCreateWithFlags(&h->sin, cudaStreamNonBlocking));
+  CK(ctx, cudaStreamCreateWithFlags(&h->sout, cudaStreamNonBlocking));
+  h->ein.resize(h->nchunk);
+  h->ecomp.resize(h->nchunk);
+  for (int k = 0; k < h->nchunk; ++k) {
+    CK(ctx, cudaEventCreateWithFlags(&h->ein[k], cudaEventDisableTiming));
+    CK(ctx, cudaEventCreateWithFlags(&h->ecomp[k], cudaEventDisableTiming));
+  }
+  CK(ctx, cudaEventCreateWithFlags(&h->estart, cudaEventDisableTiming));
+  CK(ctx, cudaEventCreateWithFlags(&h->eend, cudaEventDisableTiming));
+  // which x chunk each output chunk waits for (x chunks land in order)
+  long long* dbounds = nullptr;
+  int* dmax = nullptr;
+  CK(ctx, cudaMalloc(&dbounds, (h->nchunk + 1) * sizeof(long long)));
+  CK(ctx, cudaMalloc(&dmax, h->nchunk * sizeof(int)));
+  CK(ctx, cudaMemcpy(dbounds, h->bounds.data(), (h->nchunk + 1) * sizeof(long long),
+                     cudaMemcpyHostToDevice));
+  k_chunk_maxcol<<<h->nchunk, 256>>>(op->rowptr, op->colidx, dbounds, dmax);
+  COUNT_LAUNCH(1);
+  std::vector<int> mx(h->nchunk);
+  CK(ctx, cudaMemcpy(mx.data(), dmax, h->nchunk * sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(dbounds);
+  cudaFree(dmax);
+  h->need.resize(h->nchunk);
+  for (int k = 0; k < h->nchunk; ++k) {
+    // the diagonal term (shift) reads x rows of the chunk itself
+    const long long col = std::max<long long>(mx[k], h->bounds[k + 1] - 1);
+    int q = (int)(std::upper_bound(h->bounds.begin(), h->bounds.end(), col) - h->bounds.begin()) - 1;
+    h->need[k] = std::min(std::max(q, k), h->nchunk - 1);
+  }
+  return SAD_OK;
+}
+
+extern "C" int sad_op_apply_host(sad_op* op, int r, int dtype, const void* x_host, void* y_host,
+                                 void* stream) {
+  if (!op || !x_host || !y_host) return SAD_EINVAL;
+  sad_ctx* ctx = op->ctx;
+  int rc = check_block(ctx, r, dtype);
+  if (rc) return rc;
+  if (dtype == SAD_F64 && !op->real_ok)
+    return set_err(ctx, SAD_EINVAL, "complex shift needs a complex128 block");
+  if (op->ncols != op->n) return set_err(ctx, SAD_EINVAL, "host apply needs a square operator");
+  rc = host_apply_setup(op, r, dtype);
+  if (rc) return rc;
+  HostApply* h = op->happ;
+  cudaStream_t s = S_(stream);
+  const size_t rowb = (size_t)r * h->esz;
+  // the staging buffers are reused: uploads wait for earlier work on `stream`
+  CK(ctx, cudaEventRecord(h->estart, s));
+  CK(ctx, cudaStreamWaitEvent(h->sin, h->estart, 0));
+  CK(ctx, cudaStreamWaitEvent(h->sout, h->estart, 0));
+  for (int k = 0; k < h->nchunk; ++k) {
+    const long long b0 = h->bounds[k], b1 = h->bounds[k + 1];
+    CK(ctx, cudaMemcpyAsync((char*)h->xd + b0 * rowb, (const char*)x_host + b0 * rowb,
+                            (b1 - b0) * rowb, cudaMemcpyHostToDevice, h->sin));
+    CK(ctx, cudaEventRecord(h->ein[k], h->sin));
+  }
+  int waited = -1;
+  for (int k = 0; k < h->nchunk; ++k) {
+    const long long b0 = h->bounds[k], b1 = h->bounds[k + 1];
+    if (h->need[k] > waited) {
+      CK(ctx, cudaStreamWaitEvent(s, h->ein[h->need[k]], 0));
+      waited = h->need[k];
+    }
+    if (b1 > b0) {
+      if (dtype == SAD_F64) {
+        SpmmArgs<double> a{};
+        a.n = b1 - b0; a.row0 = b0;
+        a.rowptr = op->rowptr + b0; a.colidx = op->colidx; a.vals = op->vals;
+        a.x = (const double*)h->xd; a.y = (double*)h->yd + b0 * r;
+        a.dinv = op->dinv_r; a.sigma = op->sigma_eff;
+        rc = launch_spmm<double, SPMM_APPLY>(a, r, false, false, op->sigma_identity, ctx->nsm, s);
+      } else {
+        SpmmArgs<double2> a{};
+        a.n = b1 - b0; a.row0 = b0;
+        a.rowptr = op->rowptr + b0; a.colidx = op->colidx; a.vals = op->vals;
+        a.x = (const double2*)h->xd; a.y = (double2*)h->yd + b0 * r;
+        a.dinv = op->dinv_c; a.sigma = op->sigma_eff;
+        rc = launch_spmm<double2, SPMM_APPLY>(a, r, op->vals_complex, false, op->sigma_identity,
+                                               ctx->nsm, s);
+      }
+      if (rc) return set_err(ctx, SAD_EINVAL, "unsupported block width %d", r);
+      CKL(ctx);
+    }
+    CK(ctx, cudaEventRecord(h->ecomp[k], s));
+    CK(ctx, cudaStreamWaitEvent(h->sout, h->ecomp[k], 0));
+    CK(ctx, cudaMemcpyAsync((char*)y_host + b0 * rowb, (const char*)h->yd + b0 * rowb,
+                            (b1 - b0) * rowb, cudaMemcpyDeviceToHost, h->sout));
+  }
+  CK(ctx, cudaEventRecord(h->eend, h->sout));
+  CK(ctx, cudaStreamWaitEvent(s, h->eend, 0));
+  CK(ctx, cudaStreamSynchronize(s));
+  return SAD_OK;
 }
 
 extern "C" int sad_csr_apply(sad_csr* csr, int transpose, int r, int dtype, const void* x, void* y,
@@ -1102,6 +1282,7 @@ static PArgs<XT> make_pargs(sad_gmres* ws, sad_op* op, const void* rhs, void* x)
   a.stride = ws->n * ws->R;
   a.st = ws->pst;
   a.prof = ws->profile || ws->timers;
+  a.dbg_delay_ns = ws->dbg_delay_ns;
   return a;
 }
 
@@ -1261,6 +1442,10 @@ extern "C" int sad_gmres_set_option(sad_gmres* ws, int key, int value) {
       if (value < -1 || value > 1) return set_err(ws->ctx, SAD_EINVAL, "direct-A option must be -1, 0 or 1");
       ws->direct_a = value;
       return SAD_OK;
+    case SAD_OPT_DEBUG_DELAY:
+      if (value < 0 || value > 1000000) return set_err(ws->ctx, SAD_EINVAL, "delay must be in [0, 1e6] ns");
+      ws->dbg_delay_ns = value;
+      return SAD_OK;
   }
   return set_err(ws->ctx, SAD_EINVAL, "unknown option %d", key);
 }
@@ -1385,11 +1570,16 @@ extern "C" int sad_gmres_fixed(sad_gmres* ws, sad_op* op, const void* rhs, void*
       cudaEventElapsedTime(&ms, e0, e1);
       double st[16];
       CK(ctx, cudaMemcpy(st, ws->stats_dev, sizeof(st), cudaMemcpyDeviceToHost));
-      // {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes}
+      // {kernel_ms, phaseA_ms, phaseC_ms, algorithmic_bytes, spmmA_ms,
+      //  cycle_end_ms, arnoldi_steps, 0}
       timing_ms[0] = ms;
       timing_ms[1] = st[3] * 1e-6;
       timing_ms[2] = st[4] * 1e-6;
       timing_ms[3] = st[0];
+      timing_ms[4] = st[12] * 1e-6;
+      timing_ms[5] = (st[5] + st[6]) * 1e-6;
+      timing_ms[6] = st[1];
+      timing_ms[7] = 0.0;
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
     }

@@ -90,6 +90,7 @@ struct PArgs {
   int csr_off;           // dynamic-smem byte offset of the resident CSR slab
   int csr_budget;        // bytes available there (0 = CSR read from global)
   int sweep_direct;      // large slabs: basis sweep by basis block with direct loads (no TMA ring)
+  int dbg_delay_ns;      // tests: the last block idles this long after every phase-C release
   PState st;
 };
 
@@ -279,6 +280,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   __shared__ double s_w2[kWarps][8];
   __shared__ int s_any;
   __shared__ double s_Sj[8];     // S_{j+1} of the step just finished (block copy)
+  // Per-column Givens state the phase-C finisher reads, kept per block: block 0
+  // alone writes gs.active / gs.iters / gs.g, and no grid barrier separates
+  // those writes from a late block's reads of the same step, so every block
+  // works from its own copy (loaded at the cycle start, after a full barrier,
+  // and updated by the identical computation in every block).
+  __shared__ int s_cact[8];
+  __shared__ long long s_cit[8];
+  __shared__ double2 s_cg[8];
   const int cbase = 2 * (m + 1) * R;   // phase-C partial slots (after phase A's)
   // phase-A TMA ring
   __shared__ __align__(8) unsigned long long s_full[kStages];
@@ -396,6 +405,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   // ---- cycles ---------------------------------------------------------------
   while (true) {
     if (threadIdx.x == 0) s_any = ldcgi(gs.any_active);
+    if (threadIdx.x < R) {
+      // safe: block 0 rewrites these only after the next phase-A barrier,
+      // which this block has not reached yet
+      const int cc = threadIdx.x;
+      s_cact[cc] = ldcgi(gs.active + cc);
+      s_cit[cc] = __ldcg(gs.iters + cc);
+      s_cg[cc] = ldcg2(gs.g + (size_t)cc * (m + 1) + ldcgi(gs.j));
+    }
     __syncthreads();
     if (!s_any) break;
     // ---------------- Arnoldi steps ----------------
@@ -963,6 +980,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         // whether the cycle goes on) in shared memory.
         if (bar_arrive(st, gen)) bar_release(st);
         else bar_wait(st, gen);
+        if (a.dbg_delay_ns > 0 && blockIdx.x == gridDim.x - 1 && gridDim.x > 1) {
+          // race stress (tests): block 0 runs ahead and rewrites the global
+          // Givens state before this block's finisher runs
+          const unsigned long long t0 = gtimer();
+          while (gtimer() - t0 < (unsigned long long)a.dbg_delay_ns) {
+          }
+          __syncthreads();
+        }
         {
           const bool w0 = blockIdx.x == 0;
           const unsigned long long tfin = (prof && w0 && threadIdx.x == 0) ? gtimer() : 0ull;
@@ -974,10 +999,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           double2 gj_c = make_double2(0.0, 0.0), hjj = gj_c;
           if (threadIdx.x < R) {
             const int cc = threadIdx.x;
-            act_c = ldcgi(gs.active + cc);
-            it_c = __ldcg(gs.iters + cc);
+            act_c = s_cact[cc];
+            it_c = s_cit[cc];
             wpre_c = ldcg1(gs.wpre2 + cc);
-            gj_c = ldcg2(gs.g + (size_t)cc * (m + 1) + j);
+            gj_c = s_cg[cc];
             hjj = ldcg2(st.hc + j * R + cc);
           }
           reduce_partials_small(partT + (size_t)cbase * pT, pT, gridDim.x, R, s_nrm);
@@ -1011,6 +1036,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                 if (end) gs.active[cc] = 0;
               }
               s_actn[cc] = end ? 0 : 1;
+              s_cact[cc] = end ? 0 : 1;
+              s_cit[cc] = it;
+              s_cg[cc] = gnext;
             } else if (w0) {
               gs.S[(j + 1) * R + cc] = 0.0;
             }

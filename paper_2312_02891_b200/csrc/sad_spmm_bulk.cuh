@@ -43,6 +43,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
   }
 }
+// L2 prefetch of a global byte range (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -136,6 +140,13 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
   if (warp == kWarps) {
     // ---------------- producer ----------------
     if (lane == 0) {
+      // x rows of a tile's diagonal block: their first touch is usually by
+      // this tile or by a concurrently running neighbour tile (banded
+      // operators), so they are prefetched into L2 when the tile's CSR slice
+      // is staged, STAGES tiles ahead, instead of being a DRAM round trip on
+      // the consumers' critical path
+      const XT* xpf_base = a.x;
+      if (MODE == SPMM_ARNOLDI) xpf_base = a.x + (long long)(*a.st.j) * a.stride;
       for (long long k = 0; k < K; ++k) {
         const int st = (int)(k % S);
         // the tile's row range is loaded before waiting for the free stage, so
@@ -168,6 +179,11 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
         if (stage_cv) {
           if (c1 > c0) bulk_g2s(base, reinterpret_cast<const void*>(c0), (unsigned)(c1 - c0), full + st);
           if (v1 > v0) bulk_g2s(base + CI, reinterpret_cast<const void*>(v0), (unsigned)(v1 - v0), full + st);
+        }
+        if (a.xpf) {
+          unsigned long long x0, x1;
+          aligned_range(xpf_base, (r0 + a.row0) * R, (long long)rows * R, (int)sizeof(XT), x0, x1);
+          if (x1 > x0) bulk_prefetch_l2(reinterpret_cast<const void*>(x0), (unsigned)(x1 - x0));
         }
       }
     }
@@ -247,8 +263,9 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
         if (idx[u] < 0) continue;
         XT vres = acc[u];
         if (SIGMA || (MODE == SPMM_ARNOLDI && zout)) {
-          XT xi = x[idx[u]];
-          if (PRE) xi = mul(__ldg(a.dinv + idx[u] / R), xi);
+          const long long gidx = idx[u] + a.row0 * R;
+          XT xi = x[gidx];
+          if (PRE) xi = mul(__ldg(a.dinv + gidx / R), xi);
           if (SIGMA) vres = fma_(from_c<XT>(a.sigma), xi, vres);
           if (MODE == SPMM_ARNOLDI && zout) zout[idx[u]] = sscal(scale, xi);
         }

@@ -39,7 +39,9 @@ static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
     }
     const long long tiles = (a.n + BulkTile<R>::TR - 1) / BulkTile<R>::TR;
     const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_spmm_bulk_sms));
-    kern<<<g, kThreads + 32, smem, s>>>(a);
+    SpmmArgs<XT> ab = a;
+    ab.xpf = g_spmm_xpf;
+    kern<<<g, kThreads + 32, smem, s>>>(ab);
     count_launches(1);
   } else {
     k_spmm<XT, VT, R, MODE, PRE, SIGMA><<<grid, kThreads, 0, s>>>(a);
@@ -87,6 +89,7 @@ static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, i
   z.y = reinterpret_cast<double2*>(a.y);
   z.b = reinterpret_cast<const double2*>(a.b);
   z.sigma = a.sigma;
+  z.row0 = a.row0;
   if (mode == SPMM_APPLY) launch_spmm<double2, SPMM_APPLY>(z, R / 2, false, false, sigma, nsm, s);
   else launch_spmm<double2, SPMM_RESID>(z, R / 2, false, false, sigma, nsm, s);
   return true;

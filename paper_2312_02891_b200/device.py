@@ -134,6 +134,27 @@ class DeviceOperator:
         _lib.check(rc, self._ctx)
         return y
 
+    def apply_host(self, x, out=None, stream=None):
+        """y = Op x for HOST numpy blocks (n, r) float64/complex128, through
+        sad_op_apply_host: chunked uploads, SpMM and downloads overlapped (pinned
+        buffers, e.g. from torch's pin_memory, give full PCIe overlap)."""
+        x = np.asarray(x)
+        if x.ndim == 1:
+            x = x.reshape(-1, 1)
+        if x.dtype not in (np.float64, np.complex128) or not x.flags.c_contiguous:
+            raise ValueError("x must be a C-contiguous float64 or complex128 block")
+        if x.shape[0] != self.n:
+            raise ValueError(f"block has {x.shape[0]} rows, operator expects {self.n}")
+        if out is None:
+            out = np.empty_like(x)
+        if out.shape != x.shape or out.dtype != x.dtype or not out.flags.c_contiguous:
+            raise ValueError("out must match x (shape, dtype, C order)")
+        dtype = _lib.SAD_F64 if x.dtype == np.float64 else _lib.SAD_C128
+        rc = _lib.load().sad_op_apply_host(self.handle, x.shape[1], dtype, x.ctypes.data,
+                                           out.ctypes.data, current_stream_handle(stream))
+        _lib.check(rc, self._ctx)
+        return out
+
     def residual(self, b, x, y=None, stream=None):
         import torch
         dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
@@ -231,7 +252,7 @@ class GmresWorkspace:
 
     def fixed(self, op, rhs, x, res, steps, stream=None, timed=False):
         norms = np.zeros(self.r, dtype=np.float64)
-        timing = np.zeros(4, dtype=np.float64)
+        timing = np.zeros(8, dtype=np.float64)
         rc = _lib.load().sad_gmres_fixed(
             self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
             None if res is None else res.data_ptr(), int(steps),
