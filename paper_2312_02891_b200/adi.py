@@ -366,21 +366,32 @@ class AdiState:
     inner_residuals_A: list
     inner_residuals_B: list
     keep_inner_residuals: bool
+    #: device-resident runs: the z_k / y_k blocks (Z / Y stay None until asked)
+    z_blocks: list = None
+    y_blocks: list = None
 
     def solution(self, r):
         return LowRankSolution(Z=self.Z, gammas=self.gammas, Y=self.Y, r=r)
 
+    @staticmethod
+    def _hstack(blocks, rows):
+        if not blocks:
+            return np.zeros((rows, 0), dtype=complex)
+        if hasattr(blocks[0], "data_ptr"):            # device blocks
+            return LowRankSolution._stack(list(blocks), rows, blocks[0].shape[1])
+        return np.hstack(blocks)
+
     def S_A(self):
+        """adi.py:334-337 (device blocks are downloaded)."""
         if not self.keep_inner_residuals:
             raise ValueError("inner residual blocks were not retained")
-        return (np.hstack(self.inner_residuals_A) if self.inner_residuals_A
-                else np.zeros((self.w.shape[0], 0), dtype=complex))
+        return self._hstack(self.inner_residuals_A, self.w.shape[0])
 
     def S_B(self):
+        """adi.py:339-342."""
         if not self.keep_inner_residuals:
             raise ValueError("inner residual blocks were not retained")
-        return (np.hstack(self.inner_residuals_B) if self.inner_residuals_B
-                else np.zeros((self.t.shape[0], 0), dtype=complex))
+        return self._hstack(self.inner_residuals_B, self.t.shape[0])
 
 
 # -- the paper's tolerance strategies (host scalars) --------------------------
@@ -564,12 +575,15 @@ class DeviceAdi:
         self.solver = solver
         # the outer loop in native code (sad_adi_run) for the persistent GMRES
         # engine; the Python loop below stays the reference implementation
+        # (keep_inner_residuals: the Python loop retains each step's inner
+        # residual blocks, adi.py:533-535; the native loop reuses one buffer)
         self.native = (native is True or native == "auto") and engine == "persistent" \
             and solver == "gmres" and row_ranks == 1 and problem.r <= 8 \
-            and _strategy(config.strategy).value in _lib.STRATEGY_CODES
+            and _strategy(config.strategy).value in _lib.STRATEGY_CODES \
+            and not config.keep_inner_residuals
         if native is True and not self.native:
-            raise ValueError("native outer loop needs the persistent GMRES engine, r <= 8 and "
-                             "an iterative strategy")
+            raise ValueError("native outer loop needs the persistent GMRES engine, r <= 8, "
+                             "an iterative strategy and keep_inner_residuals=False")
         if concurrent == "auto":
             # Small blocks are latency-bound: the two solves overlap on disjoint
             # SM sets.  Large blocks are HBM-bound: one solve at a time on every
@@ -738,11 +752,13 @@ class DeviceAdi:
         res0 = product_norm_from_grams(Gw, Gt)
         report = SolveReport(rhs_norm=res0, strategy=cfg.strategy)
         zb, yb, gammas, hist = [], [], [], []
+        keep = bool(cfg.keep_inner_residuals)
+        sa_blocks, sb_blocks = [], []
         u = v = 0.0
         if res0 == 0.0:
             report.converged = True
             report.final_scaled_residual = 0.0
-            return self._finish(report, zb, yb, gammas, hist, w, t, u, v, 0, t0)
+            return self._finish(report, zb, yb, gammas, hist, w, t, u, v, 0, t0, keep=keep)
         gap = cfg.gap_budget if cfg.gap_budget is not None else cfg.outer_tolerance * res0
         res = res0
         k_done = 0
@@ -773,6 +789,9 @@ class DeviceAdi:
             yb.append(y)
             gammas.append(gam)
             hist.append((alpha, beta))
+            if keep:      # adi.py:533-535 (fresh device blocks every step)
+                sa_blocks.append(ra.residual)
+                sb_blocks.append(rb.residual)
             k_done = k
             Gw, Gt = G[4], G[5]
             res = product_norm_from_grams(Gw, Gt)
@@ -783,7 +802,8 @@ class DeviceAdi:
         report.converged = bool(res < cfg.outer_tolerance * res0)
         report.final_scaled_residual = res / res0
         report.device_timing["inner_solve_ms"] = solve_ms
-        return self._finish(report, zb, yb, gammas, hist, w, t, u, v, k_done, t0)
+        return self._finish(report, zb, yb, gammas, hist, w, t, u, v, k_done, t0,
+                            keep=keep, sa=sa_blocks, sb=sb_blocks)
 
     def _solve_pair(self, beta, w, dA, z, alpha, t, dB, y):
         import torch
@@ -816,14 +836,16 @@ class DeviceAdi:
         cur.wait_stream(self.sB)
         return ra, rb
 
-    def _finish(self, report, zb, yb, gammas, hist, w, t, u, v, k_done, t0):
+    def _finish(self, report, zb, yb, gammas, hist, w, t, u, v, k_done, t0, keep=False,
+                sa=(), sb=()):
         import torch
         torch.cuda.synchronize(self.dev)
         report.outer_iterations = k_done
         report.wall_ms = 1000.0 * (time.perf_counter() - t0)
         sol = LowRankSolution(gammas=gammas, r=self.problem.r, z_blocks=zb, y_blocks=yb,
                               n=self.problem.n, m=self.problem.m)
-        state = AdiState(k_done, None, None, gammas, w, t, u, v, hist, [], [], False)
+        state = AdiState(k_done, None, None, gammas, w, t, u, v, hist, list(sa), list(sb),
+                         bool(keep), z_blocks=zb, y_blocks=yb)
         return sol, report, state
 
 
@@ -847,8 +869,11 @@ def _run_device(problem, config, shifts, restart, flexible, device, concurrent,
     t2 = time.perf_counter()
     if not keep_on_device:
         state.Z, state.Y = sol.Z, sol.Y
+        state.z_blocks = state.y_blocks = None
         state.w = state.w.cpu().numpy().astype(complex)
         state.t = state.t.cpu().numpy().astype(complex)
+        state.inner_residuals_A = [b.cpu().numpy().astype(complex) for b in state.inner_residuals_A]
+        state.inner_residuals_B = [b.cpu().numpy().astype(complex) for b in state.inner_residuals_B]
     rep.device_timing.update(construct_ms=1e3 * (t1 - t0), run_ms=1e3 * (t2 - t1),
                              download_ms=1e3 * (time.perf_counter() - t2))
     return sol, rep, state

@@ -94,10 +94,6 @@ static std::atomic<long long> g_launches{0};   // kernels launched by this libra
 namespace sad {
 void count_launches(long long k) { COUNT_LAUNCH(k); }
 int g_spmm_bulk_sms = 148;
-int g_spmm_xpf = [] {
-  const char* e = getenv("SAD_SPMM_XPF");
-  return e ? atoi(e) : 1;
-}();
 }
 
 struct sad_op {

@@ -405,7 +405,6 @@ struct SpmmArgs {
   XT* zout;          // FGMRES Z base pointer (ARNOLDI, may be null)
   double2 sigma;
   long long stride;  // elements per basis block (n*R)
-  int xpf;           // bulk SpMM: L2-prefetch each staged tile's diagonal rows of x
   long long row0;    // bulk APPLY/RESID on a row range: global row of local row 0
                      // (rowptr, y, b are offset by the caller; x, dinv are global)
   GState st;

@@ -43,10 +43,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
   }
 }
-// L2 prefetch of a global byte range (16-byte aligned, size a multiple of 16)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -139,21 +135,34 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
 
   if (warp == kWarps) {
     // ---------------- producer ----------------
-    if (lane == 0) {
-      // x rows of a tile's diagonal block: their first touch is usually by
-      // this tile or by a concurrently running neighbour tile (banded
-      // operators), so they are prefetched into L2 when the tile's CSR slice
-      // is staged, STAGES tiles ahead, instead of being a DRAM round trip on
-      // the consumers' critical path
-      const XT* xpf_base = a.x;
-      if (MODE == SPMM_ARNOLDI) xpf_base = a.x + (long long)(*a.st.j) * a.stride;
-      for (long long k = 0; k < K; ++k) {
+    // The whole warp fetches the row ranges (rowptr at the tile boundaries) of
+    // 32 tiles at once, one tile per lane, a batch ahead of their use; lane 0
+    // then issues each tile's copies with the range taken by shuffle, so the
+    // rowptr round trip is paid once per 32 tiles instead of once per tile.
+    auto range = [&](long long kk, int& kb, int& ke) {
+      if (kk < K) {
+        const long long r0 = (blockIdx.x + kk * G) * (long long)TR;
+        const int rows = (int)min((long long)TR, a.n - r0);
+        kb = __ldg(a.rowptr + r0);
+        ke = __ldg(a.rowptr + r0 + rows);
+      }
+    };
+    int kb_cur = 0, ke_cur = 0, kb_nxt = 0, ke_nxt = 0;
+    range(lane, kb_cur, ke_cur);
+    range(32 + lane, kb_nxt, ke_nxt);
+    for (long long k = 0; k < K; ++k) {
+      const int l = (int)(k & 31);
+      if (l == 0 && k > 0) {
+        kb_cur = kb_nxt;
+        ke_cur = ke_nxt;
+        range(k + 32 + lane, kb_nxt, ke_nxt);
+      }
+      const int kb = __shfl_sync(0xffffffffu, kb_cur, l);
+      const int ke = __shfl_sync(0xffffffffu, ke_cur, l);
+      if (lane == 0) {
         const int st = (int)(k % S);
-        // the tile's row range is loaded before waiting for the free stage, so
-        // its global round trip overlaps the consumers' work
         const long long r0 = (blockIdx.x + k * G) * (long long)TR;
         const int rows = (int)min((long long)TR, a.n - r0);
-        const int kb = __ldg(a.rowptr + r0), ke = __ldg(a.rowptr + r0 + rows);
         if (k >= S) mbar_wait(empty + st, (unsigned)(((k / S) - 1) & 1));
         const int nz = ke - kb;
         unsigned long long p0, p1, c0, c1, v0, v1;
@@ -180,12 +189,8 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
           if (c1 > c0) bulk_g2s(base, reinterpret_cast<const void*>(c0), (unsigned)(c1 - c0), full + st);
           if (v1 > v0) bulk_g2s(base + CI, reinterpret_cast<const void*>(v0), (unsigned)(v1 - v0), full + st);
         }
-        if (a.xpf) {
-          unsigned long long x0, x1;
-          aligned_range(xpf_base, (r0 + a.row0) * R, (long long)rows * R, (int)sizeof(XT), x0, x1);
-          if (x1 > x0) bulk_prefetch_l2(reinterpret_cast<const void*>(x0), (unsigned)(x1 - x0));
-        }
       }
+      __syncwarp();
     }
     return;
   }
@@ -233,9 +238,14 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
         }
         maxlen = max(maxlen, len[u]);
       }
-      XT acc[U];
+      XT acc[U], xd[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = zero<XT>();
+      for (int u = 0; u < U; ++u) {
+        acc[u] = zero<XT>();
+        // the diagonal x entry (shift term / FGMRES Z), loaded with the gathers
+        xd[u] = zero<XT>();
+        if ((SIGMA || (MODE == SPMM_ARNOLDI && zout)) && idx[u] >= 0) xd[u] = x[idx[u] + a.row0 * R];
+      }
       constexpr int KB = SAD_BULK_KB;
       for (int q = 0; q < maxlen; q += KB) {
         XT xg[U][KB];
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kThreads + 32, bulk_min_blocks<XT, R>()) k_spm
         XT vres = acc[u];
         if (SIGMA || (MODE == SPMM_ARNOLDI && zout)) {
           const long long gidx = idx[u] + a.row0 * R;
-          XT xi = x[gidx];
+          XT xi = xd[u];
           if (PRE) xi = mul(__ldg(a.dinv + gidx / R), xi);
           if (SIGMA) vres = fma_(from_c<XT>(a.sigma), xi, vres);
           if (MODE == SPMM_ARNOLDI && zout) zout[idx[u]] = sscal(scale, xi);

@@ -39,9 +39,7 @@ static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
     }
     const long long tiles = (a.n + BulkTile<R>::TR - 1) / BulkTile<R>::TR;
     const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_spmm_bulk_sms));
-    SpmmArgs<XT> ab = a;
-    ab.xpf = g_spmm_xpf;
-    kern<<<g, kThreads + 32, smem, s>>>(ab);
+    kern<<<g, kThreads + 32, smem, s>>>(a);
     count_launches(1);
   } else {
     k_spmm<XT, VT, R, MODE, PRE, SIGMA><<<grid, kThreads, 0, s>>>(a);

@@ -11,7 +11,6 @@ namespace sad {
 
 void count_launches(long long k);   // defined in sad_capi.cu
 extern int g_spmm_bulk_sms;         // SMs for the persistent-style SpMM grids (sad_capi.cu)
-extern int g_spmm_xpf;              // bulk SpMM x-diagonal L2 prefetch (SAD_SPMM_XPF, default 1)
 
 // Returns 0, or 1 for an unsupported block width.
 template <typename XT, int MODE>

@@ -282,10 +282,15 @@ def verify_goldens():
             sol, rep, state = sv.run_with_state(problem, cfg, seq)
         trn = sv.true_residual_norm(problem, sol)
         gap = sv.residual_gap(problem, state)
+        fid = sv.verify_factor_identity(problem, state)
         path = os.path.join(GOLD, f"ref_verify_{name}.npz")
         np.savez_compressed(path, Z=sol.Z, Y=sol.Y, gdiag=sol.gamma_diag(),
                             true_residual_norm=trn, residual_gap=gap,
-                            steps=rep.outer_iterations)
+                            steps=rep.outer_iterations,
+                            S_A=state.S_A(), S_B=state.S_B(), w=state.w, t=state.t,
+                            gammas=np.asarray(state.gammas, dtype=complex),
+                            shift_history=np.asarray(state.shift_history, dtype=complex),
+                            u=state.u, v=state.v, factor_identity=fid)
         print(f"{path}: {rep.outer_iterations} steps, true residual {trn:.6e}, gap {gap:.6e}")
 
 

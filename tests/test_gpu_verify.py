@@ -84,3 +84,72 @@ def test_true_residual_of_converged_device_run():
     assert abs(dev - host) <= 1e-6 * host, (dev, host)
     fg = np.linalg.norm(f) * np.linalg.norm(g)   # = ||f g^*||_2 for r = 1
     assert dev <= 2.0 * cfg.outer_tolerance * fg, dev / fg
+
+
+def _golden_state(gold, r):
+    import paper_2312_02891_b200 as pb
+    k = int(gold["steps"])
+    SA, SB = gold["S_A"], gold["S_B"]
+    return pb.AdiState(k, gold["Z"], gold["Y"], list(gold["gammas"]), gold["w"], gold["t"],
+                       float(gold["u"]), float(gold["v"]),
+                       [tuple(p) for p in gold["shift_history"]],
+                       [SA[:, j * r:(j + 1) * r] for j in range(k)],
+                       [SB[:, j * r:(j + 1) * r] for j in range(k)], True)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_gap_and_factor_identity_match_reference(name):
+    """Device residual_gap / verify_factor_identity (adi.py:632-679) on the
+    state the reference's driver retained: the gap equals the reference's
+    value, the identity holds to rounding as in the reference, and a defect
+    the identity does not absorb (S^A dropped) equals the oracle's value."""
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200.verify import residual_gap, verify_factor_identity
+    gold = np.load(os.path.join(GOLD, f"ref_verify_{name}.npz"))
+    A, B, M, C, f, g = cfgs.build_problem(name)
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
+    r = f.shape[1]
+    st = _golden_state(gold, r)
+    gap = residual_gap(prob, st)
+    want = float(gold["residual_gap"])
+    assert abs(gap - want) <= 1e-9 * want, (gap, want)
+    fid = verify_factor_identity(prob, st)
+    assert fid <= 1e-15, fid
+    st.inner_residuals_A = [np.zeros_like(b) for b in st.inner_residuals_A]
+    fid0 = verify_factor_identity(prob, st)
+    hist = [tuple(p) for p in gold["shift_history"]]
+    want0 = orc.verify_factor_identity(A, B, np.zeros_like(gold["S_A"]), gold["S_B"], gold["Z"],
+                                       gold["Y"], gold["w"], gold["t"], gold["gammas"], hist, r,
+                                       M=M, C=C)
+    assert abs(fid0 - want0) <= 1e-10 * want0, (fid0, want0)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_device_run_retains_inner_residuals(name):
+    """keep_inner_residuals=True (adi.py:533-535) on the device driver: S^A and
+    S^B are retained per step, the gap they give equals the oracle's on the
+    downloaded blocks, it is bounded by the running estimate u + v, and the
+    factor identities hold to rounding."""
+    import paper_2312_02891_b200 as pb
+    from paper_2312_02891_b200.verify import residual_gap, verify_factor_identity
+    spec = cfgs.CONFIGS[name]
+    A, B, M, C, f, g = cfgs.build_problem(name)
+    pairs, cyclic = spec.load_shift_pairs()
+    prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
+    cfg = pb.AdiConfig(strategy=spec.strategy, kmax=12, precond_kind_A="jacobi",
+                       precond_kind_B="jacobi", keep_inner_residuals=True)
+    seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
+    eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible)
+    assert not eng.native
+    sol, rep, st = eng.run()
+    k, r = rep.outer_iterations, prob.r
+    SA, SB = st.S_A(), st.S_B()
+    assert SA.shape == (prob.n, k * r) and SB.shape == (prob.m, k * r)
+    gap = residual_gap(prob, st)
+    want = orc.residual_gap(A, B, SA, SB, sol.Z, sol.Y, st.gammas, r, M=M, C=C)
+    assert abs(gap - want) <= 1e-8 * want, (gap, want)
+    assert gap <= (st.u + st.v) * (1 + 1e-8)
+    assert verify_factor_identity(prob, st) <= 1e-13
+    # the public run() returns host blocks that the host oracle accepts too
+    sol2, rep2 = pb.run(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible)
+    assert rep2.outer_iterations == k

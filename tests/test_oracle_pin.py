@@ -192,6 +192,32 @@ def test_true_residual_norm_matches_reference(name):
     assert abs(got - want) <= 1e-9 * want, (got, want)
 
 
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_residual_gap_and_factor_identity_match_reference(name):
+    """oracle.residual_gap / verify_factor_identity reproduce the reference's
+    values (adi.py:632-679) on the state its driver retained
+    (keep_inner_residuals=True; ref_verify_<name>.npz)."""
+    gold = np.load(os.path.join(GOLD, f"ref_verify_{name}.npz"))
+    A, B, M, C, f, g = cfgs.build_problem(name)
+    r = f.shape[1]
+    args = (A, B, gold["S_A"], gold["S_B"], gold["Z"], gold["Y"])
+    gap = orc.residual_gap(*args, gold["gammas"], r, M=M, C=C)
+    want = float(gold["residual_gap"])
+    assert abs(gap - want) <= 1e-10 * want, (gap, want)
+    hist = [tuple(p) for p in gold["shift_history"]]
+    fid = orc.verify_factor_identity(*args, gold["w"], gold["t"], gold["gammas"], hist, r,
+                                     M=M, C=C)
+    # the identity holds to rounding: both values are at the roundoff level
+    assert fid <= 1e-15 and float(gold["factor_identity"]) <= 1e-15, (fid, gold["factor_identity"])
+    # a defect the identity does not absorb: dropping S^A leaves ||S^A|| / scale
+    # on the A side, the same number in the reference's formula
+    S0 = np.zeros_like(gold["S_A"])
+    fid0 = orc.verify_factor_identity(A, B, S0, gold["S_B"], gold["Z"], gold["Y"], gold["w"],
+                                      gold["t"], gold["gammas"], hist, r, M=M, C=C)
+    scale = np.linalg.norm(A.data) * np.linalg.norm(gold["Z"])
+    assert abs(fid0 - np.linalg.norm(gold["S_A"]) / scale) <= 1e-6 * fid0
+
+
 # -- MINRES (krylov.py:187-287), pinned to the reference's own outputs -----------
 
 MINRES_CASES = [("def_jac", None, False, "jacobi"), ("indef_jac", None, False, "jacobi"),

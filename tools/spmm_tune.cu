@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <vector>
 #include <random>
+#include <cmath>
 #include "../paper_2312_02891_b200/csrc/sad_spmm_bulk.cuh"
 using namespace sad;
 int main(int argc, char** argv) {
@@ -30,7 +31,11 @@ int main(int argc, char** argv) {
   cudaMemcpy(drp, rp.data(), (n + 1) * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dci, ci.data(), nnz * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dv, v.data(), nnz * 8, cudaMemcpyHostToDevice);
-  cudaMemset(dx, 0, n * 64);
+  {
+    std::vector<double> hx(n * 8);
+    for (long long i = 0; i < n * 8; ++i) hx[i] = std::sin(0.001 * (double)i) + 0.5;
+    cudaMemcpy(dx, hx.data(), n * 64, cudaMemcpyHostToDevice);
+  }
   SpmmArgs<double2> a{};
   a.n = n; a.rowptr = drp; a.colidx = dci; a.vals = dv; a.x = dx; a.y = dy;
   a.sigma = make_double2(-1e6, 0.0);
