@@ -12,6 +12,11 @@ if REPO not in sys.path:
     sys.path.insert(0, REPO)
 
 GOLD = os.path.join(REPO, "tests", "golden")
+#: the reference package installed by oracle/build_ref.py (git-ignored, shipped
+#: to the GPU box): the drop-in tests run its own driver and front end
+REF_INSTALL = os.path.join(REPO, "oracle", "_ref")
+if os.path.isdir(REF_INSTALL) and REF_INSTALL not in sys.path:
+    sys.path.append(REF_INSTALL)
 
 
 def pytest_configure(config):

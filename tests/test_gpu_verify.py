@@ -121,7 +121,9 @@ def test_gap_and_factor_identity_match_reference(name):
     want0 = orc.verify_factor_identity(A, B, np.zeros_like(gold["S_A"]), gold["S_B"], gold["Z"],
                                        gold["Y"], gold["w"], gold["t"], gold["gammas"], hist, r,
                                        M=M, C=C)
-    assert abs(fid0 - want0) <= 1e-10 * want0, (fid0, want0)
+    # the defect is ||S^A|| / scale plus the identity's own rounding (about
+    # 1e-18 of the scale, i.e. ~1e-6 of this value)
+    assert abs(fid0 - want0) <= 1e-6 * want0, (fid0, want0)
 
 
 @pytest.mark.parametrize("name", ["c1", "c3s"])
