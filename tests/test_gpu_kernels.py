@@ -1,11 +1,15 @@
 """GPU parity of the kernels through the C-ABI, against the CPU oracle."""
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
 
 from oracle import sylvadi_oracle as orc
 from paper_2312_02891_b200 import configs as cfgs
+
+from conftest import GOLD
 
 pytestmark = pytest.mark.gpu
 
@@ -252,6 +256,24 @@ def test_gmres_fixed_steps_match_oracle(rng, engine):
                      orth=dict(ENGINES)[engine])
     want = ob.solve(-5000.0, rhs, 1e-300 * 8)
     rel = np.abs(out.achieved_residual_norms - want.achieved_residual_norms) / want.achieved_residual_norms
+    assert np.all(rel < 1e-6), rel
+
+
+@pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
+def test_gmres_c4_fixed_steps_1024_golden(engine):
+    """Config 4's path at depth: 100 fixed Jacobi-GMRES(100) steps,
+    r = 8, on the config-4 operator at 1024^2 (1M rows: many tiles per block, the
+    TMA ring of phase A, a 100-block basis) against the oracle's per-column true
+    residual norms (tests/golden/make_golden_c4.py)."""
+    from paper_2312_02891_b200 import GpuGmresBinding
+    gold = np.load(os.path.join(GOLD, "oracle_c4_1024_fixed.npz"))
+    n0, r, steps, shift = int(gold["n0"]), int(gold["r"]), int(gold["steps"]), float(gold["shift"])
+    A, X = cfgs.build_c4(n0, r, 0)
+    gb = GpuGmresBinding("A", A, None, restart=steps, **_binding_kw(engine))
+    out = gb.solve_device(shift, torch.from_numpy(X).cuda(), 1.0, fixed_steps=steps)
+    assert np.all(out.iterations == steps)
+    want = gold[dict(ENGINES)[engine]]
+    rel = np.abs(out.achieved_residual_norms - want) / want
     assert np.all(rel < 1e-6), rel
 
 
