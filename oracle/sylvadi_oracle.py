@@ -251,7 +251,12 @@ def _bicgstab_column(op, dinv, b, tol, maxit):
     r = b.copy()
     if np.linalg.norm(r) <= tol:
         return x, 0
-    pre = (lambda v: v.copy()) if dinv is None else (lambda v: v * dinv)
+    if dinv is None:
+        pre = lambda v: v.copy()                      # noqa: E731
+    elif hasattr(dinv, "apply"):                      # incomplete factorisation (oracle/precond.py)
+        pre = lambda v: dinv.apply(v)                 # noqa: E731
+    else:
+        pre = lambda v: v * dinv                      # noqa: E731
     rhat = r.copy()
     rho = alpha = omega = 1.0 + 0.0j
     v = np.zeros(n, dtype=np.complex128)
@@ -356,8 +361,11 @@ def _minres_column(op, dinv, b, tol, maxit):
     x = np.zeros(n, dtype=np.complex128)
     if np.linalg.norm(b) <= tol:
         return x, 0
-    pabs = None if dinv is None else np.abs(dinv)
-    psolve = (lambda v: v.copy()) if pabs is None else (lambda v: v * pabs)
+    if hasattr(dinv, "apply_spd"):                    # Cholesky kinds: (G G^H)^-1 (precond.py:242-256)
+        psolve = lambda v: dinv.apply_spd(v)          # noqa: E731
+    else:
+        pabs = None if dinv is None else np.abs(dinv)
+        psolve = (lambda v: v.copy()) if pabs is None else (lambda v: v * pabs)
     r1 = b.astype(np.complex128)
     y = psolve(r1)
     beta1_sq = np.vdot(r1, y).real
@@ -593,7 +601,8 @@ class Binding:
     """
 
     def __init__(self, side, base, mass, solver="gmres", max_iterations=1000,
-                 restart=50, precond="jacobi", orth="cgs2"):
+                 restart=50, precond="jacobi", orth="cgs2", droptol=0.1):
+        self.droptol = droptol
         self.side = side
         self.base = base
         self.mass = mass
@@ -609,7 +618,17 @@ class Binding:
         hit = self._ops.get(shift)
         if hit is None:
             op = ShiftedOp(self.base, self.mass, shift, adjoint=(self.side == "B"))
-            dinv = jacobi_dinv(op) if self.precond == "jacobi" else None
+            if self.precond in ("ilu0", "ilut", "ic0", "ict"):
+                # adi.py:453-466: factorise the assembled matrix, Jacobi on breakdown
+                from . import precond as _pc
+                try:
+                    dinv = _pc.factorize(_pc.assembled(op), self.precond, self.droptol)
+                except _pc.FactorizationBreakdown as exc:
+                    warnings.warn(f"{self.side}-side {self.precond} factorization broke down "
+                                  f"at shift {shift} ({exc}); falling back to Jacobi")
+                    dinv = jacobi_dinv(op)
+            else:
+                dinv = jacobi_dinv(op) if self.precond == "jacobi" else None
             hit = (op, dinv)
             self._ops[shift] = hit
         return hit
@@ -619,7 +638,7 @@ class Binding:
         if self.solver == "minres":
             return True
         return (self.solver == "reference" and complex(shift).imag == 0.0
-                and self.precond in ("none", "jacobi") and is_symmetric(self.base)
+                and self.precond in ("none", "jacobi", "ic0", "ict") and is_symmetric(self.base)
                 and (self.mass is None or is_symmetric(self.mass)))
 
     def solve(self, shift, rhs, delta):
