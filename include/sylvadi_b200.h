@@ -50,7 +50,10 @@ enum sad_option { SAD_OPT_ENGINE = 0, SAD_OPT_MAX_SMS = 1, SAD_OPT_MIN_ELEMS_PER
                   SAD_OPT_DIST_ORTH = 5, /* row-partitioned: 1 (default) delayed-Gram CGS2, 0 CGS2 */
                   SAD_OPT_DEBUG_DELAY = 6 /* tests: the persistent kernel's last block idles this
                                              many ns after every phase-C barrier (race stress) */ };
-enum sad_precond { SAD_PRECOND_NONE = 0, SAD_PRECOND_JACOBI = 1 };
+/* precond.py:15 KINDS.  NONE / JACOBI are folded into the operator (sad_op_create);
+ * the incomplete factorisations are separate handles (sad_pc_create). */
+enum sad_precond { SAD_PRECOND_NONE = 0, SAD_PRECOND_JACOBI = 1, SAD_PRECOND_ILU0 = 2,
+                   SAD_PRECOND_ILUT = 3, SAD_PRECOND_IC0 = 4, SAD_PRECOND_ICT = 5 };
 
 typedef struct sad_ctx sad_ctx;
 typedef struct sad_csr sad_csr;
@@ -60,6 +63,7 @@ typedef struct sad_comm sad_comm;
 typedef struct sad_halo sad_halo;
 typedef struct sad_bicg sad_bicg;
 typedef struct sad_minres sad_minres;
+typedef struct sad_pc sad_pc;
 
 /* ABI version (bumped on any signature change). */
 int sad_version(void);
@@ -332,6 +336,50 @@ int64_t sad_minres_bytes(const sad_minres* ws);
 int sad_minres_solve(sad_minres* ws, sad_op* op, const void* rhs_dev, void* x_dev,
                      void* res_dev, double tol_col, int maxit, void* stream,
                      int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
+
+/* ---------------------------------------------------------------------------
+ * Incomplete-factorisation preconditioners (the paper's iLU / iC(., 0.1),
+ * PAPER.md:638-649).  sad_pc_create replaces factorize(op.assembled(), kind,
+ * droptol, shift) (precond.py:307-357) as called by SolverBinding._factorization
+ * (adi.py:453-466): the assembled shifted matrix base + shift*mass (mass NULL =
+ * identity; conjugate-transposed when adjoint), the row-wise IKJ incomplete LU
+ * with threshold dropping (ILUT / ICT: |l_ik| < droptol * ||row||_2 dropped,
+ * U entries kept when >= it) or restricted to the matrix pattern (ILU0 / IC0)
+ * (precond.py:34-125) and, for the Cholesky kinds, the negation of a negative
+ * definite matrix and the fold G = L sqrt(D) (precond.py:279-304, 338-346).
+ * The factorisation is computed once per shift on the host (a sequential
+ * recurrence with a data-dependent pattern), bit-identical to the reference's;
+ * the triangular solves run on the device.  SAD_EBREAKDOWN = the reference's
+ * FactorizationBreakdown (zero pivot, or not positive definite up to dropping).
+ *
+ * sad_pc_apply: y = M^-1 x, IncompleteFactorization.apply (precond.py:224-240,
+ * including the sign of a negated Cholesky process); spd != 0: apply_spd
+ * (precond.py:242-256), (G G^H)^-1 x, Cholesky kinds only.  y may alias x.
+ * One handle serves one stream at a time.
+ * sad_pc_info: info[8] = kind, n, nnz of L (or G), nnz of U (0 for Cholesky),
+ * complex factors (0/1), dependency levels of the first and second triangular
+ * solve, sign.  sad_pc_get_factor: the reference's raw triplets (which = 0: L
+ * without its unit diagonal, or G with the diagonal last in each row; which = 1:
+ * U with the diagonal first), data interleaved complex128.
+ * sad_bicg_solve_pc / sad_minres_solve_pc: the solvers above with the
+ * preconditioner argument of InnerSolveRequest (krylov.py:23) given as a handle
+ * (NULL = the operator's own none / Jacobi); the operator passed with a BiCGstab
+ * handle must be created with SAD_PRECOND_NONE.
+ * ------------------------------------------------------------------------- */
+int sad_pc_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* mass, double shift_re,
+                  double shift_im, int adjoint, int kind, double droptol, sad_pc** out);
+int sad_pc_destroy(sad_pc* pc);
+int sad_pc_info(const sad_pc* pc, int64_t* info);
+int sad_pc_get_factor(const sad_pc* pc, int which, int64_t* indptr, int64_t* indices,
+                      double* data_ri);
+int sad_pc_apply(sad_pc* pc, int r, int dtype, const void* x_dev, void* y_dev, int spd,
+                 void* stream);
+int sad_bicg_solve_pc(sad_bicg* ws, sad_op* op, sad_pc* pc, const void* rhs_dev, void* x_dev,
+                      void* res_dev, double tol_col, int maxit, void* stream, int64_t* iters_host,
+                      double* resnorm_host, uint8_t* conv_host);
+int sad_minres_solve_pc(sad_minres* ws, sad_op* op, sad_pc* pc, const void* rhs_dev, void* x_dev,
+                        void* res_dev, double tol_col, int maxit, void* stream,
+                        int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
 
 /* ---------------------------------------------------------------------------
  * The device-resident ADI outer loop in native code: run_with_state

@@ -27,7 +27,8 @@ UNITS = [("sad_capi", "sad_capi.cu", [])] + [
     (f"sad_spmm_{p}", "sad_spmm_launch.cu", [f"-DSAD_SPMM_PART={p}"]) for p in range(4)] + [
     (f"sad_coop_{v}", "sad_coop.cu", [f"-DSAD_COOP_VARIANT={v}"]) for v in range(N_COOP_VARIANTS)] + [
     (f"sad_bicg_{p}", "sad_bicg.cu", [f"-DSAD_BICG_PART={p}"]) for p in range(2)] + [
-    (f"sad_minres_{p}", "sad_minres.cu", [f"-DSAD_MINRES_PART={p}"]) for p in range(2)]
+    (f"sad_minres_{p}", "sad_minres.cu", [f"-DSAD_MINRES_PART={p}"]) for p in range(2)] + [
+    ("sad_precond", "sad_precond.cu", [])]
 HEADERS = sorted(glob.glob(os.path.join(SRC_DIR, "*.cuh"))) + [
     os.path.join(REPO, "include", "sylvadi_b200.h")]
 DEPS = [os.path.join(SRC_DIR, s) for s in {u[1] for u in UNITS}] + HEADERS

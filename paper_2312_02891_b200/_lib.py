@@ -15,6 +15,8 @@ LIB_PATH = os.environ.get("SAD_LIB_PATH") or os.path.join(_HERE, "libsylvadi_b20
 SAD_OK, SAD_EINVAL, SAD_EBREAKDOWN, SAD_ECUDA, SAD_ENCCL, SAD_ENOMEM = range(6)
 SAD_F64, SAD_C128 = 0, 1
 SAD_PRECOND_NONE, SAD_PRECOND_JACOBI = 0, 1
+SAD_PRECOND_ILU0, SAD_PRECOND_ILUT, SAD_PRECOND_IC0, SAD_PRECOND_ICT = 2, 3, 4, 5
+PRECOND_CODES = {"none": 0, "jacobi": 1, "ilu0": 2, "ilut": 3, "ic0": 4, "ict": 5}
 SAD_ENGINE_MULTI, SAD_ENGINE_PERSISTENT = 0, 1
 SAD_OPT_ENGINE, SAD_OPT_MAX_SMS, SAD_OPT_MIN_ELEMS_PER_THREAD, SAD_OPT_DIRECT_A = 0, 1, 2, 3
 SAD_OPT_RESIDENT_CSR = 4
@@ -101,6 +103,17 @@ SIGNATURES = {
     "sad_minres_bytes": (_i64, [_vp]),
     "sad_minres_solve": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp, _vp,
                                     _vp, _vp]),
+    # incomplete-factorisation preconditioners
+    "sad_pc_create": (_c.c_int, [_vp, _vp, _vp, _c.c_double, _c.c_double, _c.c_int, _c.c_int,
+                                 _c.c_double, _c.POINTER(_vp)]),
+    "sad_pc_destroy": (_c.c_int, [_vp]),
+    "sad_pc_info": (_c.c_int, [_vp, _vp]),
+    "sad_pc_get_factor": (_c.c_int, [_vp, _c.c_int, _vp, _vp, _vp]),
+    "sad_pc_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _c.c_int, _vp]),
+    "sad_bicg_solve_pc": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int, _vp,
+                                     _vp, _vp, _vp]),
+    "sad_minres_solve_pc": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c.c_double, _c.c_int,
+                                       _vp, _vp, _vp, _vp]),
     # native ADI outer loop
     "sad_adi_run": (_c.c_int, [_vp, _vp, _c.c_int, _c.c_int, _i64, _i64, _vp, _vp, _vp, _vp,
                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -123,7 +136,8 @@ STRATEGY_CODES = {"fixed": 0, "dynamic_mid": 1, "dynamic_mid_bl": 2, "dynamic_b"
 
 
 class FactorizationBreakdown(RuntimeError):
-    """Zero Jacobi diagonal (the reference's precond.FactorizationBreakdown)."""
+    """Zero Jacobi diagonal, zero pivot or an indefinite matrix for the Cholesky
+    kinds (the reference's precond.FactorizationBreakdown)."""
 
 
 class DeviceError(RuntimeError):

@@ -624,10 +624,12 @@ class DeviceAdi:
             self._init_tail(problem)
             return
         self.bA = GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
+                                  config.precond_droptol_A,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
                                   max_sms=sm_a, phase_a=phase_a, solver=solver)
         self.bB = GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
+                                  config.precond_droptol_B,
                                   max_iterations=config.max_inner_iterations, restart=restart,
                                   flexible=flexible, device=device, engine=engine,
                                   max_sms=sm_b, phase_a=phase_a, solver=solver)

@@ -66,6 +66,11 @@ struct BArgs {
   const void* dinv;
   const void* b;
   void *x, *dx, *r, *rhat, *p, *v, *s, *t;
+  // general right preconditioner (incomplete factorisations, sad_precond_host.cuh):
+  // phat = M^-1 p and shat = M^-1 s computed between the kernels; nullptr = the
+  // fused Jacobi scaling by dinv
+  const void* phat;
+  const void* shat;
   BState st;
 };
 
@@ -305,6 +310,8 @@ __global__ void __launch_bounds__(kThreads) k_bi_vec(BArgs a) {
   const XT* v = reinterpret_cast<const XT*>(a.v);
   XT* s = reinterpret_cast<XT*>(a.s);
   const XT* t = reinterpret_cast<const XT*>(a.t);
+  const XT* phat = reinterpret_cast<const XT*>(a.phat);
+  const XT* shat = reinterpret_cast<const XT*>(a.shat);
   // column flags and coefficients (read once)
   int on = 0, fr = 0, rm = 0;
   XT cb = zero<XT>(), co = zero<XT>(), ca = zero<XT>();
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_vec(BArgs a) {
       } else if (K == BI_SUPD) {
         const XT sv = sub(r[e], mul(ca, v[e]));
         s[e] = sv;
-        const XT ph = mul(dinv[row], p[e]);
+        const XT ph = phat ? phat[e] : mul(dinv[row], p[e]);
         dx[e] = add(dx[e], mul(ca, ph));
         q[0] += abs2(sv);
       } else if (K == BI_RUPD) {
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_vec(BArgs a) {
           r[e] = rv;
           rhat[e] = rh;
         } else {
-          const XT sh = mul(dinv[row], sv);
+          const XT sh = shat ? shat[e] : mul(dinv[row], sv);
           dx[e] = add(dx[e], mul(co, sh));
           rv = sub(sv, mul(co, t[e]));
           r[e] = rv;
@@ -401,7 +408,9 @@ __global__ void __launch_bounds__(kThreads) k_bi_spmm(BArgs a) {
   const BState& st = a.st;
   const VT* vals = reinterpret_cast<const VT*>(a.vals);
   const XT* dinv = reinterpret_cast<const XT*>(a.dinv);
-  const XT* in = reinterpret_cast<const XT*>(K == BI_SPMM_P ? a.p : (K == BI_SPMM_S ? a.s : a.x));
+  // with a general preconditioner the operator is applied to phat / shat (its dinv is 1)
+  const XT* in = reinterpret_cast<const XT*>(
+      K == BI_SPMM_P ? (a.phat ? a.phat : a.p) : (K == BI_SPMM_S ? (a.shat ? a.shat : a.s) : a.x));
   XT* out = reinterpret_cast<XT*>(K == BI_SPMM_P ? a.v : (K == BI_SPMM_S ? a.t : a.r));
   const XT* other = reinterpret_cast<const XT*>(K == BI_SPMM_P ? a.rhat : (K == BI_SPMM_S ? a.s : a.b));
   bool on = lane_ok;

@@ -19,6 +19,7 @@ struct sad_bicg {
   int R = 1, dtype = 0;
   size_t esz = 8;
   char* vecs = nullptr;          // dx r rhat p v s t (n x R each)
+  char* pvecs = nullptr;         // phat shat (general preconditioners; lazy)
   char* state = nullptr;
   double* part = nullptr;
   int max_blocks = 0;
@@ -96,6 +97,7 @@ extern "C" int sad_bicg_create(sad_ctx* ctx, int64_t n, int r, int dtype, sad_bi
 extern "C" int sad_bicg_destroy(sad_bicg* w) {
   if (!w) return SAD_OK;
   ctx_free(w->ctx, w->vecs);
+  ctx_free(w->ctx, w->pvecs);
   ctx_free(w->ctx, w->state);
   ctx_free(w->ctx, w->part);
   if (w->hflag_host) cudaFreeHost(w->hflag_host);
@@ -126,9 +128,22 @@ static __global__ void k_bi_init(BState st) {
   }
 }
 
+extern "C" int sad_bicg_solve_pc(sad_bicg* w, sad_op* op, sad_pc* pc, const void* rhs, void* x,
+                                 void* res, double tol_col, int maxit, void* stream,
+                                 int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
+
 extern "C" int sad_bicg_solve(sad_bicg* w, sad_op* op, const void* rhs, void* x, void* res,
                               double tol_col, int maxit, void* stream, int64_t* iters_host,
                               double* resnorm_host, uint8_t* conv_host) {
+  return sad_bicg_solve_pc(w, op, nullptr, rhs, x, res, tol_col, maxit, stream, iters_host,
+                           resnorm_host, conv_host);
+}
+
+// pc != nullptr: right preconditioning by an incomplete factorisation
+// (_precond_apply, krylov.py:73-76); the operator must carry no Jacobi scaling
+extern "C" int sad_bicg_solve_pc(sad_bicg* w, sad_op* op, sad_pc* pc, const void* rhs, void* x,
+                                 void* res, double tol_col, int maxit, void* stream,
+                                 int64_t* iters_host, double* resnorm_host, uint8_t* conv_host) {
   if (!w) return SAD_EINVAL;
   sad_ctx* ctx = w->ctx;
   if (!op || !rhs || !x) return set_err(ctx, SAD_EINVAL, "null argument");
@@ -158,6 +173,20 @@ extern "C" int sad_bicg_solve(sad_bicg* w, sad_op* op, const void* rhs, void* x,
   a.v = w->vecs + 4 * blk;
   a.s = w->vecs + 5 * blk;
   a.t = w->vecs + 6 * blk;
+  if (pc) {
+    if (pc->n != w->n) return set_err(ctx, SAD_EINVAL, "preconditioner size != workspace size");
+    if (op->precond != SAD_PRECOND_NONE)
+      return set_err(ctx, SAD_EINVAL, "an operator used with sad_pc must be created with SAD_PRECOND_NONE");
+    if (pc->cplx && w->dtype != SAD_C128)
+      return set_err(ctx, SAD_EINVAL, "complex factors need a complex128 workspace");
+    if (!w->pvecs) {
+      if (ctx_malloc(ctx, (void**)&w->pvecs, blk * 2) != cudaSuccess)
+        return set_err(ctx, SAD_ENOMEM, "BiCGstab preconditioner vectors allocation failed");
+      w->bytes += (int64_t)(blk * 2);
+    }
+    a.phat = w->pvecs;
+    a.shat = w->pvecs + blk;
+  }
   w->st.tol = tol_col;
   w->st.maxit = maxit;
   a.st = w->st;
@@ -197,7 +226,15 @@ extern "C" int sad_bicg_solve(sad_bicg* w, sad_op* op, const void* rhs, void* x,
       if (stop) break;
       // the first iterations are issued before any flag can say "stop":
       // a run that ends early leaves them as no-ops (gated on the masks)
-      if (vec(BI_PUPD) || spmm(BI_SPMM_P) || vec(BI_SUPD) || spmm(BI_SPMM_S) || vec(BI_RUPD))
+      if (pc) {
+        if (vec(BI_PUPD)) return set_err(ctx, SAD_EINVAL, "unsupported block width");
+        if ((rc = sad_pc_apply(pc, R, w->dtype, a.p, (void*)a.phat, 0, s))) return rc;
+        if (spmm(BI_SPMM_P) || vec(BI_SUPD))
+          return set_err(ctx, SAD_EINVAL, "unsupported block width / value type");
+        if ((rc = sad_pc_apply(pc, R, w->dtype, a.s, (void*)a.shat, 0, s))) return rc;
+        if (spmm(BI_SPMM_S) || vec(BI_RUPD))
+          return set_err(ctx, SAD_EINVAL, "unsupported block width / value type");
+      } else if (vec(BI_PUPD) || spmm(BI_SPMM_P) || vec(BI_SUPD) || spmm(BI_SPMM_S) || vec(BI_RUPD))
         return set_err(ctx, SAD_EINVAL, "unsupported block width / value type");
       CKL(ctx);
     }

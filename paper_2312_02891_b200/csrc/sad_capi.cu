@@ -1895,6 +1895,7 @@ extern "C" int sad_ts_gemv(sad_ctx* ctx, int64_t n, int64_t K, int64_t ldx, int 
 }
 
 #include "sad_dist.cuh"
+#include "sad_precond_host.cuh"
 #include "sad_bicg_host.cuh"
 #include "sad_minres_host.cuh"
 #include "sad_adi_host.cuh"

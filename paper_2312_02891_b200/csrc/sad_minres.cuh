@@ -66,6 +66,11 @@ struct MArgs {
   const void* dinv;   // Jacobi dinv (XT); |dinv| is the SPD split
   const void* b;
   void *x, *r1, *r2, *y, *t, *v, *w, *w2;
+  // 0: y = |dinv| r2 fused (none / Jacobi).  Cholesky kinds (apply_spd,
+  // precond.py:242-256) split START and YUPD around the triangular solves:
+  // 1 = write the vectors and y = r2 (no reduction), 2 = the dots on the solved y
+  // and the finisher
+  int pmode;
   MState st;
 };
 
@@ -234,21 +239,32 @@ __global__ void __launch_bounds__(kThreads) k_mr_vec(MArgs a) {
       if (K == MR_START) {
         // r1 = r2 = b, y = P r1, w = w2 = x = 0
         const XT bv = b[e];
-        r1[e] = bv;
-        r2[e] = bv;
-        const XT yv = sscal(pabs(dinv[row]), bv);
-        y[e] = yv;
-        w[e] = zero<XT>();
-        w2[e] = zero<XT>();
-        x[e] = zero<XT>();
+        XT yv;
+        if (a.pmode == 2) {
+          yv = y[e];
+        } else {
+          r1[e] = bv;
+          r2[e] = bv;
+          yv = a.pmode == 1 ? bv : sscal(pabs(dinv[row]), bv);
+          y[e] = yv;
+          w[e] = zero<XT>();
+          w2[e] = zero<XT>();
+          x[e] = zero<XT>();
+        }
         q[0] += abs2(bv);
         q[1] += to_c(cfma(bv, yv, zero<XT>())).x;   // Re <r1, y>
       } else if (K == MR_YUPD) {
         // y -= (alfa / beta) r2; r1 <- y (the new r2); y = P r2
-        const XT yv = sub(t[e], sscal(cf, r2[e]));
-        r1[e] = yv;
-        const XT py = sscal(pabs(dinv[row]), yv);
-        y[e] = py;
+        XT yv, py;
+        if (a.pmode == 2) {
+          yv = r1[e];
+          py = y[e];
+        } else {
+          yv = sub(t[e], sscal(cf, r2[e]));
+          r1[e] = yv;
+          py = a.pmode == 1 ? yv : sscal(pabs(dinv[row]), yv);
+          y[e] = py;
+        }
         q[0] += to_c(cfma(yv, py, zero<XT>())).x;     // Re <r2, y>
       } else {  // MR_WUPD
         // w = (v - oldeps w1 - delta w2) / gamma with w1 = old w2, w2 = old w
@@ -262,6 +278,7 @@ __global__ void __launch_bounds__(kThreads) k_mr_vec(MArgs a) {
     }
   }
   if constexpr (NQ > 0) {
+    if (a.pmode == 1) return;   // uniform: the dots follow the triangular solves
     __shared__ double tot_s[2 * 8];
     if (part_reduce<R, NQ>(st.part, st.pstride, st.ticket, q, grp, c, lane_ok, tot_s)) {
       mr_finish(st, K, tot_s);

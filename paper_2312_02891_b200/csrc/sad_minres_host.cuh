@@ -118,9 +118,22 @@ static __global__ void k_mr_init(MState st) {
   }
 }
 
+extern "C" int sad_minres_solve_pc(sad_minres* w, sad_op* op, sad_pc* pc, const void* rhs, void* x,
+                                   void* res, double tol_col, int maxit, void* stream,
+                                   int64_t* iters_host, double* resnorm_host, uint8_t* conv_host);
+
 extern "C" int sad_minres_solve(sad_minres* w, sad_op* op, const void* rhs, void* x, void* res,
                                 double tol_col, int maxit, void* stream, int64_t* iters_host,
                                 double* resnorm_host, uint8_t* conv_host) {
+  return sad_minres_solve_pc(w, op, nullptr, rhs, x, res, tol_col, maxit, stream, iters_host,
+                             resnorm_host, conv_host);
+}
+
+// pc != nullptr: the SPD split of an incomplete Cholesky factorisation,
+// psolve = (G G^H)^-1 (apply_spd, precond.py:242-256; krylov.py:197-199)
+extern "C" int sad_minres_solve_pc(sad_minres* w, sad_op* op, sad_pc* pc, const void* rhs, void* x,
+                                   void* res, double tol_col, int maxit, void* stream,
+                                   int64_t* iters_host, double* resnorm_host, uint8_t* conv_host) {
   if (!w) return SAD_EINVAL;
   sad_ctx* ctx = w->ctx;
   if (!op || !rhs || !x) return set_err(ctx, SAD_EINVAL, "null argument");
@@ -130,6 +143,12 @@ extern "C" int sad_minres_solve(sad_minres* w, sad_op* op, const void* rhs, void
     return set_err(ctx, SAD_EINVAL, "operator size %lld != workspace size %lld", op->n, w->n);
   if (!op->real_ok || op->vals_complex)
     return set_err(ctx, SAD_EINVAL, "MINRES needs a real shift (Hermitian operator), adi.py:468-472");
+  if (pc) {
+    if (pc->n != w->n) return set_err(ctx, SAD_EINVAL, "preconditioner size != workspace size");
+    if (pc->kind != SAD_PRECOND_IC0 && pc->kind != SAD_PRECOND_ICT)
+      return set_err(ctx, SAD_EINVAL, "MINRES needs an SPD split (ic0 / ict), adi.py:468-472");
+    if (pc->cplx) return set_err(ctx, SAD_EINVAL, "MINRES needs real Cholesky factors");
+  }
   cudaStream_t s = S_(stream);
   const int R = w->R;
   const size_t blkb = (size_t)w->n * R * w->esz;
@@ -156,10 +175,21 @@ extern "C" int sad_minres_solve(sad_minres* w, sad_op* op, const void* rhs, void
   const int gpw = 32 / R;
   const int grid = grid_for(w->n, kWarps * gpw, std::min(w->max_blocks, ctx->nsm * 4));
   const bool cplx = w->dtype == SAD_C128;
-  auto vec = [&](int K) {
+  auto vec1 = [&](int K, int pmode) {
     a.r1 = r1;
     a.r2 = r2;
+    a.pmode = pmode;
     return cplx ? minres_launch_vec_z(K, a, R, grid, s) : minres_launch_vec_d(K, a, R, grid, s);
+  };
+  // START / YUPD: with a Cholesky split, the vector part, y = (G G^H)^-1 y on the
+  // device, then the dots and the finisher
+  int pc_rc = SAD_OK;
+  auto vec = [&](int K) {
+    if (!pc || K == MR_WUPD) return vec1(K, 0);
+    if (vec1(K, 1)) return 1;
+    pc_rc = sad_pc_apply(pc, R, w->dtype, a.y, a.y, 1, s);
+    if (pc_rc) return 1;
+    return vec1(K, 2);
   };
   auto spmm = [&](int K) {
     a.r1 = r1;
@@ -172,7 +202,7 @@ extern "C" int sad_minres_solve(sad_minres* w, sad_op* op, const void* rhs, void
   std::atomic_thread_fence(std::memory_order_seq_cst);
   k_mr_init<<<1, 32, 0, s>>>(w->st);
   COUNT_LAUNCH(1);
-  if (vec(MR_START)) return set_err(ctx, SAD_EINVAL, "unsupported block width");
+  if (vec(MR_START)) return pc_rc ? pc_rc : set_err(ctx, SAD_EINVAL, "unsupported block width");
   const int LAG = 3;
   for (long long step = 0;; ++step) {
     bool stop = false;
@@ -186,7 +216,7 @@ extern "C" int sad_minres_solve(sad_minres* w, sad_op* op, const void* rhs, void
     // the first iterations are issued before any flag can say "stop": a column
     // that has ended leaves them as no-ops (gated on its flags)
     if (spmm(MR_SPMM) || vec(MR_YUPD))
-      return set_err(ctx, SAD_EINVAL, "unsupported block width / value type");
+      return pc_rc ? pc_rc : set_err(ctx, SAD_EINVAL, "unsupported block width / value type");
     std::swap(r1, r2);     // r1 <- old r2, r2 <- the new residual (written into old r1)
     if (vec(MR_WUPD) || spmm(MR_CHECK))
       return set_err(ctx, SAD_EINVAL, "unsupported block width / value type");

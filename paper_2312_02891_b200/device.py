@@ -96,24 +96,95 @@ class DeviceMatrix:
             self.handle = None
 
 
-class DeviceOperator:
-    """``base + shift*mass`` (or its conjugate transpose) with device Jacobi
-    (ShiftedOperator, sparse.py:158-206 + precond.py:272-276)."""
+class DevicePrecond:
+    """Incomplete factorisation of ``base + shift*mass`` (or its conjugate
+    transpose): ``factorize(op.assembled(), kind, droptol)`` (precond.py:307-357)
+    with the factors on the device (sad_pc_create).  Raises
+    FactorizationBreakdown like the reference."""
 
-    def __init__(self, base, mass, shift, adjoint=False, precond_kind="jacobi"):
-        if precond_kind not in _KIND:
-            raise ValueError(f"preconditioner {precond_kind!r} is not available on the "
-                             "GPU path (supported: none, jacobi)")
+    def __init__(self, base, mass, shift, adjoint, kind, droptol):
+        if kind not in ("ilu0", "ilut", "ic0", "ict"):
+            raise ValueError(f"{kind!r} is not an incomplete factorisation kind")
+        self.kind, self.droptol = kind, float(droptol)
+        self.n = base.shape[0]
+        self._ctx = base._ctx
+        shift = complex(shift)
+        h = ctypes.c_void_p()
+        rc = _lib.load().sad_pc_create(self._ctx, base.handle,
+                                       None if mass is None else mass.handle, shift.real,
+                                       shift.imag, 1 if adjoint else 0,
+                                       _lib.PRECOND_CODES[kind], self.droptol, ctypes.byref(h))
+        _lib.check(rc, self._ctx)
+        self.handle = h
+        info = np.zeros(8, dtype=np.int64)
+        _lib.check(_lib.load().sad_pc_info(h, info.ctypes.data), self._ctx)
+        self.nnz = (int(info[2]), int(info[3]))
+        self.is_complex = bool(info[4])
+        self.levels = (int(info[5]), int(info[6]))
+        self.sign = float(info[7])
+
+    @property
+    def is_spd_capable(self):
+        return self.kind in ("ic0", "ict")
+
+    def factor(self, which=0):
+        """The reference's raw triplets (indptr, indices, data complex128): 0 = L
+        (unit diagonal not stored) or G (diagonal last per row), 1 = U (diagonal
+        first) -- IncompleteFactorization._lu / _chol (precond.py:193-202)."""
+        nnz = self.nnz[which]
+        ip = np.zeros(self.n + 1, dtype=np.int64)
+        ix = np.zeros(max(nnz, 1), dtype=np.int64)
+        dv = np.zeros(max(nnz, 1), dtype=np.complex128)
+        _lib.check(_lib.load().sad_pc_get_factor(self.handle, which, ip.ctypes.data,
+                                                 ix.ctypes.data, dv.ctypes.data), self._ctx)
+        return ip, ix[:nnz], dv[:nnz]
+
+    def apply(self, x, y=None, spd=False, stream=None):
+        """y = M^-1 x (precond.py:224-240), or (G G^H)^-1 x with ``spd``
+        (precond.py:242-256) on a device block; y may be x."""
+        import torch
+        dtype = _lib.SAD_F64 if x.dtype == torch.float64 else _lib.SAD_C128
+        if y is None:
+            y = torch.empty_like(x)
+        rc = _lib.load().sad_pc_apply(self.handle, x.shape[1], dtype, x.data_ptr(), y.data_ptr(),
+                                      1 if spd else 0, current_stream_handle(stream))
+        _lib.check(rc, self._ctx)
+        return y
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.load().sad_pc_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class DeviceOperator:
+    """``base + shift*mass`` (or its conjugate transpose) with its preconditioner
+    (ShiftedOperator, sparse.py:158-206 + precond.py): none / Jacobi folded into
+    the operator (device dinv), the incomplete factorisations as ``self.pc``."""
+
+    def __init__(self, base, mass, shift, adjoint=False, precond_kind="jacobi", droptol=0.1):
+        if precond_kind not in _lib.PRECOND_CODES:
+            raise ValueError(f"unknown preconditioner kind {precond_kind!r}")
         self.base, self.mass = base, mass
         self.shift = complex(shift)
         self.adjoint = bool(adjoint)
         self.n = base.shape[0]
         self._ctx = base._ctx
+        self.precond_kind = precond_kind
+        self.pc = None
+        if precond_kind not in _KIND:
+            # may raise FactorizationBreakdown (the binding falls back to Jacobi)
+            self.pc = DevicePrecond(base, mass, shift, adjoint, precond_kind, droptol)
         h = ctypes.c_void_p()
         rc = _lib.load().sad_op_create(self._ctx, base.handle,
                                        None if mass is None else mass.handle,
                                        self.shift.real, self.shift.imag,
-                                       1 if adjoint else 0, _KIND[precond_kind],
+                                       1 if adjoint else 0,
+                                       _KIND.get(precond_kind, _lib.SAD_PRECOND_NONE),
                                        ctypes.byref(h))
         _lib.check(rc, self._ctx)
         self.handle = h
@@ -179,6 +250,12 @@ class DeviceOperator:
 ENGINES = {"multi": _lib.SAD_ENGINE_MULTI, "persistent": _lib.SAD_ENGINE_PERSISTENT}
 
 
+def _no_pc(op):
+    if getattr(op, "pc", None) is not None:
+        raise ValueError("incomplete-factorisation preconditioners run with the reference's "
+                         "solvers (solver='bicgstab', 'minres' or 'reference'), not with GMRES")
+
+
 class GmresWorkspace:
     """(restart+1) basis blocks (+ restart Z blocks for FGMRES) on the device.
 
@@ -219,6 +296,7 @@ class GmresWorkspace:
 
     def solve(self, op, rhs, x, res, tol_col, maxit, stream=None):
         """Returns (iterations int64[r], residual norms float64[r], converged bool[r])."""
+        _no_pc(op)
         r = self.r
         iters = np.zeros(r, dtype=np.int64)
         norms = np.zeros(r, dtype=np.float64)
@@ -233,6 +311,7 @@ class GmresWorkspace:
 
     def launch(self, op, rhs, x, tol_col, maxit, stream=None):
         """Enqueue a solve (returns immediately for the persistent engine)."""
+        _no_pc(op)
         rc = _lib.load().sad_gmres_launch(self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
                                           float(tol_col), int(maxit),
                                           current_stream_handle(stream))
@@ -251,6 +330,7 @@ class GmresWorkspace:
         return iters, norms, conv.astype(bool)
 
     def fixed(self, op, rhs, x, res, steps, stream=None, timed=False):
+        _no_pc(op)
         norms = np.zeros(self.r, dtype=np.float64)
         timing = np.zeros(8, dtype=np.float64)
         rc = _lib.load().sad_gmres_fixed(
@@ -296,8 +376,9 @@ class BicgWorkspace:
         iters = np.zeros(r, dtype=np.int64)
         norms = np.zeros(r, dtype=np.float64)
         conv = np.zeros(r, dtype=np.uint8)
-        rc = _lib.load().sad_bicg_solve(
-            self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
+        rc = _lib.load().sad_bicg_solve_pc(
+            self.handle, op.handle, None if op.pc is None else op.pc.handle,
+            rhs.data_ptr(), x.data_ptr(),
             None if res is None else res.data_ptr(), float(tol_col), int(maxit),
             current_stream_handle(stream), iters.ctypes.data, norms.ctypes.data,
             conv.ctypes.data)
@@ -340,8 +421,9 @@ class MinresWorkspace:
         iters = np.zeros(r, dtype=np.int64)
         norms = np.zeros(r, dtype=np.float64)
         conv = np.zeros(r, dtype=np.uint8)
-        rc = _lib.load().sad_minres_solve(
-            self.handle, op.handle, rhs.data_ptr(), x.data_ptr(),
+        rc = _lib.load().sad_minres_solve_pc(
+            self.handle, op.handle, None if op.pc is None else op.pc.handle,
+            rhs.data_ptr(), x.data_ptr(),
             None if res is None else res.data_ptr(), float(tol_col), int(maxit),
             current_stream_handle(stream), iters.ctypes.data, norms.ctypes.data,
             conv.ctypes.data)

@@ -120,6 +120,8 @@ PHASE_A = {"auto": -1, "tma": 0, "direct": 1}
 
 
 SOLVERS = ("gmres", "bicgstab", "minres", "reference")
+#: precond.py:15 kinds that carry triangular factors
+FACTOR_KINDS = ("ilu0", "ilut", "ic0", "ict")
 
 
 def _side_symmetric(mat, tol=1e-12):
@@ -153,11 +155,14 @@ class GpuGmresBinding:
             raise NotImplementedError(
                 "direct (sparse LU) inner solves are outside the GPU hot path; "
                 "use the reference's SolverBinding for exact_direct")
-        if precond_kind not in ("none", "jacobi"):
-            raise ValueError(f"preconditioner {precond_kind!r} is not available on the GPU "
-                             "path (supported: none, jacobi)")
+        if precond_kind not in _lib.PRECOND_CODES:
+            raise ValueError(f"unknown preconditioner kind {precond_kind!r}")
         if solver not in SOLVERS:
             raise ValueError(f"solver must be one of {SOLVERS}")
+        if precond_kind in FACTOR_KINDS and solver == "gmres":
+            raise ValueError("incomplete-factorisation preconditioners (the reference's "
+                             "ilu0/ilut/ic0/ict) run with the reference's solvers: "
+                             "solver='reference', 'bicgstab' or 'minres'")
         self.solver = solver
         self.side = side
         self.mode = mode
@@ -190,16 +195,24 @@ class GpuGmresBinding:
         shift = complex(shift)
         op = self._operators.get(shift)
         if op is None:
+            adj = (self.side == "B")
             try:
-                op = DeviceOperator(self.base, self.mass, shift, adjoint=(self.side == "B"),
-                                    precond_kind=self.precond_kind)
-            except _lib.FactorizationBreakdown:
-                if self.precond_kind == "none":
+                op = DeviceOperator(self.base, self.mass, shift, adjoint=adj,
+                                    precond_kind=self.precond_kind, droptol=self.droptol)
+            except _lib.FactorizationBreakdown as exc:
+                if self.precond_kind in FACTOR_KINDS:
+                    # adi.py:458-465: fall back to Jacobi (its own breakdown propagates)
+                    warnings.warn(f"{self.side}-side {self.precond_kind} factorization broke "
+                                  f"down at shift {shift} ({exc}); falling back to Jacobi")
+                    op = DeviceOperator(self.base, self.mass, shift, adjoint=adj,
+                                        precond_kind="jacobi")
+                elif self.precond_kind == "none":
                     raise
-                warnings.warn(f"{self.side}-side jacobi factorization broke down at shift "
-                              f"{shift}; continuing without preconditioner")
-                op = DeviceOperator(self.base, self.mass, shift, adjoint=(self.side == "B"),
-                                    precond_kind="none")
+                else:
+                    warnings.warn(f"{self.side}-side jacobi factorization broke down at shift "
+                                  f"{shift}; continuing without preconditioner")
+                    op = DeviceOperator(self.base, self.mass, shift, adjoint=adj,
+                                        precond_kind="none")
             self._operators[shift] = op
         return op
 
@@ -208,7 +221,8 @@ class GpuGmresBinding:
         if self.solver == "minres":
             return True
         return (self.solver == "reference" and self.symmetric
-                and complex(shift).imag == 0.0 and self.precond_kind in ("none", "jacobi"))
+                and complex(shift).imag == 0.0
+                and self.precond_kind in ("none", "jacobi", "ic0", "ict"))
 
     def kind_for(self, shift):
         """The inner algorithm a solve at ``shift`` runs."""
@@ -346,11 +360,13 @@ def make_gpu_bindings(problem, config, restart=50, flexible=False, device=0,
     """GPU counterpart of make_bindings (adi.py:497-505)."""
     kind_a = getattr(config, "precond_kind_A", "jacobi")
     kind_b = getattr(config, "precond_kind_B", "jacobi")
+    tol_a = getattr(config, "precond_droptol_A", 0.1)
+    tol_b = getattr(config, "precond_droptol_B", 0.1)
     maxit = getattr(config, "max_inner_iterations", 1000)
     return SolverBindings(
-        A=GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a,
+        A=GpuGmresBinding("A", problem.A, problem.M, "iterative", kind_a, tol_a,
                           max_iterations=maxit, restart=restart, flexible=flexible,
                           device=device, engine=engine, solver=solver),
-        B=GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b,
+        B=GpuGmresBinding("B", problem.B, problem.C, "iterative", kind_b, tol_b,
                           max_iterations=maxit, restart=restart, flexible=flexible,
                           device=device, engine=engine, solver=solver))
