@@ -774,7 +774,9 @@ def run_ours_c4(args, dist):
     # DCGS2 bytes of Arnoldi step j (J = j + 1 basis blocks): (2J + 2) N
     orth_b = sum((2 * (j + 1) + 2) * blk for j in range(arn))
     orth_ms = max(tm[1] - tm[4], 0.0) + tm[2]
-    traffic, tr_ent = ncu_traffic("c4_spmm")
+    band = op.band_info()
+    spmm_kernel = "k_spmm_band" if band else "k_spmm_bulk"
+    traffic, tr_ent = ncu_traffic("c4_spmm_band" if band else "c4_spmm")
     straffic, str_ent = ncu_traffic("c4_persistent")
     del gb, op, ws, x, res, rhs, y, flush
     _free_device()
@@ -798,8 +800,14 @@ def run_ours_c4(args, dist):
                              "working set also exceeds L2",
                        "parallelism": "single GPU" if dist.world == 1 else "replicas"},
             "roofline": {"bound": "hbm", "achieved": spmm_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": spmm_gbs / peak, "traffic": traffic, "kernel": "k_spmm_bulk",
+                         "frac": spmm_gbs / peak, "traffic": traffic, "kernel": spmm_kernel,
                          "frac_of_nominal_8000": spmm_gbs / 8000.0,
+                         # the banded plan stores 16-bit local columns and no row offsets:
+                         # its DRAM traffic is below the CSR's algorithmic bytes, so the
+                         # device's own rate is traffic / time
+                         "dram_gbs": traffic / (spmm_ms * 1e-3) / 1e9 if traffic else None,
+                         "dram_frac": traffic / (spmm_ms * 1e-3) / 1e9 / peak if traffic else None,
+                         "band_plan": band,
                          "traffic_source": tr_ent and (f"profiles/traffic.json[c4_spmm]: "
                                                        f"{tr_ent['note']}"),
                          "peak_kind": peak_kind, "algorithmic_bytes_per_launch": spmm_b,

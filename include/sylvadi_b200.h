@@ -105,6 +105,14 @@ int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* mass,
                   int precond_kind, sad_op** out);
 int sad_op_destroy(sad_op* op);
 /* Copy dinv (n complex128 values, interleaved) to host; for tests. */
+/* The banded SpMM plan of the operator's sparsity pattern, if it has one
+ * (built at creation for operators with >= 2^20 nonzeros, or as the environment
+ * variable SAD_SPMM_BAND = 0 / 1 says): rows in tiles, the x rows a tile
+ * reads staged in shared memory by TMA, 16-bit local column indices.  info[7] =
+ * plan present (0/1), tiles, padded entries, nonzeros, local x rows per tile
+ * (max), padded row length (max), rows per tile (256, 128 or 64; SAD_BAND_ROWS
+ * overrides).  Patterns that do not fit run the CSR kernels. */
+int sad_op_band_info(const sad_op* op, int64_t* info);
 int sad_op_get_dinv(const sad_op* op, double* dinv_host);
 
 /* y = Op x  (ShiftedOperator.apply, sparse.py:192-206). */

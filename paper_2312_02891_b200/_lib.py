@@ -44,6 +44,7 @@ SIGNATURES = {
                                  _c.c_int, _c.POINTER(_vp)]),
     "sad_op_destroy": (_c.c_int, [_vp]),
     "sad_op_get_dinv": (_c.c_int, [_vp, _vp]),
+    "sad_op_band_info": (_c.c_int, [_vp, _vp]),
     "sad_op_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
     "sad_op_apply_host": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
     "sad_op_residual": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),

@@ -77,8 +77,17 @@ struct DevCsr {
   double* vals = nullptr;
 };
 
+namespace { struct BandPlan; }   // sad_band_host.cuh
+
 struct sad_csr {
   sad_ctx* ctx = nullptr;
+  unsigned long long uid = 0;
+  // banded SpMM plans of the pattern ([1]: the transpose) and of merged
+  // base + mass patterns (keyed by the mass matrix's uid and the side)
+  std::mutex band_mu;
+  BandPlan* band[2] = {nullptr, nullptr};
+  bool band_tried[2] = {false, false};
+  std::map<std::pair<unsigned long long, int>, BandPlan*> band_merged;
   long long nrows = 0, ncols = 0, nnz = 0;
   DevCsr d, dt;  // matrix and (optional) transpose
   bool has_t = false;
@@ -104,6 +113,9 @@ struct sad_op {
   const int* rowptr = nullptr;
   const int* colidx = nullptr;
   const void* vals = nullptr;
+  const BandPlan* band = nullptr;     // banded SpMM plan of the pattern (null: CSR kernels)
+  const void* band_val = nullptr;     // values in the plan's layout (double, or double2 if vals_complex)
+  void* own_band_val = nullptr;
   bool vals_complex = false;
   bool sigma_identity = false;  // identity mass: shift added in the epilogue
   double2 sigma_eff = {0.0, 0.0};
@@ -340,6 +352,8 @@ extern "C" int sad_ctx_destroy(sad_ctx* c) {
 extern "C" const char* sad_last_error(const sad_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
 extern "C" int sad_ctx_num_sms(const sad_ctx* c) { return c ? c->nsm : 0; }
 
+#include "sad_band_host.cuh"
+
 // -----------------------------------------------------------------------------
 // CSR
 // -----------------------------------------------------------------------------
@@ -406,6 +420,7 @@ extern "C" int sad_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_
   }
   sad_csr* c = new sad_csr();
   c->ctx = ctx;
+  c->uid = g_op_uid.fetch_add(1);
   c->nrows = nrows;
   c->ncols = ncols;
   c->nnz = nnz;
@@ -431,6 +446,9 @@ extern "C" int sad_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_
 
 extern "C" int sad_csr_destroy(sad_csr* c) {
   if (!c) return SAD_OK;
+  band_free(c->ctx, c->band[0]);
+  band_free(c->ctx, c->band[1]);
+  for (auto& kv : c->band_merged) band_free(c->ctx, kv.second);
   free_csr(c->ctx, c->d);
   free_csr(c->ctx, c->dt);
   delete c;
@@ -481,6 +499,27 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
     op->vals_complex = false;
     op->sigma_identity = true;
     op->real_ok = (sig.y == 0.0);
+    if (band_wanted(base->nnz)) {
+      // one plan (and one padded copy of the values) per matrix side, shared by
+      // the operators of every shift
+      sad_csr* bm = const_cast<sad_csr*>(base);
+      std::lock_guard<std::mutex> lk(bm->band_mu);
+      const int t = adjoint ? 1 : 0;
+      if (!bm->band_tried[t]) {
+        bm->band_tried[t] = true;
+        BandPlan* p = band_build(ctx, base->nrows, adjoint ? base->ht_rowptr : base->h_rowptr,
+                                 adjoint ? base->ht_colidx : base->h_colidx);
+        if (p && band_values<double>(ctx, p, bd.vals, &p->pval_base) != SAD_OK) {
+          band_free(ctx, p);
+          p = nullptr;
+        }
+        bm->band[t] = p;
+      }
+      if (bm->band[t]) {
+        op->band = bm->band[t];
+        op->band_val = bm->band[t]->pval_base;
+      }
+    }
   } else {
     // assemble base + sigma*mass on the merged pattern (sparse.py:138-155)
     const std::vector<int>& brp = adjoint ? base->ht_rowptr : base->h_rowptr;
@@ -533,6 +572,28 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
     op->vals_complex = cplx;
     op->sigma_identity = false;
     op->real_ok = !cplx;
+    if (band_wanted((long long)nz)) {
+      // the merged pattern is the same for every shift: one plan per (mass, side),
+      // the padded values per operator
+      sad_csr* bm = const_cast<sad_csr*>(base);
+      std::lock_guard<std::mutex> lk(bm->band_mu);
+      const auto key = std::make_pair(mass->uid, adjoint ? 1 : 0);
+      auto it = bm->band_merged.find(key);
+      if (it == bm->band_merged.end())
+        it = bm->band_merged.emplace(key, band_build(ctx, n, rp, ci)).first;
+      const BandPlan* p = it->second;
+      if (p && p->nnz == (long long)nz) {
+        int brc = cplx ? band_values<double2>(ctx, p, (const double2*)op->own_vals, (double2**)&op->own_band_val)
+                       : band_values<double>(ctx, p, (const double*)op->own_vals, (double**)&op->own_band_val);
+        if (brc == SAD_OK) {
+          op->band = p;
+          op->band_val = op->own_band_val;
+        } else {
+          ctx_free(ctx, op->own_band_val);
+          op->own_band_val = nullptr;
+        }
+      }
+    }
   }
   // Jacobi dinv (precond.py:272-276): 1/diag(assembled op); identity when "none"
   const long long n = op->n;
@@ -595,8 +656,26 @@ extern "C" int sad_op_destroy(sad_op* op) {
   ctx_free(op->ctx, op->own_rowptr);
   ctx_free(op->ctx, op->own_colidx);
   ctx_free(op->ctx, op->own_vals);
+  ctx_free(op->ctx, op->own_band_val);
   ctx_free(op->ctx, op->dinv_c);   // dinv_r lives in the same allocation
   delete op;
+  return SAD_OK;
+}
+
+// info[7]: plan present (0/1), tiles, padded entries, nonzeros, local x rows per
+// tile (max), padded row length (max), rows per tile
+extern "C" int sad_op_band_info(const sad_op* op, int64_t* info) {
+  if (!op || !info) return SAD_EINVAL;
+  for (int i = 0; i < 7; ++i) info[i] = 0;
+  if (op->band) {
+    info[0] = 1;
+    info[1] = op->band->ntiles;
+    info[2] = op->band->nent;
+    info[3] = op->band->nnz;
+    info[4] = op->band->xcap;
+    info[5] = op->band->wmax;
+    info[6] = op->band->tr;
+  }
   return SAD_OK;
 }
 
@@ -612,6 +691,17 @@ static int check_block(sad_ctx* ctx, int r, int dtype) {
   return SAD_OK;
 }
 
+template <typename XT>
+static void op_band_args(const sad_op* op, SpmmArgs<XT>& a) {
+  if (!op->band) return;
+  a.band_meta = op->band->meta;
+  a.band_idx = op->band->idx;
+  a.band_val = op->band_val;
+  a.band_xcap = op->band->xcap;
+  a.band_wmax = op->band->wmax;
+  a.band_tr = op->band->tr;
+}
+
 template <int MODE>
 static int op_spmm(sad_op* op, int r, int dtype, const void* b, const void* x, void* y, void* stream) {
   sad_ctx* ctx = op->ctx;
@@ -623,12 +713,14 @@ static int op_spmm(sad_op* op, int r, int dtype, const void* b, const void* x, v
     a.n = op->n; a.rowptr = op->rowptr; a.colidx = op->colidx; a.vals = op->vals;
     a.x = (const double*)x; a.y = (double*)y; a.b = (const double*)b;
     a.dinv = op->dinv_r; a.sigma = op->sigma_eff;
+    op_band_args(op, a);
     rc = launch_spmm<double, MODE>(a, r, false, false, op->sigma_identity, ctx->nsm, S_(stream));
   } else {
     SpmmArgs<double2> a{};
     a.n = op->n; a.rowptr = op->rowptr; a.colidx = op->colidx; a.vals = op->vals;
     a.x = (const double2*)x; a.y = (double2*)y; a.b = (const double2*)b;
     a.dinv = op->dinv_c; a.sigma = op->sigma_eff;
+    op_band_args(op, a);
     rc = launch_spmm<double2, MODE>(a, r, op->vals_complex, false, op->sigma_identity, ctx->nsm,
                                     S_(stream));
   }
@@ -1059,6 +1151,7 @@ struct Launcher {
     a.st = ws->st;
     a.dinv = reinterpret_cast<const XT*>(sizeof(XT) == 8 ? (const void*)op->dinv_r
                                                          : (const void*)op->dinv_c);
+    if (ws->n_ext == ws->n) op_band_args(op, a);
     if (mode == SPMM_ARNOLDI) {
       a.x = reinterpret_cast<const XT*>(ws->V);
       a.zout = reinterpret_cast<XT*>(ws->Z);

@@ -407,6 +407,12 @@ struct SpmmArgs {
   long long stride;  // elements per basis block (n*R)
   long long row0;    // bulk APPLY/RESID on a row range: global row of local row 0
                      // (rowptr, y, b are offset by the caller; x, dinv are global)
+  // banded plan (sad_spmm_band.cuh; null = the CSR kernels): tile records, 16-bit
+  // local row indices and values in the padded slot-major layout
+  const void* band_meta;
+  const unsigned short* band_idx;
+  const void* band_val;
+  int band_xcap, band_wmax, band_tr;   // local x rows / padded row length (max), rows per tile
   GState st;
 };
 

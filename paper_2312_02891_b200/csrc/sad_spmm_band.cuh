@@ -1,0 +1,244 @@
+// sad_spmm_band.cuh -- shifted SpMM with the x block staged in shared memory.
+//
+// The gathers of x are what bounds a CSR SpMM on r-column blocks: every
+// nonzero is a dependent global load, and a warp can only keep a handful in
+// flight (k_spmm_bulk: 4.6 TB/s on config 4 with 36 warps per SM; the same
+// loop inside the persistent GMRES kernel, 16 warps per SM: ~1 TB/s).  The
+// matrices of this path (finite differences / elements on grids; any banded
+// matrix) reference, from a tile of consecutive rows, a few CONTIGUOUS ranges
+// of x rows.  So an inspector (sad_band_host.cuh, once per sparsity pattern)
+// records for every tile of kBandRows rows
+//   * up to kBandMaxRanges ranges [xs, xs + xl) of x rows that cover every column
+//     of the tile, and where each lands in a shared-memory row buffer (ro);
+//   * the tile's nonzeros in a slot-major padded layout [W][kBandRows] with the
+//     column replaced by the 16-bit LOCAL row index into that buffer.
+// The kernel is then pure streaming: a producer warp issues, per tile, one
+// cp.async.bulk (1-D TMA) per x range, one for the indices and one for the
+// values (and one per range of the Jacobi diagonal), S tiles ahead, completing
+// on an mbarrier; consumer warps read everything from shared memory with no
+// global load on their critical path, no row-length predicates, and write y.
+// Per row the products are summed in the CSR (increasing column) order, padded
+// slots add v = 0 times the row's own x entry.
+// HBM bytes per row: W * (2 + sizeof(VT)) + the x rows of the tile's own range
+// once (the far ranges are L2 hits: their rows are some other tile's own rows)
+// + the y row -- fewer than the CSR's algorithmic bytes.
+#pragma once
+
+#include "sad_spmm_bulk.cuh"
+
+namespace sad {
+
+// rows per tile: chosen per pattern by the inspector (256, 128 or 64: the largest
+// whose stage fits three times in shared memory; larger tiles mean fewer, longer
+// TMA copies per row -- config 4: 64 rows 4.6 TB/s, 128 rows 5.96, 256 rows 6.6)
+constexpr int kBandMaxRanges = 6;    // x ranges per tile
+constexpr int kBandMaxStages = 8;
+
+struct __align__(16) BandMeta {      // 64 bytes per tile
+  unsigned eoff;                     // first element of the tile's padded segment
+  short W;                           // padded row length of the tile
+  short nr;                          // ranges in use
+  int self_off;                      // local row of the tile's first row
+  int xs[kBandMaxRanges];            // first x row of range q
+  unsigned short xl[kBandMaxRanges]; // rows in range q
+  unsigned short ro[kBandMaxRanges]; // local row of range q (ro == xs mod 2, one spare row between ranges)
+  int pad;
+};
+static_assert(sizeof(BandMeta) == 64, "BandMeta is one 64-byte record");
+
+struct BandCfg {
+  int S;                  // pipeline stages
+  unsigned SB;            // bytes per stage
+  unsigned offD, offI, offV;   // dinv rows, indices, values inside a stage (x rows at 0)
+};
+
+
+// U: rows per lane group in flight (independent accumulator chains; the consumers
+// run 8 or 16 warps per SM on dependent shared-memory loads, so the instruction-
+// level parallelism is what keeps them ahead of the copies): 4 when a tile holds
+// four passes of the block, else 2 (config 4, 256-row tiles: U = 2 0.537 ms, 4 0.509 ms)
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U>
+__global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, BandCfg cfg) {
+  constexpr int GPW = 32 / R;
+  const int TR = a.band_tr;
+  constexpr unsigned RB = R * sizeof(XT);
+  extern __shared__ __align__(128) unsigned char smem_b[];
+  __shared__ __align__(8) unsigned long long full[kBandMaxStages], empty[kBandMaxStages];
+  __shared__ int s_W[kBandMaxStages], s_self[kBandMaxStages];
+
+  if (MODE == SPMM_ARNOLDI && *a.st.any_active == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int S = cfg.S;
+  const long long ntiles = (a.n + TR - 1) / TR;
+  const long long G = gridDim.x;
+  const long long K = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, kWarps);
+    }
+    fence_mbar_init();
+  }
+  const XT* x = a.x;
+  XT* y = a.y;
+  XT* zout = nullptr;
+  int jcur = 0;
+  if (MODE == SPMM_ARNOLDI) {
+    jcur = *a.st.j;
+    x = a.x + (long long)jcur * a.stride;
+    y = const_cast<XT*>(a.x) + (long long)(jcur + 1) * a.stride;
+    if (a.zout) zout = a.zout + (long long)jcur * a.stride;
+  }
+  __syncthreads();
+  const BandMeta* metas = reinterpret_cast<const BandMeta*>(a.band_meta);
+
+  if (warp == kWarps) {
+    // ---------------- producer ----------------
+    // Tile records are fetched 32 at a time, one per lane, a batch ahead of their
+    // use, into shared memory.  Per tile every copy has its own lane: lane q < nr
+    // the x range q (and, PRE, its Jacobi rows), lane 30 the indices, lane 31 the
+    // values -- the address arithmetic runs in parallel and ONE convergent
+    // cp.async.bulk instruction issues all of them; lane 0 only waits for the
+    // stage to be free and arms the barrier with the byte total.
+    __shared__ __align__(16) BandMeta s_meta[2][32];
+    const VT* vals = reinterpret_cast<const VT*>(a.band_val);
+    auto fetch = [&](long long kk, int buf) {
+      if (kk < K) {
+        const int4* src = reinterpret_cast<const int4*>(metas + (blockIdx.x + kk * G));
+        int4* dst = reinterpret_cast<int4*>(&s_meta[buf][lane]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = __ldg(src + i);
+      }
+    };
+    fetch(lane, 0);
+    fetch(32 + lane, 1);
+    __syncwarp();
+    for (long long k = 0; k < K; ++k) {
+      const int l = (int)(k & 31);
+      const int buf = (int)((k >> 5) & 1);
+      if (l == 0 && k > 0) {
+        // the other buffer's batch is finished with: refill it two batches ahead
+        fetch(k + 32 + lane, buf ^ 1);
+        __syncwarp();
+      }
+      const BandMeta& m = s_meta[buf][l];
+      const int st = (int)(k % S);
+      const int nr = m.nr;
+      const unsigned nent = (unsigned)m.W * TR;
+      unsigned long long src = 0, dsrc = 0;
+      unsigned len = 0, dlen = 0, dst = 0, ddst = 0;
+      // widened, 16-byte aligned copies: source and destination are congruent
+      // mod 16 (ro == xs mod 2, 16-aligned bases), spare rows absorb the slack
+      if (lane < nr) {
+        const unsigned long long s0 = reinterpret_cast<unsigned long long>(x) + (unsigned long long)m.xs[lane] * RB;
+        const unsigned long long s1 = s0 + (unsigned long long)m.xl[lane] * RB;
+        src = s0 & ~15ull;
+        len = (unsigned)(((s1 + 15ull) & ~15ull) - src);
+        dst = 16u + (unsigned)m.ro[lane] * RB - (unsigned)(s0 - src);
+        if (PRE) {
+          const unsigned long long d0 = reinterpret_cast<unsigned long long>(a.dinv) + (unsigned long long)m.xs[lane] * sizeof(XT);
+          const unsigned long long d1 = d0 + (unsigned long long)m.xl[lane] * sizeof(XT);
+          dsrc = d0 & ~15ull;
+          dlen = (unsigned)(((d1 + 15ull) & ~15ull) - dsrc);
+          ddst = cfg.offD + 16u + (unsigned)m.ro[lane] * (unsigned)sizeof(XT) - (unsigned)(d0 - dsrc);
+        }
+      } else if (lane == 30) {
+        src = reinterpret_cast<unsigned long long>(a.band_idx + m.eoff);
+        len = nent * 2u;
+        dst = cfg.offI;
+      } else if (lane == 31) {
+        src = reinterpret_cast<unsigned long long>(vals + m.eoff);
+        len = nent * (unsigned)sizeof(VT);
+        dst = cfg.offV;
+      }
+      unsigned bytes = len + dlen;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+      unsigned char* base = smem_b + (size_t)st * cfg.SB;
+      if (lane == 0) {
+        if (k >= S) mbar_wait(empty + st, (unsigned)(((k / S) - 1) & 1));
+        s_W[st] = m.W;
+        s_self[st] = m.self_off;
+        mbar_expect_tx(full + st, bytes);
+      }
+      __syncwarp();
+      if (len) bulk_g2s(base + dst, reinterpret_cast<const void*>(src), len, full + st);
+      if (PRE && dlen) bulk_g2s(base + ddst, reinterpret_cast<const void*>(dsrc), dlen, full + st);
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int grp = lane / R, c = lane - grp * R;
+  const bool lane_ok = grp < GPW;
+  double scale = 1.0;
+  if (MODE == SPMM_ARNOLDI) scale = lane_ok ? a.st.S[jcur * R + c] : 0.0;
+  for (long long k = 0; k < K; ++k) {
+    const int st = (int)(k % S);
+    mbar_wait(full + st, (unsigned)((k / S) & 1));
+    const unsigned char* base = smem_b + (size_t)st * cfg.SB;
+    const XT* xs = reinterpret_cast<const XT*>(base + 16);
+    const XT* ds = reinterpret_cast<const XT*>(base + cfg.offD + 16);
+    const unsigned short* si = reinterpret_cast<const unsigned short*>(base + cfg.offI);
+    const VT* sv = reinterpret_cast<const VT*>(base + cfg.offV);
+    const int W = s_W[st], self = s_self[st];
+    const long long r0 = (blockIdx.x + k * G) * (long long)TR;
+    if (lane_ok) {
+      for (int rb = 0; rb < TR; rb += kWarps * GPW * U) {
+        int lr[U];
+        bool ok[U];
+        XT acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          lr[u] = rb + (u * kWarps + warp) * GPW + grp;
+          ok[u] = lr[u] < TR && r0 + lr[u] < a.n;
+          if (!ok[u]) lr[u] = 0;
+          acc[u] = zero<XT>();
+        }
+        if (!ok[0] && !ok[U - 1]) continue;
+#pragma unroll 4
+        for (int t = 0; t < W; ++t) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int e = t * TR + lr[u];
+            const int l = si[e];
+            XT xv = xs[l * R + c];
+            if (PRE) xv = mul(ds[l], xv);
+            acc[u] = fma_(sv[e], xv, acc[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+          const long long idx = (r0 + lr[u]) * R + c;
+          XT vres = acc[u];
+          if (SIGMA || (MODE == SPMM_ARNOLDI && zout)) {
+            const int ls = self + lr[u];
+            XT xi = xs[ls * R + c];
+            if (PRE) xi = mul(ds[ls], xi);
+            if (SIGMA) vres = fma_(from_c<XT>(a.sigma), xi, vres);
+            if (MODE == SPMM_ARNOLDI && zout) zout[idx] = sscal(scale, xi);
+          }
+          if (MODE == SPMM_ARNOLDI) vres = sscal(scale, vres);
+          if (MODE == SPMM_RESID || MODE == SPMM_RESID_CYCLE) vres = sub(a.b[idx], vres);
+          y[idx] = vres;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + st)) : "memory");
+  }
+}
+
+// values of a padded plan from the operator's CSR values: pval[e] = vals[perm[e]] (0 for padding)
+template <typename VT>
+__global__ void k_band_values(long long nent, const int* __restrict__ perm, const VT* __restrict__ vals,
+                              VT* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nent;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int p = perm[e];
+    out[e] = p >= 0 ? vals[p] : zero<VT>();
+  }
+}
+
+}  // namespace sad

@@ -7,6 +7,7 @@
 
 #include "sad_spmm_launch.cuh"
 #include "sad_spmm_bulk.cuh"
+#include "sad_spmm_band.cuh"
 
 #ifndef SAD_SPMM_PART
 #error "compile with -DSAD_SPMM_PART=<0..3>"
@@ -25,9 +26,72 @@ static int grid_for(long long work, int per_block, int cap) {
 // -----------------------------------------------------------------------------
 // SpMM dispatch
 // -----------------------------------------------------------------------------
+static size_t al128(size_t b) { return (b + 127) & ~size_t(127); }
+
+// Banded plan: stage layout and pipeline depth for this block type; false when
+// two stages do not fit (the CSR kernel runs instead)
+template <typename XT, typename VT, int R, bool PRE>
+static bool band_config(int xcap, int wmax, int tr, BandCfg& cfg, size_t& smem) {
+  const size_t xb = al128(32 + (size_t)xcap * R * sizeof(XT));
+  const size_t db = PRE ? al128(32 + (size_t)xcap * sizeof(XT)) : 0;
+  const size_t ib = al128((size_t)wmax * tr * 2);
+  const size_t vb = al128((size_t)wmax * tr * sizeof(VT));
+  const size_t sb = xb + db + ib + vb;
+  int S = (int)std::min<size_t>(6, (110 * 1024) / sb);         // two blocks per SM
+  if (S < 3) S = (int)std::min<size_t>(6, (212 * 1024) / sb);  // one block per SM
+  if (S < 2) return false;
+  cfg.S = S;
+  cfg.SB = (unsigned)sb;
+  cfg.offD = (unsigned)xb;
+  cfg.offI = (unsigned)(xb + db);
+  cfg.offV = (unsigned)(xb + db + ib);
+  smem = (size_t)S * sb;
+  return true;
+}
+
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U>
+static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s);
+
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
+static bool launch_band(const SpmmArgs<XT>& a, cudaStream_t s) {
+  if (!a.band_meta || a.row0 != 0) return false;
+  if (a.band_tr >= 4 * kWarps * (32 / R)) return launch_band_u<XT, VT, R, MODE, PRE, SIGMA, 4>(a, s);
+  return launch_band_u<XT, VT, R, MODE, PRE, SIGMA, 2>(a, s);
+}
+
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U>
+static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s) {
+  // TMA sources must be 16-byte aligned up to the parity rule of the plan
+  const XT* xsrc = a.x;
+  if ((reinterpret_cast<uintptr_t>(xsrc) & 15) || (reinterpret_cast<uintptr_t>(a.dinv) & 15)) return false;
+  if (MODE == SPMM_ARNOLDI && ((size_t)a.stride * sizeof(XT)) % 16) return false;
+  BandCfg cfg{};
+  size_t smem = 0;
+  if (!band_config<XT, VT, R, PRE>(a.band_xcap, a.band_wmax, a.band_tr, cfg, smem)) return false;
+  auto kern = k_spmm_band<XT, VT, R, MODE, PRE, SIGMA, U>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
+    attr = true;
+  }
+  static size_t nb_smem = 0;
+  static int nb = 0;
+  if (nb_smem != smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads + 32, smem);
+    nb_smem = smem;
+  }
+  if (nb < 1) return false;
+  const long long tiles = (a.n + a.band_tr - 1) / a.band_tr;
+  const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_spmm_bulk_sms));
+  kern<<<g, kThreads + 32, smem, s>>>(a, cfg);
+  count_launches(1);
+  return true;
+}
+
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
 static void launch_spmm_t(const SpmmArgs<XT>& a, int grid, cudaStream_t s) {
   if constexpr (MODE == SPMM_APPLY || MODE == SPMM_RESID || MODE == SPMM_ARNOLDI) {
+    if (launch_band<XT, VT, R, MODE, PRE, SIGMA>(a, s)) return;
     // TMA-staged SpMM; grid = resident blocks (persistent over row tiles)
     auto kern = k_spmm_bulk<XT, VT, R, MODE, PRE, SIGMA>;
     constexpr size_t smem = bulk_smem_bytes<VT, R>();
@@ -88,6 +152,8 @@ static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, i
   z.b = reinterpret_cast<const double2*>(a.b);
   z.sigma = a.sigma;
   z.row0 = a.row0;
+  z.band_meta = a.band_meta; z.band_idx = a.band_idx; z.band_val = a.band_val;
+  z.band_xcap = a.band_xcap; z.band_wmax = a.band_wmax; z.band_tr = a.band_tr;
   if (mode == SPMM_APPLY) launch_spmm<double2, SPMM_APPLY>(z, R / 2, false, false, sigma, nsm, s);
   else launch_spmm<double2, SPMM_RESID>(z, R / 2, false, false, sigma, nsm, s);
   return true;

@@ -190,6 +190,17 @@ class DeviceOperator:
         self.handle = h
         self.is_real = (self.shift.imag == 0.0)
 
+    def band_info(self):
+        """The banded SpMM plan of this operator (sad_op_band_info): dict with
+        tiles, padded entries, nnz, max local x rows and padded row length, or
+        None when the operator runs the CSR kernels."""
+        info = np.zeros(7, dtype=np.int64)
+        _lib.check(_lib.load().sad_op_band_info(self.handle, info.ctypes.data), self._ctx)
+        if not info[0]:
+            return None
+        return dict(tiles=int(info[1]), entries=int(info[2]), nnz=int(info[3]),
+                    xcap=int(info[4]), wmax=int(info[5]), rows=int(info[6]))
+
     def dinv(self):
         out = np.empty(self.n, dtype=np.complex128)
         _lib.check(_lib.load().sad_op_get_dinv(self.handle, out.ctypes.data), self._ctx)
