@@ -111,8 +111,11 @@ int sad_op_destroy(sad_op* op);
  * reads staged in shared memory by TMA, 16-bit local column indices.  info[7] =
  * plan present (0/1), tiles, padded entries, nonzeros, local x rows per tile
  * (max), padded row length (max), rows per tile (256, 128 or 64; SAD_BAND_ROWS
- * overrides).  Patterns that do not fit run the CSR kernels. */
-int sad_op_band_info(const sad_op* op, int64_t* info);
+ * overrides).  Patterns that do not fit run the CSR kernels.  Plans are built
+ * on first use, per class: 0 = the stand-alone SpMM (sad_op_apply / residual,
+ * the multi-kernel engine), 1 = the SpMM sub-phase of the persistent GMRES
+ * kernel (smaller tiles, SAD_BAND_ROWS_P). */
+int sad_op_band_info(sad_op* op, int plan_class, int64_t* info);
 int sad_op_get_dinv(const sad_op* op, double* dinv_host);
 
 /* y = Op x  (ShiftedOperator.apply, sparse.py:192-206). */

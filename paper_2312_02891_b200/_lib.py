@@ -44,7 +44,7 @@ SIGNATURES = {
                                  _c.c_int, _c.POINTER(_vp)]),
     "sad_op_destroy": (_c.c_int, [_vp]),
     "sad_op_get_dinv": (_c.c_int, [_vp, _vp]),
-    "sad_op_band_info": (_c.c_int, [_vp, _vp]),
+    "sad_op_band_info": (_c.c_int, [_vp, _c.c_int, _vp]),
     "sad_op_apply": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
     "sad_op_apply_host": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp]),
     "sad_op_residual": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp, _vp, _vp]),
@@ -160,6 +160,8 @@ def load(path=None):
             "(there is no CPU fallback for the inner-solve path)")
     lib = ctypes.CDLL(p)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("SAD_LIB_PATH") and not hasattr(lib, name):
+            continue            # A/B builds of older sources (tools/build_variant.py)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -277,7 +277,7 @@ class LowRankSolution:
 
     #: factors up to this size are concatenated on the device and downloaded in
     #: one copy; larger ones in chunks of this size
-    CONCAT_BYTES = 4 << 30
+    CONCAT_BYTES = 256 << 20
 
     def __init__(self, Z=None, gammas=(), Y=None, r=1, z_blocks=None, y_blocks=None,
                  n=None, m=None):
@@ -304,18 +304,76 @@ class LowRankSolution:
             host.copy_(dev, non_blocking=True)        # one contiguous D2H copy
             torch.cuda.synchronize(dev.device)
             return host.numpy()
-        # large factors (configs 3-5): bounded device staging, chunk by chunk
-        out = np.empty((rows, k * r), dtype=np.complex128)
-        group = max(1, LowRankSolution.CONCAT_BYTES // (rows * r * 16))
-        stage = None
-        for i0 in range(0, k, group):
-            i1 = min(k, i0 + group)
-            dev = torch.cat(blocks[i0:i1], dim=1).to(torch.complex128)
-            if stage is None or stage.shape != dev.shape:
-                stage = torch.empty(dev.shape, dtype=torch.complex128, pin_memory=True)
-            stage.copy_(dev)
-            out[:, i0 * r:i1 * r] = stage.numpy()
-            del dev
+        # large factors (configs 3-5): row chunks packed on the device into the
+        # host layout, double-buffered asynchronous copies into pinned staging
+        # (the next chunk is packed and copied while host threads move the
+        # previous one into the result, whose pages they also first-touch)
+        return LowRankSolution._stack_chunked(blocks, rows, r)
+
+    #: bytes per pinned staging buffer of the chunked download
+    STAGE_BYTES = 256 << 20
+    #: host threads moving staged chunks into the result array
+    COPY_THREADS = 8
+    _STAGING = None
+
+    @staticmethod
+    def _stack_chunked(blocks, rows, r):
+        import torch
+        from concurrent.futures import ThreadPoolExecutor
+        k = len(blocks)
+        width = k * r
+        out = np.empty((rows, width), dtype=np.complex128)
+        dev = blocks[0].device
+        chunk = max(1, min(rows, LowRankSolution.STAGE_BYTES // (width * 16)))
+        # the two pinned buffers are kept for the next download (Z, then Y)
+        cache = LowRankSolution._STAGING
+        if cache is None or cache[0].numel() < chunk * width:
+            cache = [torch.empty(chunk * width, dtype=torch.complex128, pin_memory=True)
+                     for _ in range(2)]
+            LowRankSolution._STAGING = cache
+        stages = [c[:chunk * width].view(chunk, width) for c in cache]
+        events = [torch.cuda.Event(), torch.cuda.Event()]
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        nthr = LowRankSolution.COPY_THREADS
+
+        def enqueue(i, r0):
+            r1 = min(rows, r0 + chunk)
+            with torch.cuda.stream(side):
+                packed = torch.cat([b[r0:r1] for b in blocks], dim=1)
+                if packed.dtype != torch.complex128:
+                    packed = packed.to(torch.complex128)
+                stages[i][:r1 - r0].copy_(packed, non_blocking=True)
+                events[i].record(side)
+            return r1
+
+        def move(dst, src):
+            np.copyto(dst, src)
+
+        starts = list(range(0, rows, chunk))
+        with ThreadPoolExecutor(max_workers=nthr) as pool:
+            pending = None
+            enqueue(0, starts[0])
+            for ci, r0 in enumerate(starts):
+                i = ci & 1
+                if ci + 1 < len(starts):
+                    if pending is not None:          # the other buffer must be drained first
+                        for f in pending:
+                            f.result()
+                        pending = None
+                    enqueue(i ^ 1, starts[ci + 1])
+                events[i].synchronize()
+                r1 = min(rows, r0 + chunk)
+                src = stages[i].numpy()[:r1 - r0]
+                if pending is not None:
+                    for f in pending:
+                        f.result()
+                step = max(1, (r1 - r0 + nthr - 1) // nthr)
+                pending = [pool.submit(move, out[r0 + s:min(r1, r0 + s + step)], src[s:s + step])
+                           for s in range(0, r1 - r0, step)]
+            if pending is not None:
+                for f in pending:
+                    f.result()
         return out
 
     @property

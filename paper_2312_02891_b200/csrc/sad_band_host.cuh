@@ -26,6 +26,22 @@ struct BandPlan {
                                        // identity mass share them; the shift is in the epilogue)
 };
 
+// the plans of one pattern (a matrix side, or a merged base + mass pattern whose
+// host arrays are kept here), by class
+struct BandSet {
+  std::vector<int> rp, ci;
+  BandPlan* plan[2] = {nullptr, nullptr};
+  bool tried[2] = {false, false};
+};
+
+void band_free(sad_ctx* ctx, BandPlan* p);
+void bandset_free(sad_ctx* ctx, BandSet* b) {
+  if (!b) return;
+  band_free(ctx, b->plan[0]);
+  band_free(ctx, b->plan[1]);
+  delete b;
+}
+
 void band_free(sad_ctx* ctx, BandPlan* p) {
   if (!p) return;
   ctx_free(ctx, p->meta);
@@ -182,12 +198,20 @@ BandPlan* band_build_tr(sad_ctx* ctx, long long n, const std::vector<int>& rp, c
 
 // The largest tile (256, 128, 64 rows) whose stage fits three times in shared
 // memory; small matrices take 64 (more tiles than SMs matter more there).
-BandPlan* band_build(sad_ctx* ctx, long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
-  const char* e = std::getenv("SAD_BAND_ROWS");
-  if (e && *e) return band_build_tr(ctx, n, rp, ci, std::max(32, std::atoi(e)), 0);
-  for (int tr : {256, 128}) {
-    if (n < (long long)tr * ctx->nsm * 4) continue;
-    if (BandPlan* p = band_build_tr(ctx, n, rp, ci, tr, 70 * 1024)) return p;
+// Class 1 (the persistent GMRES kernel's SpMM sub-phase, two blocks per SM next
+// to the kernel's other shared memory): 128-row tiles when two stages fit in
+// ~70 KB, else 64.  SAD_BAND_ROWS / SAD_BAND_ROWS_P override (multiples of 8).
+BandPlan* band_build(sad_ctx* ctx, long long n, const std::vector<int>& rp, const std::vector<int>& ci,
+                     int cls) {
+  const char* e = std::getenv(cls ? "SAD_BAND_ROWS_P" : "SAD_BAND_ROWS");
+  if (e && *e) return band_build_tr(ctx, n, rp, ci, std::max(32, std::atoi(e) & ~7), 0);
+  if (cls == 0) {
+    for (int tr : {256, 128}) {
+      if (n < (long long)tr * ctx->nsm * 4) continue;
+      if (BandPlan* p = band_build_tr(ctx, n, rp, ci, tr, 70 * 1024)) return p;
+    }
+  } else if (n >= (long long)128 * ctx->nsm * 8) {
+    if (BandPlan* p = band_build_tr(ctx, n, rp, ci, 128, 35 * 1024)) return p;
   }
   return band_build_tr(ctx, n, rp, ci, 64, 0);
 }

@@ -77,17 +77,15 @@ struct DevCsr {
   double* vals = nullptr;
 };
 
-namespace { struct BandPlan; }   // sad_band_host.cuh
+namespace { struct BandPlan; struct BandSet; }   // sad_band_host.cuh
 
 struct sad_csr {
   sad_ctx* ctx = nullptr;
   unsigned long long uid = 0;
-  // banded SpMM plans of the pattern ([1]: the transpose) and of merged
-  // base + mass patterns (keyed by the mass matrix's uid and the side)
+  // banded SpMM plans of the patterns this matrix is the base of: its own (mass
+  // uid 0) and the merged base + mass patterns, per side; built on first use
   std::mutex band_mu;
-  BandPlan* band[2] = {nullptr, nullptr};
-  bool band_tried[2] = {false, false};
-  std::map<std::pair<unsigned long long, int>, BandPlan*> band_merged;
+  std::map<std::pair<unsigned long long, int>, BandSet*> bands;
   long long nrows = 0, ncols = 0, nnz = 0;
   DevCsr d, dt;  // matrix and (optional) transpose
   bool has_t = false;
@@ -113,9 +111,19 @@ struct sad_op {
   const int* rowptr = nullptr;
   const int* colidx = nullptr;
   const void* vals = nullptr;
-  const BandPlan* band = nullptr;     // banded SpMM plan of the pattern (null: CSR kernels)
-  const void* band_val = nullptr;     // values in the plan's layout (double, or double2 if vals_complex)
-  void* own_band_val = nullptr;
+  // banded SpMM plans (built on first use; null: CSR kernels).  Class 0: the
+  // stand-alone SpMM (large tiles); class 1: the persistent kernel's SpMM
+  // sub-phase (tiles that fit next to its other shared memory).  Values in a
+  // plan's layout: double, or double2 if vals_complex.
+  const sad_csr* base_csr = nullptr;
+  unsigned long long mass_uid = 0;
+  int adjoint = 0;
+  BandSet* bset = nullptr;
+  const BandPlan* band[2] = {nullptr, nullptr};
+  const void* band_val[2] = {nullptr, nullptr};
+  void* own_band_val[2] = {nullptr, nullptr};
+  bool band_tried[2] = {false, false};
+  bool band_ok = false;               // SAD_SPMM_BAND / size rule, read when the operator is created
   bool vals_complex = false;
   bool sigma_identity = false;  // identity mass: shift added in the epilogue
   double2 sigma_eff = {0.0, 0.0};
@@ -446,9 +454,7 @@ extern "C" int sad_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, int64_
 
 extern "C" int sad_csr_destroy(sad_csr* c) {
   if (!c) return SAD_OK;
-  band_free(c->ctx, c->band[0]);
-  band_free(c->ctx, c->band[1]);
-  for (auto& kv : c->band_merged) band_free(c->ctx, kv.second);
+  for (auto& kv : c->bands) bandset_free(c->ctx, kv.second);
   free_csr(c->ctx, c->d);
   free_csr(c->ctx, c->dt);
   delete c;
@@ -487,6 +493,9 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
   op->uid = g_op_uid.fetch_add(1);
   op->n = base->nrows;
   op->ncols = base->nrows;
+  op->base_csr = base;
+  op->mass_uid = mass ? mass->uid : 0;
+  op->adjoint = adjoint ? 1 : 0;
   op->precond = precond_kind;
   const double2 sig = adjoint ? make_double2(sre, -sim) : make_double2(sre, sim);
   op->sigma_eff = sig;
@@ -499,27 +508,6 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
     op->vals_complex = false;
     op->sigma_identity = true;
     op->real_ok = (sig.y == 0.0);
-    if (band_wanted(base->nnz)) {
-      // one plan (and one padded copy of the values) per matrix side, shared by
-      // the operators of every shift
-      sad_csr* bm = const_cast<sad_csr*>(base);
-      std::lock_guard<std::mutex> lk(bm->band_mu);
-      const int t = adjoint ? 1 : 0;
-      if (!bm->band_tried[t]) {
-        bm->band_tried[t] = true;
-        BandPlan* p = band_build(ctx, base->nrows, adjoint ? base->ht_rowptr : base->h_rowptr,
-                                 adjoint ? base->ht_colidx : base->h_colidx);
-        if (p && band_values<double>(ctx, p, bd.vals, &p->pval_base) != SAD_OK) {
-          band_free(ctx, p);
-          p = nullptr;
-        }
-        bm->band[t] = p;
-      }
-      if (bm->band[t]) {
-        op->band = bm->band[t];
-        op->band_val = bm->band[t]->pval_base;
-      }
-    }
   } else {
     // assemble base + sigma*mass on the merged pattern (sparse.py:138-155)
     const std::vector<int>& brp = adjoint ? base->ht_rowptr : base->h_rowptr;
@@ -573,28 +561,19 @@ extern "C" int sad_op_create(sad_ctx* ctx, const sad_csr* base, const sad_csr* m
     op->sigma_identity = false;
     op->real_ok = !cplx;
     if (band_wanted((long long)nz)) {
-      // the merged pattern is the same for every shift: one plan per (mass, side),
-      // the padded values per operator
+      // the merged pattern is the same for every shift: kept once per (mass, side)
+      // for the plans built on first use
       sad_csr* bm = const_cast<sad_csr*>(base);
       std::lock_guard<std::mutex> lk(bm->band_mu);
-      const auto key = std::make_pair(mass->uid, adjoint ? 1 : 0);
-      auto it = bm->band_merged.find(key);
-      if (it == bm->band_merged.end())
-        it = bm->band_merged.emplace(key, band_build(ctx, n, rp, ci)).first;
-      const BandPlan* p = it->second;
-      if (p && p->nnz == (long long)nz) {
-        int brc = cplx ? band_values<double2>(ctx, p, (const double2*)op->own_vals, (double2**)&op->own_band_val)
-                       : band_values<double>(ctx, p, (const double*)op->own_vals, (double**)&op->own_band_val);
-        if (brc == SAD_OK) {
-          op->band = p;
-          op->band_val = op->own_band_val;
-        } else {
-          ctx_free(ctx, op->own_band_val);
-          op->own_band_val = nullptr;
-        }
+      BandSet*& bs = bm->bands[std::make_pair(mass->uid, adjoint ? 1 : 0)];
+      if (!bs) {
+        bs = new BandSet();
+        bs->rp = rp;
+        bs->ci = ci;
       }
     }
   }
+  op->band_ok = band_wanted(op->nnz);
   // Jacobi dinv (precond.py:272-276): 1/diag(assembled op); identity when "none"
   const long long n = op->n;
   // one allocation for both dinv copies; the breakdown flag lives in the ctx
@@ -656,25 +635,74 @@ extern "C" int sad_op_destroy(sad_op* op) {
   ctx_free(op->ctx, op->own_rowptr);
   ctx_free(op->ctx, op->own_colidx);
   ctx_free(op->ctx, op->own_vals);
-  ctx_free(op->ctx, op->own_band_val);
+  ctx_free(op->ctx, op->own_band_val[0]);
+  ctx_free(op->ctx, op->own_band_val[1]);
   ctx_free(op->ctx, op->dinv_c);   // dinv_r lives in the same allocation
   delete op;
   return SAD_OK;
 }
 
+// The operator's plan of class cls (0 stand-alone SpMM, 1 persistent kernel),
+// built on first use; nullptr when the pattern has none
+static const BandPlan* op_band(sad_op* op, int cls) {
+  if (op->band_tried[cls]) return op->band[cls];
+  op->band_tried[cls] = true;
+  if (!op->base_csr || !op->band_ok) return nullptr;
+  sad_ctx* ctx = op->ctx;
+  sad_csr* bm = const_cast<sad_csr*>(op->base_csr);
+  std::lock_guard<std::mutex> lk(bm->band_mu);
+  BandSet*& bs = bm->bands[std::make_pair(op->mass_uid, op->adjoint)];
+  if (!bs) {
+    if (op->mass_uid) return nullptr;     // merged pattern not kept
+    bs = new BandSet();
+  }
+  if (!bs->tried[cls]) {
+    bs->tried[cls] = true;
+    const std::vector<int>& rp = op->mass_uid ? bs->rp : (op->adjoint ? bm->ht_rowptr : bm->h_rowptr);
+    const std::vector<int>& ci = op->mass_uid ? bs->ci : (op->adjoint ? bm->ht_colidx : bm->h_colidx);
+    BandPlan* p = band_build(ctx, op->n, rp, ci, cls);
+    if (p && !op->mass_uid) {
+      // identity mass: the operators of every shift share the matrix's values
+      const DevCsr& bd = op->adjoint ? bm->dt : bm->d;
+      if (band_values<double>(ctx, p, bd.vals, &p->pval_base) != SAD_OK) {
+        band_free(ctx, p);
+        p = nullptr;
+      }
+    }
+    bs->plan[cls] = p;
+  }
+  const BandPlan* p = bs->plan[cls];
+  if (!p || p->nnz != op->nnz) return nullptr;
+  if (!op->mass_uid) {
+    op->band_val[cls] = p->pval_base;
+  } else {
+    const int rc = op->vals_complex
+        ? band_values<double2>(ctx, p, (const double2*)op->own_vals, (double2**)&op->own_band_val[cls])
+        : band_values<double>(ctx, p, (const double*)op->own_vals, (double**)&op->own_band_val[cls]);
+    if (rc != SAD_OK) {
+      ctx_free(ctx, op->own_band_val[cls]);
+      op->own_band_val[cls] = nullptr;
+      return nullptr;
+    }
+    op->band_val[cls] = op->own_band_val[cls];
+  }
+  op->band[cls] = p;
+  return p;
+}
+
 // info[7]: plan present (0/1), tiles, padded entries, nonzeros, local x rows per
 // tile (max), padded row length (max), rows per tile
-extern "C" int sad_op_band_info(const sad_op* op, int64_t* info) {
-  if (!op || !info) return SAD_EINVAL;
+extern "C" int sad_op_band_info(sad_op* op, int cls, int64_t* info) {
+  if (!op || !info || cls < 0 || cls > 1) return SAD_EINVAL;
   for (int i = 0; i < 7; ++i) info[i] = 0;
-  if (op->band) {
+  if (const BandPlan* p = op_band(op, cls)) {
     info[0] = 1;
-    info[1] = op->band->ntiles;
-    info[2] = op->band->nent;
-    info[3] = op->band->nnz;
-    info[4] = op->band->xcap;
-    info[5] = op->band->wmax;
-    info[6] = op->band->tr;
+    info[1] = p->ntiles;
+    info[2] = p->nent;
+    info[3] = p->nnz;
+    info[4] = p->xcap;
+    info[5] = p->wmax;
+    info[6] = p->tr;
   }
   return SAD_OK;
 }
@@ -692,14 +720,15 @@ static int check_block(sad_ctx* ctx, int r, int dtype) {
 }
 
 template <typename XT>
-static void op_band_args(const sad_op* op, SpmmArgs<XT>& a) {
-  if (!op->band) return;
-  a.band_meta = op->band->meta;
-  a.band_idx = op->band->idx;
-  a.band_val = op->band_val;
-  a.band_xcap = op->band->xcap;
-  a.band_wmax = op->band->wmax;
-  a.band_tr = op->band->tr;
+static void op_band_args(sad_op* op, SpmmArgs<XT>& a) {
+  const BandPlan* p = op_band(op, 0);
+  if (!p) return;
+  a.band_meta = p->meta;
+  a.band_idx = p->idx;
+  a.band_val = op->band_val[0];
+  a.band_xcap = p->xcap;
+  a.band_wmax = p->wmax;
+  a.band_tr = p->tr;
 }
 
 template <int MODE>
@@ -1404,7 +1433,12 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t finA = ((2 * m1 + 1) * R + 2 * m1 * R + ws->m * R) * 16 + (m1 + ws->m) * R * 8 +
                       8 * 4 + 64;
   const size_t gblk = R * m1 * m1 * 16;
-  const bool g_smem = finA + gblk <= 200 * 1024;
+  // SAD_GSMEM_KB caps the staged Gram block (A/B experiments on the L1 carve-out)
+  static const size_t gsmem_cap = [] {
+    const char* e = getenv("SAD_GSMEM_KB");
+    return (size_t)(e && *e ? atoi(e) : 200) * 1024;
+  }();
+  const bool g_smem = finA + gblk <= gsmem_cap;
   // phase-A TMA stages: one block-tile (kWarps * GPW * UA rows) of one basis block
   const size_t gpw = 32 / R, ua = ws->esz == 8 ? 8 : 4;
   const size_t tile_rows = (size_t)kWarps * gpw * ua;
@@ -1425,8 +1459,8 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t sums = 2 * m1 * R * ws->esz + (direct ? stage_rows_bytes : 0);
   // TMA path: the basis ring and the A1 CSR ring share one region
   const size_t vsz = op->vals_complex ? 16 : 8;
-  const size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
-                                                  (size_t)kStagesA1 * a1_stage_bytes((int)R, vsz));
+  size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
+                                            (size_t)kStagesA1 * a1_stage_bytes((int)R, vsz));
   // large-slab basis sweep: by basis block with direct loads when the block
   // width does not divide the warp (R = 3: config 3 sweep 228 -> 221 us per
   // A-side step, solve -3 %), through the TMA ring otherwise (config 4, R = 8:
@@ -1438,6 +1472,46 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     return std::string(e) == "tma" ? 0 : 1;
   }();
   const int sweep_direct = sweep_env >= 0 ? sweep_env : ((32 % ws->R) != 0 ? 1 : 0);
+  // Banded plan for the SpMM sub-phase (large slabs): the stages share the ring
+  // region; two blocks per SM must still fit, with at least two stages
+  const BandPlan* bp = nullptr;
+  BandCfg bcfg{};
+  static const int band_p_env = [] {
+    const char* e = getenv("SAD_BAND_PERSISTENT");
+    return e && *e ? atoi(e) : 1;
+  }();
+  // Only with the TMA-ring basis sweep: the by-basis-block sweep (block widths that
+  // do not divide the warp, config 3) reads w / v_j through L1, the banded stages
+  // push two blocks past the 196 KB carve-out (L1 60 -> 28 KB) and the sweeps lose
+  // 17 % while its SpMM sub-phase gains nothing (53 tiles per block).
+  if (!direct && !sweep_direct && band_p_env && (((size_t)ws->n * R * ws->esz) % 16) == 0) {
+    if (const BandPlan* p = op_band(op, 1)) {
+      auto al128 = [](size_t b) { return (b + 127) & ~size_t(127); };
+      const size_t xb = al128(32 + (size_t)p->xcap * R * ws->esz);
+      const size_t db = al128(32 + (size_t)p->xcap * ws->esz);
+      const size_t ib = al128((size_t)p->wmax * p->tr * 2);
+      const size_t vb = al128((size_t)p->wmax * p->tr * vsz);
+      const size_t sb = xb + db + ib + vb;
+      const size_t other = 2 * m1 * R * ws->esz;
+      const size_t cap = 92 * 1024;    // per block: two blocks stay within the 196 KB carve-out
+      const size_t recs = 2 * 32 * sizeof(BandMeta);   // tile records after the stages
+      int S = other + recs < cap ? (int)std::min<size_t>(kBandMaxStages, (cap - other - recs) / sb) : 0;
+      static const int s_env = [] {
+        const char* e = getenv("SAD_BAND_STAGES_P");
+        return e && *e ? atoi(e) : 0;
+      }();
+      if (s_env > 0) S = std::min(S, s_env);
+      if (S >= 2) {
+        bp = p;
+        bcfg.S = S;
+        bcfg.SB = (unsigned)sb;
+        bcfg.offD = (unsigned)xb;
+        bcfg.offI = (unsigned)(xb + db);
+        bcfg.offV = (unsigned)(xb + db + ib);
+        ring_bytes = std::max(ring_bytes, (size_t)S * sb + recs);
+      }
+    }
+  }
   size_t smem = std::max({ring_bytes + sums,                              // rings + sums
                           R * (m1 * 16 + ws->m * 24),                  // Givens staging
                           (size_t)kWarps * ws->m * 16,                 // back substitution
@@ -1453,6 +1527,13 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   cudaError_t e;
   if (ws->dtype == SAD_F64) {
     PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
+    if (bp) {
+      a.band_meta = bp->meta;
+      a.band_idx = bp->idx;
+      a.band_val = op->band_val[1];
+      a.band_tr = bp->tr;
+      a.band_cfg = bcfg;
+    }
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;
@@ -1464,6 +1545,13 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
+    if (bp) {
+      a.band_meta = bp->meta;
+      a.band_idx = bp->idx;
+      a.band_val = op->band_val[1];
+      a.band_tr = bp->tr;
+      a.band_cfg = bcfg;
+    }
     a.g_smem = g_smem ? 1 : 0;
     a.stage_bytes = (int)stage;
     a.direct_a = direct ? 1 : 0;

@@ -47,6 +47,11 @@ static cudaError_t coop_launch_t(PArgs<XT> a, const CoopCfg& cfg, cudaStream_t s
   if (grid > (long long)cfg.max_blocks) grid = cfg.max_blocks;
   if (grid < 1) grid = 1;
   a.rows_per_block = (a.n + grid - 1) / grid;
+  if (a.band_meta) {
+    // banded sub-phase A1: slabs are whole tiles
+    a.rows_per_block = (a.rows_per_block + a.band_tr - 1) / a.band_tr * a.band_tr;
+    grid = (a.n + a.rows_per_block - 1) / a.rows_per_block;
+  }
   if (a.direct_a && a.rows_per_block > a.direct_rows) return cudaErrorInvalidConfiguration;
   a.pT = cfg.max_blocks;
   void* args[] = {(void*)&a};

@@ -26,6 +26,7 @@
 
 #include "sad_kernels.cuh"
 #include "sad_spmm_bulk.cuh"
+#include "sad_spmm_band.cuh"
 
 namespace sad {
 
@@ -91,6 +92,13 @@ struct PArgs {
   int csr_budget;        // bytes available there (0 = CSR read from global)
   int sweep_direct;      // large slabs: basis sweep by basis block with direct loads (no TMA ring)
   int dbg_delay_ns;      // tests: the last block idles this long after every phase-C release
+  // banded plan for sub-phase A1 (sad_spmm_band.cuh; null: the CSR tiles): rows per
+  // block are a multiple of band_tr, the stages live in the ring region
+  const void* band_meta;
+  const unsigned short* band_idx;
+  const void* band_val;
+  int band_tr;
+  BandCfg band_cfg;
   PState st;
 };
 
@@ -298,9 +306,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   __shared__ __align__(8) unsigned long long s_full1[kStagesA1];
   __shared__ int s_off1[kStagesA1][3], s_kb1[kStagesA1], s_st1[kStagesA1];
   unsigned long long ring1 = 0;
+  // sub-phase A1 with a banded plan: tile records (two batches of 32), stage barriers
+  // (the records live in dynamic shared memory after the stages: static shared
+  // memory stays small -- two blocks of config 3 sit just under the 196 KB
+  // carve-out, and the next step, 228 KB, leaves 28 KB of L1 instead of 60 KB,
+  // which costs the basis sweeps 17 %)
+  __shared__ __align__(8) unsigned long long s_fullb[kBandMaxStages];
+  __shared__ int s_bW[kBandMaxStages], s_bself[kBandMaxStages];
+  unsigned long long ringb = 0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kStages; ++q) mbar_init(s_full + q, 1);
     for (int q = 0; q < kStagesA1; ++q) mbar_init(s_full1 + q, 1);
+    for (int q = 0; q < kBandMaxStages; ++q) mbar_init(s_fullb + q, 1);
     fence_mbar_init();
   }
   // The block's CSR slab stays in shared memory for the whole solve when it
@@ -536,6 +553,142 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           // ---- sub-phase A1: w = Op(D^-1 v_j) for the whole slab, CSR tiles
           // staged by TMA (kStagesA1 deep), one row per lane group, 5 gathers of
           // x in flight; w (and Z) written once, read back below from L2 ----
+          // ---- sub-phase A1 with a banded plan: the tile's x rows (v_j), Jacobi
+          // rows, 16-bit local columns and values staged by TMA, warp 0 issuing
+          // every copy of a tile from its own lane; all warps consume from shared
+          // memory (sad_spmm_band.cuh) ----
+          if (a.band_meta) {
+            const unsigned long long tsp = (timing && prof) ? gtimer() : 0ull;
+            const int TR = a.band_tr, S1 = a.band_cfg.S;
+            constexpr unsigned RB = R * sizeof(XT);
+            const BandMeta* metas = reinterpret_cast<const BandMeta*>(a.band_meta) + r0 / TR;
+            const VT* bvals = reinterpret_cast<const VT*>(a.band_val);
+            const long long ntile = r1 > r0 ? (r1 - r0 + TR - 1) / TR : 0;
+            BandMeta(*s_bmeta)[32] =
+                reinterpret_cast<BandMeta(*)[32]>(smem_c + (size_t)S1 * a.band_cfg.SB);
+            auto bfetch = [&](long long kk, int buf) {
+              if (kk < ntile) {
+                const int4* src = reinterpret_cast<const int4*>(metas + kk);
+                int4* dst = reinterpret_cast<int4*>(&s_bmeta[buf][lane]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[i] = __ldg(src + i);
+              }
+            };
+            auto bissue = [&](long long t) {   // warp 0, converged
+              const BandMeta& m = s_bmeta[(int)((t >> 5) & 1)][(int)(t & 31)];
+              const int q = (int)((ringb + t) % S1);
+              const unsigned nent = (unsigned)m.W * TR;
+              unsigned long long src = 0, dsrc = 0;
+              unsigned len = 0, dlen = 0, dst = 0, ddst = 0;
+              if (lane < m.nr) {
+                const unsigned long long s0 = reinterpret_cast<unsigned long long>(vj) + (unsigned long long)m.xs[lane] * RB;
+                const unsigned long long s1 = s0 + (unsigned long long)m.xl[lane] * RB;
+                src = s0 & ~15ull;
+                len = (unsigned)(((s1 + 15ull) & ~15ull) - src);
+                dst = 16u + (unsigned)m.ro[lane] * RB - (unsigned)(s0 - src);
+                if (PRE) {
+                  const unsigned long long d0 = reinterpret_cast<unsigned long long>(a.dinv) + (unsigned long long)m.xs[lane] * sizeof(XT);
+                  const unsigned long long d1 = d0 + (unsigned long long)m.xl[lane] * sizeof(XT);
+                  dsrc = d0 & ~15ull;
+                  dlen = (unsigned)(((d1 + 15ull) & ~15ull) - dsrc);
+                  ddst = a.band_cfg.offD + 16u + (unsigned)m.ro[lane] * (unsigned)sizeof(XT) - (unsigned)(d0 - dsrc);
+                }
+              } else if (lane == 30) {
+                src = reinterpret_cast<unsigned long long>(a.band_idx + m.eoff);
+                len = nent * 2u;
+                dst = a.band_cfg.offI;
+              } else if (lane == 31) {
+                src = reinterpret_cast<unsigned long long>(bvals + m.eoff);
+                len = nent * (unsigned)sizeof(VT);
+                dst = a.band_cfg.offV;
+              }
+              unsigned bytes = len + dlen;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+              unsigned char* sb = smem_c + (size_t)q * a.band_cfg.SB;
+              if (lane == 0) {
+                s_bW[q] = m.W;
+                s_bself[q] = m.self_off;
+                mbar_expect_tx(s_fullb + q, bytes);
+              }
+              __syncwarp();
+              if (len) bulk_g2s(sb + dst, reinterpret_cast<const void*>(src), len, s_fullb + q);
+              if (PRE && dlen) bulk_g2s(sb + ddst, reinterpret_cast<const void*>(dsrc), dlen, s_fullb + q);
+            };
+            if (warp == 0) {
+              bfetch(lane, 0);
+              bfetch(32 + lane, 1);
+              fence_proxy_async();
+              __syncwarp();
+              for (long long t = 0; t < min((long long)S1, ntile); ++t) bissue(t);
+            }
+            for (long long t = 0; t < ntile; ++t) {
+              const unsigned long long kk = ringb + t;
+              const int q = (int)(kk % S1);
+              mbar_wait(s_fullb + q, (unsigned)((kk / S1) & 1));
+              const unsigned char* sb = smem_c + (size_t)q * a.band_cfg.SB;
+              const XT* xs = reinterpret_cast<const XT*>(sb + 16);
+              const XT* ds = reinterpret_cast<const XT*>(sb + a.band_cfg.offD + 16);
+              const unsigned short* si = reinterpret_cast<const unsigned short*>(sb + a.band_cfg.offI);
+              const VT* sv = reinterpret_cast<const VT*>(sb + a.band_cfg.offV);
+              const int W = s_bW[q], self = s_bself[q];
+              const long long row0 = r0 + t * TR;
+              if (lane_ok) {
+                constexpr int UB = 2;
+                for (int rb = 0; rb < TR; rb += kWarps * GPW * UB) {
+                  int lr[UB];
+                  bool ok[UB];
+                  XT acc[UB];
+#pragma unroll
+                  for (int u = 0; u < UB; ++u) {
+                    lr[u] = rb + (u * kWarps + warp) * GPW + grp;
+                    ok[u] = lr[u] < TR && row0 + lr[u] < r1;
+                    if (!ok[u]) lr[u] = 0;
+                    acc[u] = zero<XT>();
+                  }
+                  if (!ok[0] && !ok[UB - 1]) continue;
+#pragma unroll 4
+                  for (int tt = 0; tt < W; ++tt) {
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                      const int e = tt * TR + lr[u];
+                      const int l = si[e];
+                      XT xv = xs[l * R + c];
+                      if (PRE) xv = mul(ds[l], xv);
+                      acc[u] = fma_(sv[e], xv, acc[u]);
+                    }
+                  }
+#pragma unroll
+                  for (int u = 0; u < UB; ++u) {
+                    if (!ok[u]) continue;
+                    const long long id = (row0 + lr[u]) * R + c;
+                    const int ls = self + lr[u];
+                    const XT xi = xs[ls * R + c];
+                    const XT xsc = PRE ? mul(ds[ls], xi) : xi;
+                    XT av = acc[u];
+                    if (SIGMA) av = fma_(from_c<XT>(a.sigma), xsc, av);
+                    const XT wv1 = sscal(sj, av);
+                    w[id] = wv1;
+                    if (FLEX) a.Z[(long long)j * a.stride + id] = sscal(sj, xsc);
+                    w2 += abs2(wv1);
+                  }
+                }
+              }
+              __syncthreads();   // stage q consumed
+              if (warp == 0 && t + S1 < ntile) {
+                const long long ti = t + S1;
+                if ((ti & 31) == 0) {
+                  // batch ti/32 is about to be issued: the other buffer's batch is
+                  // finished with, refill it with the batch after
+                  bfetch(ti + 32 + lane, (int)(((ti >> 5) & 1) ^ 1));
+                  __syncwarp();
+                }
+                bissue(ti);
+              }
+            }
+            ringb += (unsigned long long)ntile;
+            if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
+          } else
           {
             const unsigned long long tsp = (timing && prof) ? gtimer() : 0ull;
             constexpr int T1 = a1_tile_rows(R);

@@ -190,12 +190,14 @@ class DeviceOperator:
         self.handle = h
         self.is_real = (self.shift.imag == 0.0)
 
-    def band_info(self):
-        """The banded SpMM plan of this operator (sad_op_band_info): dict with
-        tiles, padded entries, nnz, max local x rows and padded row length, or
-        None when the operator runs the CSR kernels."""
+    def band_info(self, plan_class=0):
+        """The banded SpMM plan of this operator (sad_op_band_info; built on first
+        use): dict with tiles, padded entries, nnz, max local x rows, padded row
+        length and rows per tile, or None when the operator runs the CSR kernels.
+        plan_class 0: the stand-alone SpMM; 1: the persistent kernel's sub-phase."""
         info = np.zeros(7, dtype=np.int64)
-        _lib.check(_lib.load().sad_op_band_info(self.handle, info.ctypes.data), self._ctx)
+        _lib.check(_lib.load().sad_op_band_info(self.handle, int(plan_class), info.ctypes.data),
+                   self._ctx)
         if not info[0]:
             return None
         return dict(tiles=int(info[1]), entries=int(info[2]), nnz=int(info[3]),

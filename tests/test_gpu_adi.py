@@ -134,3 +134,22 @@ def test_reduced_configs_match_oracle(name):
     sol, rep, state = _gpu_run(name)
     _check_against_golden(rep, name)
     _x_parity(name, sol)
+
+
+def test_chunked_factor_download_matches_concat(monkeypatch, rng):
+    """LowRankSolution._stack (adi.py:529-530 layout: Z = [z_1 ... z_k]): the
+    double-buffered chunked download of large factors equals the one-copy path,
+    for real and complex blocks and a ragged last chunk."""
+    import torch
+    from paper_2312_02891_b200.adi import LowRankSolution
+    rows, r, k = 1531, 3, 7
+    for dt in (torch.complex128, torch.float64):
+        blocks = [torch.randn(rows, r, dtype=dt, device="cuda") for _ in range(k)]
+        want = np.hstack([b.cpu().numpy().astype(complex) for b in blocks])
+        monkeypatch.setattr(LowRankSolution, "CONCAT_BYTES", 1 << 40)
+        assert np.array_equal(LowRankSolution._stack(blocks, rows, r), want)
+        monkeypatch.setattr(LowRankSolution, "CONCAT_BYTES", 0)
+        monkeypatch.setattr(LowRankSolution, "STAGE_BYTES", 200 * k * r * 16)   # 8 chunks
+        monkeypatch.setattr(LowRankSolution, "_STAGING", None)
+        got = LowRankSolution._stack(blocks, rows, r)
+        assert got.shape == want.shape and np.array_equal(got, want)

@@ -108,27 +108,35 @@ def test_band_3d_and_irregular_patterns(monkeypatch, rng):
     assert np.max(np.abs(host(rb.apply(dev(xr))) - want)) <= 1e-13 * np.max(np.abs(want))
 
 
-@pytest.mark.parametrize("engine", ["multi", "persistent"])
+@pytest.mark.parametrize("engine", ["multi", "persistent", "persistent-tma"])
 @pytest.mark.parametrize("flexible", [False, True])
-def test_gmres_with_band_plan_matches_csr_path(monkeypatch, rng, engine, flexible):
+@pytest.mark.parametrize("r,cplx", [(3, True), (8, False), (4, True), (1, False)])
+def test_gmres_with_band_plan_matches_csr_path(monkeypatch, rng, engine, flexible, r, cplx):
     """Jacobi-GMRES through the banded SpMM (Jacobi prologue from the staged dinv
-    rows, Arnoldi-mode scaling, FGMRES Z): identical iteration counts and
+    rows, Arnoldi-mode scaling, FGMRES Z) -- the stand-alone kernel in the
+    multi-kernel engine, the SpMM sub-phase inside the persistent kernel
+    ("persistent-tma": its large-slab path) -- identical iteration counts and
     solutions to 1e-10 against the same solve on the CSR kernels."""
     from paper_2312_02891_b200 import GpuGmresBinding
     A = fd2(48, 60.0)
     n = A.shape[0]
-    b = rng.standard_normal((n, 3)) + 1j * rng.standard_normal((n, 3))
-    shift = -250.0 + 90.0j
+    b = rng.standard_normal((n, r)) + (1j * rng.standard_normal((n, r)) if cplx else 0.0)
+    shift = -250.0 + (90.0j if cplx else 0.0)
     out = []
+    eng, _, pa = engine.partition("-")
     for flag in ("1", "0"):
         monkeypatch.setenv("SAD_SPMM_BAND", flag)
         gb = GpuGmresBinding("A", A, None, precond_kind="jacobi", restart=30, flexible=flexible,
-                             engine=engine)
-        assert (gb.operator(shift).band_info() is not None) == (flag == "1")
+                             engine=eng, phase_a=pa or "auto")
+        cls = 1 if eng == "persistent" else 0
+        info = gb.operator(shift).band_info(cls)
+        assert (info is not None) == (flag == "1")
         out.append(gb.solve(shift, b, 1e-8))
     got, ref = out
     assert np.array_equal(got.iterations, ref.iterations)
     assert np.all(got.converged)
     assert np.linalg.norm(got.solution - ref.solution) <= 1e-10 * np.linalg.norm(ref.solution)
-    orc_res = orc.Binding("A", A, None, solver="fgmres" if flexible else "gmres", restart=30).solve(shift, b, 1e-8)
-    assert np.all(np.abs(got.iterations - orc_res.iterations) <= 2)
+    if r <= 3:
+        orc_res = orc.Binding("A", A, None, solver="fgmres" if flexible else "gmres", restart=30,
+                              orth="dcgs2" if eng == "persistent" else "cgs2").solve(shift, b, 1e-8)
+        assert np.all(np.abs(got.iterations - orc_res.iterations) <= 2)
