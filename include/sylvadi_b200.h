@@ -407,9 +407,11 @@ typedef struct {
   int max_inner_iterations;
   double outer_tolerance;
   double xi;
-  double gap_budget;           /* <= 0: outer_tolerance * ||f g^*|| (adi.py:563-565) */
+  double gap_budget;           /* used when has_gap_budget != 0 */
   double fixed_delta;
   double delta_min_A, delta_max_A, delta_min_B, delta_max_B;
+  int has_gap_budget;          /* 0: AdiConfig.gap_budget is None -> outer_tolerance * ||f g^*||
+                                  (adi.py:563-565); a budget of 0.0 is a budget */
 } sad_adi_config;
 /* records[k][14] per step: scaled_res, delta_A, delta_B, achieved_rA,
  * achieved_rB, inner_it_A, inner_it_B, u, v, a_converged, b_converged,

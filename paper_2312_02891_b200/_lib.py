@@ -128,7 +128,8 @@ class AdiConfigC(_c.Structure):
                 ("outer_tolerance", _c.c_double), ("xi", _c.c_double),
                 ("gap_budget", _c.c_double), ("fixed_delta", _c.c_double),
                 ("delta_min_A", _c.c_double), ("delta_max_A", _c.c_double),
-                ("delta_min_B", _c.c_double), ("delta_max_B", _c.c_double)]
+                ("delta_min_B", _c.c_double), ("delta_max_B", _c.c_double),
+                ("has_gap_budget", _c.c_int)]
 
 
 SAD_ADI_REC = 14

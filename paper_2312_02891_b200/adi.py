@@ -749,7 +749,8 @@ class DeviceAdi:
             strategy=_lib.STRATEGY_CODES[_strategy(cfg.strategy).value], kmax=K,
             max_inner_iterations=int(cfg.max_inner_iterations),
             outer_tolerance=cfg.outer_tolerance, xi=cfg.xi,
-            gap_budget=-1.0 if cfg.gap_budget is None else float(cfg.gap_budget),
+            gap_budget=0.0 if cfg.gap_budget is None else float(cfg.gap_budget),
+            has_gap_budget=0 if cfg.gap_budget is None else 1,
             fixed_delta=cfg.fixed_delta, delta_min_A=cfg.delta_min_A, delta_max_A=cfg.delta_max_A,
             delta_min_B=cfg.delta_min_B, delta_max_B=cfg.delta_max_B)
         recs = np.zeros((K, _lib.SAD_ADI_REC), dtype=np.float64)

@@ -36,7 +36,7 @@ class ConfigSpec:
 
     @property
     def shift_file(self):
-        return os.path.join(SHIFT_DIR, f"shifts_{self.name}.json")
+        return os.path.join(SHIFT_DIR, f"shifts_{self.extra.get('shifts', self.name)}.json")
 
     def load_shift_pairs(self):
         """ShiftSequence JSON (shifts.py:53-67 layout) -> list of (alpha, beta)."""
@@ -82,6 +82,13 @@ def _c3s_matrices():
     return _c3_matrices(n0_a=48, n0_b=40)
 
 
+def _c3m_matrices():
+    """Config 3 at an intermediate size (250^2 / 175^2) with the FULL-size
+    problem's pinned shifts: the regime where the small pair alpha ~ -1535,
+    beta ~ -1575 makes the A-side Jacobi-GMRES(40) stagnate."""
+    return _c3_matrices(n0_a=250, n0_b=175)
+
+
 def _c5s_matrices():
     """Config 5 operator family at proxy size (n0=16 / 13)."""
     return _c5_matrices(n0_a=16, n0_b=13)
@@ -105,12 +112,16 @@ CONFIGS = {
                      npairs=16),
     "c3s": ConfigSpec("c3s", "config 3 at 48^2 / 40^2 (generalised pencils), r=3, GMRES(40)",
                       r=3, seed=0, kmax=150, restart=40, flexible=False, npairs=10),
+    "c3m": ConfigSpec("c3m", "config 3 at 250^2 / 175^2 with config 3's own shifts, r=3, GMRES(40)",
+                      r=3, seed=0, kmax=8, restart=40, flexible=False, npairs=10,
+                      extra={"shifts": "c3"}),
     "c5s": ConfigSpec("c5s", "config 5 family at 16^3 / 13^3, r=4, GMRES(30)",
                       r=4, seed=0, kmax=400, restart=30, flexible=False, npairs=16),
 }
 
 _BUILDERS = {"c1": _c1_matrices, "c2": _c2_matrices, "c3": _c3_matrices,
-             "c5": _c5_matrices, "c3s": _c3s_matrices, "c5s": _c5s_matrices}
+             "c5": _c5_matrices, "c3s": _c3s_matrices, "c5s": _c5s_matrices,
+             "c3m": _c3m_matrices}
 
 
 def build_problem(name, **sizes):

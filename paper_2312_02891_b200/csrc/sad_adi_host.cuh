@@ -209,7 +209,7 @@ extern "C" int sad_adi_run(sad_ctx* ctx, const sad_adi_config* cfg, int r, int d
     summary[2] = 0.0;
     return SAD_OK;
   }
-  const double gap = cfg->gap_budget > 0.0 ? cfg->gap_budget : cfg->outer_tolerance * res0;
+  const double gap = cfg->has_gap_budget ? cfg->gap_budget : cfg->outer_tolerance * res0;
   double u = 0.0, v = 0.0, res = res0;
   int64_t itA[8], itB[8];
   double nrA[8], nrB[8];

@@ -22,7 +22,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-PROBES = {"c1": 8, "c2": 4, "c3s": 8, "c5s": 8}
+PROBES = {"c1": 8, "c2": 4, "c3s": 8, "c5s": 8, "c3m": 8}
+#: configurations whose per-step oracle records are written here too
+WITH_CSV = ("c3m",)
 
 
 def probes(n, k):
@@ -66,6 +68,9 @@ def make(name):
              steps=len(ref.gammas), r=r, x_fro=xnorm,
              inner_A=np.array([s.inner_it_A for s in ref.records]),
              inner_B=np.array([s.inner_it_B for s in ref.records]))
+    if name in WITH_CSV:
+        with open(os.path.join(HERE, f"oracle_{name}_gmres.csv"), "w") as fh:
+            fh.write(orc.steps_csv(ref))
     return name, len(ref.gammas), xnorm, float(np.linalg.norm(S))
 
 

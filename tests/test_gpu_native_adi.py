@@ -23,7 +23,8 @@ def _engine(name, **kw):
     pairs, cyclic = spec.load_shift_pairs()
     prob = pb.SylvesterProblem(A=A, B=B, f=f, g=g, M=M, C=C)
     strategy = kw.pop("strategy", spec.strategy)
-    cfg = pb.AdiConfig(strategy=strategy, kmax=spec.kmax, outer_tolerance=spec.outer_tolerance,
+    cfg = pb.AdiConfig(strategy=strategy, kmax=kw.pop("kmax", spec.kmax),
+                       outer_tolerance=spec.outer_tolerance, gap_budget=kw.pop("gap_budget", None),
                        precond_kind_A="jacobi", precond_kind_B="jacobi")
     seq = pb.ShiftSequence(pairs=pairs, cyclic=cyclic)
     return pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible, **kw)
@@ -87,3 +88,19 @@ def test_native_gram_algebra_r_gt_2():
     for a, b in zip(rep_n.records, rep_p.records):
         assert abs(a.achieved_rA - b.achieved_rA) <= 1e-9 * b.achieved_rA
         assert abs(a.scaled_res - b.scaled_res) <= 1e-6 * b.scaled_res
+
+
+@pytest.mark.parametrize("gap", [0.0, 3e-7])
+def test_native_loop_explicit_gap_budget(gap):
+    """AdiConfig.gap_budget is used whenever it is not None (adi.py:563-565): a
+    budget of 0.0 is a budget (all tolerances at their lower clamps), not "unset"."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        eng = _engine("c1", kmax=4, gap_budget=gap)
+        _, rep_n, _ = eng.run()
+        _, rep_p, _ = eng._run_python()
+        _, rep_d, _ = _engine("c1", kmax=4).run()
+    for a, b, d in zip(rep_n.records, rep_p.records, rep_d.records):
+        assert abs(a.delta_A - b.delta_A) <= 1e-6 * b.delta_A
+        assert abs(a.delta_B - b.delta_B) <= 1e-6 * b.delta_B
+        assert a.delta_A != d.delta_A           # not the default outer_tolerance * ||f g^*||
