@@ -200,7 +200,7 @@ BandPlan* band_build_tr(sad_ctx* ctx, long long n, const std::vector<int>& rp, c
 // memory; small matrices take 64 (more tiles than SMs matter more there).
 // Class 1 (the persistent GMRES kernel's SpMM sub-phase, two blocks per SM next
 // to the kernel's other shared memory): 128-row tiles when two stages fit in
-// ~70 KB, else 64.  SAD_BAND_ROWS / SAD_BAND_ROWS_P override (multiples of 8).
+// ~90 KB, else 64.  SAD_BAND_ROWS / SAD_BAND_ROWS_P override (multiples of 8).
 BandPlan* band_build(sad_ctx* ctx, long long n, const std::vector<int>& rp, const std::vector<int>& ci,
                      int cls) {
   const char* e = std::getenv(cls ? "SAD_BAND_ROWS_P" : "SAD_BAND_ROWS");
@@ -211,7 +211,7 @@ BandPlan* band_build(sad_ctx* ctx, long long n, const std::vector<int>& rp, cons
       if (BandPlan* p = band_build_tr(ctx, n, rp, ci, tr, 70 * 1024)) return p;
     }
   } else if (n >= (long long)128 * ctx->nsm * 8) {
-    if (BandPlan* p = band_build_tr(ctx, n, rp, ci, 128, 35 * 1024)) return p;
+    if (BandPlan* p = band_build_tr(ctx, n, rp, ci, 128, 46 * 1024)) return p;
   }
   return band_build_tr(ctx, n, rp, ci, 64, 0);
 }

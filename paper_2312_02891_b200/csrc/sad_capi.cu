@@ -1480,11 +1480,13 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     const char* e = getenv("SAD_BAND_PERSISTENT");
     return e && *e ? atoi(e) : 1;
   }();
-  // Only with the TMA-ring basis sweep: the by-basis-block sweep (block widths that
-  // do not divide the warp, config 3) reads w / v_j through L1, the banded stages
-  // push two blocks past the 196 KB carve-out (L1 60 -> 28 KB) and the sweeps lose
-  // 17 % while its SpMM sub-phase gains nothing (53 tiles per block).
-  if (!direct && !sweep_direct && band_p_env && (((size_t)ws->n * R * ws->esz) % 16) == 0) {
+  // With the by-basis-block sweep (block widths that do not divide the warp, config 3)
+  // w / v_j are read through L1: stages that push two blocks past the 196 KB
+  // carve-out (L1 60 -> 28 KB) cost the sweeps 17 %, so there the stages may only
+  // use what the kernel's other phases already need (no growth).
+  const size_t smem_base = std::max({ring_bytes + sums, R * (m1 * 16 + ws->m * 24),
+                                     (size_t)kWarps * ws->m * 16, finA + (g_smem ? gblk : 0)});
+  if (!direct && band_p_env && (((size_t)ws->n * R * ws->esz) % 16) == 0) {
     if (const BandPlan* p = op_band(op, 1)) {
       auto al128 = [](size_t b) { return (b + 127) & ~size_t(127); };
       const size_t xb = al128(32 + (size_t)p->xcap * R * ws->esz);
@@ -1493,7 +1495,12 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
       const size_t vb = al128((size_t)p->wmax * p->tr * vsz);
       const size_t sb = xb + db + ib + vb;
       const size_t other = 2 * m1 * R * ws->esz;
-      const size_t cap = 92 * 1024;    // per block: two blocks stay within the 196 KB carve-out
+      // per block: two blocks stay within the 196 KB carve-out (SAD_BAND_CAP_KB: A/B runs)
+      static const size_t cap_env = [] {
+        const char* e = getenv("SAD_BAND_CAP_KB");
+        return (size_t)(e && *e ? atoi(e) : 92) * 1024;
+      }();
+      const size_t cap = sweep_direct ? std::min(cap_env, smem_base) : cap_env;
       const size_t recs = 2 * 32 * sizeof(BandMeta);   // tile records after the stages
       int S = other + recs < cap ? (int)std::min<size_t>(kBandMaxStages, (cap - other - recs) / sb) : 0;
       static const int s_env = [] {
@@ -1524,6 +1531,10 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t csr_budget = (direct && ws->resident_csr && csr_off + 4096 <= per_block_cap)
                                 ? per_block_cap - csr_off : 0;
   if (csr_budget) smem = csr_off + csr_budget;
+  static const int ring_c_env = [] {
+    const char* e = getenv("SAD_RING_C");
+    return e && *e ? atoi(e) : 2;
+  }();
   cudaError_t e;
   if (ws->dtype == SAD_F64) {
     PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
@@ -1542,6 +1553,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
     a.sweep_direct = sweep_direct;
+    a.ring_c = ring_c_env;
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
@@ -1560,6 +1572,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.csr_off = (int)csr_off;
     a.csr_budget = (int)csr_budget;
     a.sweep_direct = sweep_direct;
+    a.ring_c = ring_c_env;
     e = coop_dispatch_z(a, ws, op, s, smem);
   }
   if (e != cudaSuccess)

@@ -91,6 +91,8 @@ struct PArgs {
   int csr_off;           // dynamic-smem byte offset of the resident CSR slab
   int csr_budget;        // bytes available there (0 = CSR read from global)
   int sweep_direct;      // large slabs: basis sweep by basis block with direct loads (no TMA ring)
+  int ring_c;            // large slabs: phase C through the TMA ring (SAD_RING_C: 0 off, 1 only with
+                         // the TMA-ring phase-A sweep, 2 = default: always)
   int dbg_delay_ns;      // tests: the last block idles this long after every phase-C release
   // banded plan for sub-phase A1 (sad_spmm_band.cuh; null: the CSR tiles): rows per
   // block are a multiple of band_tr, the stages live in the ring region
@@ -311,13 +313,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   // memory stays small -- two blocks of config 3 sit just under the 196 KB
   // carve-out, and the next step, 228 KB, leaves 28 KB of L1 instead of 60 KB,
   // which costs the basis sweeps 17 %)
-  __shared__ __align__(8) unsigned long long s_fullb[kBandMaxStages];
+  __shared__ __align__(8) unsigned long long s_fullb[kBandMaxStages], s_emptyb[kBandMaxStages];
   __shared__ int s_bW[kBandMaxStages], s_bself[kBandMaxStages];
   unsigned long long ringb = 0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kStages; ++q) mbar_init(s_full + q, 1);
     for (int q = 0; q < kStagesA1; ++q) mbar_init(s_full1 + q, 1);
-    for (int q = 0; q < kBandMaxStages; ++q) mbar_init(s_fullb + q, 1);
+    for (int q = 0; q < kBandMaxStages; ++q) {
+      mbar_init(s_fullb + q, 1);
+      mbar_init(s_emptyb + q, kWarps - 1);
+    }
     fence_mbar_init();
   }
   // The block's CSR slab stays in shared memory for the whole solve when it
@@ -615,77 +620,86 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               if (len) bulk_g2s(sb + dst, reinterpret_cast<const void*>(src), len, s_fullb + q);
               if (PRE && dlen) bulk_g2s(sb + ddst, reinterpret_cast<const void*>(dsrc), dlen, s_fullb + q);
             };
+            // warp 0 produces (runs up to S1 tiles ahead, waiting on the stage's
+            // "empty" barrier), warps 1..7 consume: no block-wide synchronisation
+            // per tile, the copies of the next tiles are always in flight
             if (warp == 0) {
               bfetch(lane, 0);
               bfetch(32 + lane, 1);
               fence_proxy_async();
               __syncwarp();
-              for (long long t = 0; t < min((long long)S1, ntile); ++t) bissue(t);
-            }
-            for (long long t = 0; t < ntile; ++t) {
-              const unsigned long long kk = ringb + t;
-              const int q = (int)(kk % S1);
-              mbar_wait(s_fullb + q, (unsigned)((kk / S1) & 1));
-              const unsigned char* sb = smem_c + (size_t)q * a.band_cfg.SB;
-              const XT* xs = reinterpret_cast<const XT*>(sb + 16);
-              const XT* ds = reinterpret_cast<const XT*>(sb + a.band_cfg.offD + 16);
-              const unsigned short* si = reinterpret_cast<const unsigned short*>(sb + a.band_cfg.offI);
-              const VT* sv = reinterpret_cast<const VT*>(sb + a.band_cfg.offV);
-              const int W = s_bW[q], self = s_bself[q];
-              const long long row0 = r0 + t * TR;
-              if (lane_ok) {
-                constexpr int UB = 2;
-                for (int rb = 0; rb < TR; rb += kWarps * GPW * UB) {
-                  int lr[UB];
-                  bool ok[UB];
-                  XT acc[UB];
-#pragma unroll
-                  for (int u = 0; u < UB; ++u) {
-                    lr[u] = rb + (u * kWarps + warp) * GPW + grp;
-                    ok[u] = lr[u] < TR && row0 + lr[u] < r1;
-                    if (!ok[u]) lr[u] = 0;
-                    acc[u] = zero<XT>();
-                  }
-                  if (!ok[0] && !ok[UB - 1]) continue;
-#pragma unroll 4
-                  for (int tt = 0; tt < W; ++tt) {
-#pragma unroll
-                    for (int u = 0; u < UB; ++u) {
-                      const int e = tt * TR + lr[u];
-                      const int l = si[e];
-                      XT xv = xs[l * R + c];
-                      if (PRE) xv = mul(ds[l], xv);
-                      acc[u] = fma_(sv[e], xv, acc[u]);
-                    }
-                  }
-#pragma unroll
-                  for (int u = 0; u < UB; ++u) {
-                    if (!ok[u]) continue;
-                    const long long id = (row0 + lr[u]) * R + c;
-                    const int ls = self + lr[u];
-                    const XT xi = xs[ls * R + c];
-                    const XT xsc = PRE ? mul(ds[ls], xi) : xi;
-                    XT av = acc[u];
-                    if (SIGMA) av = fma_(from_c<XT>(a.sigma), xsc, av);
-                    const XT wv1 = sscal(sj, av);
-                    w[id] = wv1;
-                    if (FLEX) a.Z[(long long)j * a.stride + id] = sscal(sj, xsc);
-                    w2 += abs2(wv1);
-                  }
-                }
-              }
-              __syncthreads();   // stage q consumed
-              if (warp == 0 && t + S1 < ntile) {
-                const long long ti = t + S1;
-                if ((ti & 31) == 0) {
-                  // batch ti/32 is about to be issued: the other buffer's batch is
-                  // finished with, refill it with the batch after
-                  bfetch(ti + 32 + lane, (int)(((ti >> 5) & 1) ^ 1));
+              for (long long t = 0; t < ntile; ++t) {
+                if ((t & 31) == 0 && t > 0) {
+                  bfetch(t + 32 + lane, (int)(((t >> 5) & 1) ^ 1));
                   __syncwarp();
                 }
-                bissue(ti);
+                const unsigned long long kk = ringb + t;
+                if (lane == 0 && kk >= (unsigned long long)S1)
+                  mbar_wait(s_emptyb + (int)(kk % S1), (unsigned)(((kk / S1) - 1) & 1));
+                __syncwarp();
+                bissue(t);
+              }
+            } else {
+              constexpr int CW = kWarps - 1;   // consumer warps
+              const int cw = warp - 1;
+              for (long long t = 0; t < ntile; ++t) {
+                const unsigned long long kk = ringb + t;
+                const int q = (int)(kk % S1);
+                mbar_wait(s_fullb + q, (unsigned)((kk / S1) & 1));
+                const unsigned char* sb = smem_c + (size_t)q * a.band_cfg.SB;
+                const XT* xs = reinterpret_cast<const XT*>(sb + 16);
+                const XT* ds = reinterpret_cast<const XT*>(sb + a.band_cfg.offD + 16);
+                const unsigned short* si = reinterpret_cast<const unsigned short*>(sb + a.band_cfg.offI);
+                const VT* sv = reinterpret_cast<const VT*>(sb + a.band_cfg.offV);
+                const int W = s_bW[q], self = s_bself[q];
+                const long long row0 = r0 + t * TR;
+                if (lane_ok) {
+                  constexpr int UB = 2;
+                  for (int rb = 0; rb < TR; rb += CW * GPW * UB) {
+                    int lr[UB];
+                    bool ok[UB];
+                    XT acc[UB];
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                      lr[u] = rb + (u * CW + cw) * GPW + grp;
+                      ok[u] = lr[u] < TR && row0 + lr[u] < r1;
+                      if (!ok[u]) lr[u] = 0;
+                      acc[u] = zero<XT>();
+                    }
+                    if (!ok[0] && !ok[UB - 1]) continue;
+#pragma unroll 4
+                    for (int tt = 0; tt < W; ++tt) {
+#pragma unroll
+                      for (int u = 0; u < UB; ++u) {
+                        const int e = tt * TR + lr[u];
+                        const int l = si[e];
+                        XT xv = xs[l * R + c];
+                        if (PRE) xv = mul(ds[l], xv);
+                        acc[u] = fma_(sv[e], xv, acc[u]);
+                      }
+                    }
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                      if (!ok[u]) continue;
+                      const long long id = (row0 + lr[u]) * R + c;
+                      const int ls = self + lr[u];
+                      const XT xi = xs[ls * R + c];
+                      const XT xsc = PRE ? mul(ds[ls], xi) : xi;
+                      XT av = acc[u];
+                      if (SIGMA) av = fma_(from_c<XT>(a.sigma), xsc, av);
+                      const XT wv1 = sscal(sj, av);
+                      w[id] = wv1;
+                      if (FLEX) a.Z[(long long)j * a.stride + id] = sscal(sj, xsc);
+                      w2 += abs2(wv1);
+                    }
+                  }
+                }
+                __syncwarp();
+                if (lane == 0)
+                  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(s_emptyb + q)) : "memory");
               }
             }
+            __syncthreads();   // every tile written before the sweep reads w back
             ringb += (unsigned long long)ntile;
             if (timing && prof) t_acc[6] += (double)(gtimer() - tsp);
           } else
@@ -1085,10 +1099,82 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
       // ======== phase C: w -= V coef, ||w||^2 -> Givens ========
       {
         XT* w = a.V + (long long)J * a.stride;
-        XT* s_coef = reinterpret_cast<XT*>(smem_p);
+        // large slabs with the TMA-ring sweep: the coefficients sit after the ring
+        const bool ringC = !a.direct_a && (a.ring_c > 1 || (a.ring_c && !a.sweep_direct));
+        XT* s_coef = ringC ? reinterpret_cast<XT*>(reinterpret_cast<unsigned char*>(smem_p) + (size_t)a.ring_bytes)
+                           : reinterpret_cast<XT*>(smem_p);
         for (int o = threadIdx.x; o < J * R; o += kThreads) s_coef[o] = from_c<XT>(ldcg2(st.coef + o));
         __syncthreads();
         double n2 = 0.0;
+        if (ringC) {
+          // The basis is streamed through the phase-A TMA ring (one stage = the
+          // tile's rows of one basis block, kStages deep): the update sweep then
+          // runs at the rate of the phase-A sweep (config 4: 5.1 -> ~6 TB/s)
+          // instead of at what the direct loads of 16 warps per SM sustain.
+          unsigned char* const smem_c = reinterpret_cast<unsigned char*>(smem_p);
+          constexpr int T = kWarps * GPW * UA;
+          for (long long base = r0; base < r1; base += T) {
+            const long long nrows = min((long long)T, r1 - base);
+            auto issue = [&](int i, int q) {
+              const unsigned long long src =
+                  reinterpret_cast<unsigned long long>(a.V + (long long)i * a.stride + base * R);
+              const unsigned long long e = src + (unsigned long long)(nrows * R) * sizeof(XT);
+              const unsigned long long a0 = src & ~15ull, a1 = (e + 15ull) & ~15ull;
+              s_soff[q] = (int)((src - a0) / sizeof(XT));
+              mbar_expect_tx(s_full + q, (unsigned)(a1 - a0));
+              bulk_g2s(smem_c + (size_t)q * a.stage_bytes, reinterpret_cast<const void*>(a0),
+                       (unsigned)(a1 - a0), s_full + q);
+            };
+            if (threadIdx.x == 0) {
+              fence_proxy_async();
+              for (int i = 0; i < min(kStages, J); ++i) issue(i, (int)((ring + i) % kStages));
+            }
+            XT acc[UA];
+            long long idx[UA];
+            int lr[UA];
+#pragma unroll
+            for (int u = 0; u < UA; ++u) {
+              lr[u] = (u * kWarps + warp) * GPW + grp;
+              idx[u] = (lane_ok && lr[u] < nrows) ? (base + lr[u]) * R + c : -1;
+              if (idx[u] < 0) lr[u] = 0;
+              acc[u] = zero<XT>();
+            }
+            for (int i0 = 0; i0 < J; i0 += kGroup) {
+              const int ng = min(kGroup, J - i0);
+#pragma unroll
+              for (int gi = 0; gi < kGroup; ++gi) {
+                if (gi < ng) {
+                  const unsigned long long kk = ring + i0 + gi;
+                  const int q = (int)(kk % kStages);
+                  mbar_wait(s_full + q, (unsigned)((kk / kStages) & 1));
+                  if (lane_ok) {
+                    const XT* Vs =
+                        reinterpret_cast<const XT*>(smem_c + (size_t)q * a.stage_bytes) + s_soff[q];
+                    const XT cf = s_coef[(i0 + gi) * R + c];
+#pragma unroll
+                    for (int u = 0; u < UA; ++u) acc[u] = fma_(Vs[lr[u] * R + c], cf, acc[u]);
+                  }
+                }
+              }
+              __syncthreads();   // the group's stages are consumed
+              if (threadIdx.x == 0) {
+                fence_proxy_async();
+                for (int gi = 0; gi < ng; ++gi) {
+                  const int i = i0 + gi;
+                  if (i + kStages < J) issue(i + kStages, (int)((ring + i) % kStages));
+                }
+              }
+            }
+            ring += J;
+#pragma unroll
+            for (int u = 0; u < UA; ++u) {
+              if (idx[u] < 0) continue;
+              const XT wv = sub(w[idx[u]], acc[u]);
+              w[idx[u]] = wv;
+              n2 += abs2(wv);
+            }
+          }
+        } else
         for (long long base = r0; base < r1; base += (long long)kWarps * GPW * UC) {
           XT acc[UC];
           long long idx[UC];
