@@ -1456,7 +1456,8 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
                                   : (size_t)ws->n <= 2 * tile_rows * (size_t)sms;
   if (direct && stage_rows_bytes > 96 * 1024) direct = false;   // rows do not fit: TMA ring
   const size_t stage = direct ? 0 : ((tile_rows * R * ws->esz + 32 + 127) & ~size_t(127));
-  const size_t sums = 2 * m1 * R * ws->esz + (direct ? stage_rows_bytes : 0);
+  // s_blk [2(m+1)R] + the ring sweep's per-warp sums (two parity buffers)
+  const size_t sums = 2 * m1 * R * ws->esz + (direct ? stage_rows_bytes : 4 * kGroup * kWarps * R * ws->esz);
   // TMA path: the basis ring and the A1 CSR ring share one region
   const size_t vsz = op->vals_complex ? 16 : 8;
   size_t ring_bytes = direct ? 0 : std::max((size_t)kStages * stage,
@@ -1494,7 +1495,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
       const size_t ib = al128((size_t)p->wmax * p->tr * 2);
       const size_t vb = al128((size_t)p->wmax * p->tr * vsz);
       const size_t sb = xb + db + ib + vb;
-      const size_t other = 2 * m1 * R * ws->esz;
+      const size_t other = sums;
       // per block: two blocks stay within the 196 KB carve-out (SAD_BAND_CAP_KB: A/B runs)
       static const size_t cap_env = [] {
         const char* e = getenv("SAD_BAND_CAP_KB");

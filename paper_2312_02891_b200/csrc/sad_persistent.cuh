@@ -302,7 +302,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   // phase-A TMA ring
   __shared__ __align__(8) unsigned long long s_full[kStages];
   __shared__ int s_soff[kStages];
-  __shared__ XT s_ph[kGroup][kWarps][R], s_pg[kGroup][kWarps][R];
   unsigned long long ring = 0;   // basis-tile copies issued so far (block-uniform)
   // sub-phase A1 CSR ring
   __shared__ __align__(8) unsigned long long s_full1[kStagesA1];
@@ -455,6 +454,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         // h / g contributions through shared memory in a fixed order.
         unsigned char* const smem_c = reinterpret_cast<unsigned char*>(smem_p);
         XT* s_blk = reinterpret_cast<XT*>(smem_c + (size_t)a.ring_bytes);  // [2J][R]
+        // per-warp sums of the ring sweep, two buffers by group parity (after s_blk's
+        // 2(m+1)R slots): the group after next only overwrites a buffer once warp 0
+        // has been through the next group's __syncthreads, so ONE block-wide
+        // synchronisation per group is enough
+        XT* s_pw = s_blk + (size_t)2 * (m + 1) * R;   // [2][2][kGroup][kWarps][R]
         for (int o = threadIdx.x; o < 2 * J * R; o += kThreads) s_blk[o] = zero<XT>();
         double w2 = 0.0;
         __syncthreads();
@@ -879,7 +883,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                 }
               }
             }
-          } else
+          } else {
+          unsigned gcount = 0;   // groups so far: the parity of the per-warp sum buffers
           for (long long base = r0; base < r1; base += T) {
             const long long nrows = min((long long)T, r1 - base);
             auto issue = [&](int i, int q) {
@@ -939,20 +944,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                   const XT h = group_reduce<R>(ph[gi], grp);
                   const XT gq = group_reduce<R>(pg[gi], grp);
                   if (grp == 0 && lane_ok) {
-                    s_ph[gi][warp][c] = h;
-                    s_pg[gi][warp][c] = gq;
+                    XT* pw = s_pw + (size_t)(gcount & 1u) * 2 * kGroup * kWarps * R;
+                    pw[(gi * kWarps + warp) * R + c] = h;
+                    pw[((kGroup + gi) * kWarps + warp) * R + c] = gq;
                   }
                 }
               }
               __syncthreads();
               if (warp == 0 && lane < R) {
+                const XT* pw0 = s_pw + (size_t)(gcount & 1u) * 2 * kGroup * kWarps * R;
                 for (int gi = 0; gi < ng; ++gi) {
                   const int i = i0 + gi;
                   XT th = s_blk[i * R + lane], tg = s_blk[(J + i) * R + lane];
   #pragma unroll
                   for (int wq = 0; wq < kWarps; ++wq) {
-                    th = add(th, s_ph[gi][wq][lane]);
-                    tg = add(tg, s_pg[gi][wq][lane]);
+                    th = add(th, pw0[(gi * kWarps + wq) * R + lane]);
+                    tg = add(tg, pw0[((kGroup + gi) * kWarps + wq) * R + lane]);
                   }
                   s_blk[i * R + lane] = th;
                   s_blk[(J + i) * R + lane] = tg;
@@ -965,9 +972,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                   if (i + kStages < J) issue(i + kStages, (int)((ring + i) % kStages));
                 }
               }
-              __syncthreads();   // s_ph/s_pg reused by the next group
+              ++gcount;
             }
             ring += J;
+          }
           }
         }
         w2 = group_reduce<R>(w2, grp);
