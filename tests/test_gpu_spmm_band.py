@@ -140,3 +140,39 @@ def test_gmres_with_band_plan_matches_csr_path(monkeypatch, rng, engine, flexibl
         orc_res = orc.Binding("A", A, None, solver="fgmres" if flexible else "gmres", restart=30,
                               orth="dcgs2" if eng == "persistent" else "cgs2").solve(shift, b, 1e-8)
         assert np.all(np.abs(got.iterations - orc_res.iterations) <= 2)
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 128, 257])
+def test_band_edge_sizes_and_patterns(monkeypatch, rng, n):
+    """Tiny and tile-aligned sizes, an empty row, a missing diagonal entry (the
+    tile's own rows are staged anyway: the shift term needs them)."""
+    d = rng.standard_normal((n, n))
+    d[np.abs(np.subtract.outer(np.arange(n), np.arange(n))) > 2] = 0.0      # pentadiagonal
+    if n >= 5:
+        d[3, :] = 0.0            # empty row
+        d[1, 1] = 0.0            # no diagonal entry in row 1
+    A = sp.csr_matrix(d)
+    A.eliminate_zeros()
+    for shift in (-0.7 + 0j, 0.3 - 1.1j):
+        band, plain = _ops(monkeypatch, A, None, shift, False)
+        assert band.band_info() is not None
+        for r in (1, 3, 8):
+            x = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+            want = orc.ShiftedOp(A, None, shift).apply(x)
+            got = host(band.apply(dev(x)))
+            assert np.array_equal(got, host(plain.apply(dev(x))))
+            assert np.max(np.abs(got - want)) <= 1e-13 * max(np.max(np.abs(want)), 1e-300)
+
+
+@pytest.mark.parametrize("rows", ["32", "64", "128", "256"])
+def test_band_tile_rows_override(monkeypatch, rng, rows):
+    """SAD_BAND_ROWS: every tile size gives the CSR kernel's bits (the 3-D stencil
+    needs five ranges per tile; 256-row tiles merge the +-n0 ranges)."""
+    from paper_2312_02891_b200.problems import convdiff_fd
+    monkeypatch.setenv("SAD_BAND_ROWS", rows)
+    A = convdiff_fd(3, 12, (20.0, -20.0, 20.0))
+    band, plain = _ops(monkeypatch, A, None, -3.0 + 2.0j, True)
+    info = band.band_info()
+    assert info is not None and info["rows"] == int(rows)
+    x = rng.standard_normal((A.shape[0], 4)) + 1j * rng.standard_normal((A.shape[0], 4))
+    assert np.array_equal(host(band.apply(dev(x))), host(plain.apply(dev(x))))
