@@ -928,7 +928,8 @@ def run_ours_c4_rowpart(args, dist):
     lib = _lib.load()
     n0, steps = args.c4_n0, args.c4_steps
     A, X = cfgs.build_c4(n0=n0, r=8, seed=0)
-    shift = 0.1 * (-abs(A.diagonal()).max() * 2.0)
+    pinned = c4_pinned_shift(n0)          # configs/shift_c4.json (the reference's arnoldi_ritz)
+    shift = pinned[0] if pinned is not None else 0.1 * (-abs(A.diagonal()).max() * 2.0)
     n, r = A.shape[0], 8
     rp = RowPartitionedGmres("A", A, None, precond_kind="jacobi", restart=steps,
                              max_iterations=steps, nranks=dist.world, comm="nccl", device=dev)

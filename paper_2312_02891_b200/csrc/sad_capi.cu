@@ -1180,7 +1180,7 @@ struct Launcher {
     a.st = ws->st;
     a.dinv = reinterpret_cast<const XT*>(sizeof(XT) == 8 ? (const void*)op->dinv_r
                                                          : (const void*)op->dinv_c);
-    if (ws->n_ext == ws->n) op_band_args(op, a);
+    op_band_args(op, a);
     if (mode == SPMM_ARNOLDI) {
       a.x = reinterpret_cast<const XT*>(ws->V);
       a.zout = reinterpret_cast<XT*>(ws->Z);

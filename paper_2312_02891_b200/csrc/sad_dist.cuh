@@ -21,6 +21,7 @@
 // kernel ever waits on another rank's kernel) -- the one-GPU test vehicle.
 #pragma once
 
+#include "sad_ring.cuh"
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -356,6 +357,52 @@ static void dot_dual_launch(const OrthArgs& a, int grid, size_t smem, cudaStream
   k_dot_dual<XT, R><<<grid, kThreads, smem, s>>>(a);
 }
 
+// ---- the two DCGS2 sweeps through a TMA ring (sad_ring.cuh), large slabs ----
+template <typename XT, int R>
+static bool ring_launch(const OrthArgs& a, bool dot, int m1, int nsm, bool force, cudaStream_t s) {
+  const size_t smem = dot ? ring_dot_smem<XT, R>(m1) : ring_upd_smem<XT, R>(m1);
+  if (smem > 110 * 1024) return false;                       // two blocks per SM
+  const long long ntiles = (a.n + ring_tile_rows<XT, R>() - 1) / ring_tile_rows<XT, R>();
+  if (ntiles < 4LL * nsm && !force) return false;            // small slabs: the direct kernels
+  static size_t attr[2] = {0, 0};
+  if (smem > attr[dot ? 0 : 1]) {
+    const cudaError_t e = dot
+        ? cudaFuncSetAttribute(k_dot_dual_ring<XT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        : cudaFuncSetAttribute(k_update_ring<XT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    attr[dot ? 0 : 1] = smem;
+  }
+  const int grid = (int)std::min<long long>(ntiles, 2LL * nsm);
+  if (dot) k_dot_dual_ring<XT, R><<<grid, kThreads, smem, s>>>(a);
+  else k_update_ring<XT, R><<<grid, kThreads, smem, s>>>(a);
+  return true;
+}
+
+// false: not launched (block too small / shared memory), the caller runs the direct kernel
+template <typename XT>
+static bool ring_sweep(int R, const OrthArgs& a, bool dot, int m1, int nsm, cudaStream_t s) {
+  // SAD_DIST_RING: 0 = the direct kernels, 1 (default) = the ring for large slabs,
+  // 2 = the ring for every size (tests)
+  const char* ev = getenv("SAD_DIST_RING");
+  const int env = ev && *ev ? atoi(ev) : 1;
+  if (!env) return false;
+  const bool force = env > 1;
+  switch (R) {
+    case 1: return ring_launch<XT, 1>(a, dot, m1, nsm, force, s);
+    case 2: return ring_launch<XT, 2>(a, dot, m1, nsm, force, s);
+    case 3: return ring_launch<XT, 3>(a, dot, m1, nsm, force, s);
+    case 4: return ring_launch<XT, 4>(a, dot, m1, nsm, force, s);
+    case 5: return ring_launch<XT, 5>(a, dot, m1, nsm, force, s);
+    case 6: return ring_launch<XT, 6>(a, dot, m1, nsm, force, s);
+    case 7: return ring_launch<XT, 7>(a, dot, m1, nsm, force, s);
+    case 8: return ring_launch<XT, 8>(a, dot, m1, nsm, force, s);
+  }
+  return false;
+}
+
 template <typename XT>
 static void dot_dual(int R, const OrthArgs& a, int grid, size_t smem, cudaStream_t s) {
   switch (R) {
@@ -540,12 +587,15 @@ extern "C" int sad_local_csr_create(sad_ctx* ctx, int64_t nrows, int64_t ncols, 
   }
   sad_csr* c = new sad_csr();
   c->ctx = ctx;
+  c->uid = g_op_uid.fetch_add(1);
   c->nrows = nrows;
   c->ncols = ncols;
   c->nnz = nnz;
-  std::vector<int> rp(rowptr, rowptr + nrows + 1), ci(colidx, colidx + nnz);
-  std::vector<double> v(vals, vals + nnz);
-  int rc = upload_csr(ctx, c->d, rp, ci, v);
+  // host copies: the banded SpMM plan of the slab pattern is built from them
+  c->h_rowptr.assign(rowptr, rowptr + nrows + 1);
+  c->h_colidx.assign(colidx, colidx + nnz);
+  c->h_vals.assign(vals, vals + nnz);
+  int rc = upload_csr(ctx, c->d, c->h_rowptr, c->h_colidx, c->h_vals);
   if (rc != SAD_OK) {
     free_csr(ctx, c->d);
     delete c;
@@ -570,6 +620,10 @@ extern "C" int sad_local_op_create(sad_ctx* ctx, const sad_csr* base, double sre
   op->n = base->nrows;
   op->ncols = base->ncols;
   op->precond = precond_kind;
+  // banded plan of the slab pattern ([local | halo] columns: the halo rows of x
+  // are one or two more ranges per tile), on first use
+  op->base_csr = base;
+  op->band_ok = band_wanted(base->nnz);
   op->sigma_eff = make_double2(sre, sim);
   op->rowptr = base->d.rowptr;
   op->colidx = base->d.colidx;
@@ -879,14 +933,26 @@ extern "C" int sad_dist_gmres_solve(sad_comm* cm, int nl, sad_gmres* const* W, s
         // DCGS2: one dual dot sweep, finisher A, one update sweep, finisher C
         for (int i = 0; i < nl; ++i) {
           const OrthArgs oa = L[i].orth_args();
-          if (W[i]->dtype == SAD_F64) dot_dual<double>(R, oa, L[i].grid_dot, W[i]->dual_smem, s);
-          else dot_dual<double2>(R, oa, L[i].grid_dot, W[i]->dual_smem, s);
+          const int m1 = W[i]->m + 1;
+          if (W[i]->dtype == SAD_F64) {
+            if (!ring_sweep<double>(R, oa, true, m1, ctx->nsm, s))
+              dot_dual<double>(R, oa, L[i].grid_dot, W[i]->dual_smem, s);
+          } else if (!ring_sweep<double2>(R, oa, true, m1, ctx->nsm, s)) {
+            dot_dual<double2>(R, oa, L[i].grid_dot, W[i]->dual_smem, s);
+          }
         }
         COUNT_LAUNCH(nl);
         if ((rc = AR(cnt_dual))) return rc;
         for (int i = 0; i < nl; ++i) k_dist_finA<<<1, kThreads, 0, s>>>(W[i]->st, W[i]->pst);
         COUNT_LAUNCH(nl);
-        for (int i = 0; i < nl; ++i) L[i].arnoldi(4);     // w -= V S c, ||w||^2
+        for (int i = 0; i < nl; ++i) {                    // w -= V S c, ||w||^2
+          const OrthArgs oa = L[i].orth_args();
+          const int m1 = W[i]->m + 1;
+          const bool ringed = W[i]->dtype == SAD_F64 ? ring_sweep<double>(R, oa, false, m1, ctx->nsm, s)
+                                                     : ring_sweep<double2>(R, oa, false, m1, ctx->nsm, s);
+          if (ringed) COUNT_LAUNCH(1);
+          else L[i].arnoldi(4);
+        }
         if ((rc = AR(R))) return rc;
         for (int i = 0; i < nl; ++i) k_dist_finC<<<1, 32, 0, s>>>(W[i]->st, W[i]->pst);
         COUNT_LAUNCH(nl);

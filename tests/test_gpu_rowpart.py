@@ -228,3 +228,30 @@ def test_sharded_adi_world1_c1(force):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P", [1, 3])
+@pytest.mark.parametrize("r,cplx,flexible", [(2, True, False), (3, True, True), (8, False, False), (5, False, False)])
+def test_rowpart_ring_sweeps_match_direct_kernels(c1, rng, monkeypatch, P, r, cplx, flexible):
+    """The DCGS2 sweeps through the TMA ring (k_dot_dual_ring / k_update_ring,
+    forced here at a small size with SAD_DIST_RING=2; by default only for large
+    slabs) against the direct-load kernels they replace (SAD_DIST_RING=0): same
+    iteration counts, solutions to 1e-10, and the single-GPU counts (+-2)."""
+    from paper_2312_02891_b200.krylov import GpuGmresBinding
+    from paper_2312_02891_b200.rowpart import RowPartitionedGmres
+    A = c1[0]
+    n = A.shape[0]
+    shift = -40.0 + (12.0j if cplx else 0.0)
+    rhs = rng.standard_normal((n, r)) + (1j * rng.standard_normal((n, r)) if cplx else 0.0)
+    delta = 1e-9 * np.linalg.norm(rhs)
+    out = {}
+    for mode in ("2", "0"):
+        monkeypatch.setenv("SAD_DIST_RING", mode)
+        rp = RowPartitionedGmres("A", A, None, nranks=P, restart=30, flexible=flexible)
+        out[mode] = rp.solve(shift, rhs, delta)
+    ring, direct = out["2"], out["0"]
+    assert np.all(ring.converged)
+    assert np.array_equal(ring.iterations, direct.iterations)
+    assert np.max(np.abs(ring.solution - direct.solution)) <= 1e-10 * np.max(np.abs(direct.solution))
+    one = GpuGmresBinding("A", A, None, restart=30, flexible=flexible).solve(shift, rhs, delta)
+    assert np.all(np.abs(ring.iterations - one.iterations) <= 2)
