@@ -513,7 +513,7 @@ def run(problem, config, shift_sequence, bindings=None, **kw):
 
 def run_with_state(problem, config, shift_sequence, bindings=None, *, restart=50,
                    flexible=False, device=0, concurrent="auto", keep_on_device=False,
-                   engine="persistent", solver="gmres"):
+                   engine="auto", solver="gmres"):
     """adi.py:553-607.  ``bindings=None`` runs the device-resident driver with
     GpuGmresBinding(restart, flexible) on both sides; otherwise the host loop
     drives the given bindings."""
@@ -609,6 +609,8 @@ def _record(k, scaled, dec, rA, rB, ra, rb, u, v, wall_ms):
 #: largest A-side block (n x r complex128 bytes) for which the A and B solves
 #: run concurrently by default (DeviceAdi(concurrent="auto"))
 CONCURRENT_MAX_BLOCK_BYTES = 16 << 20
+#: engine="auto": the ring multi-kernel engine when both sides' blocks are at least this large
+AUTO_RING_BLOCK_BYTES = 192 << 20
 
 
 class DeviceAdi:
@@ -616,7 +618,7 @@ class DeviceAdi:
     (the bench times repeated runs with the inputs already in HBM)."""
 
     def __init__(self, problem, config, shift_sequence, *, restart=50, flexible=False,
-                 device=0, concurrent="auto", engine="persistent", phase_a="auto",
+                 device=0, concurrent="auto", engine="auto", phase_a="auto",
                  row_ranks=1, solver="gmres", native="auto", sm_split=None):
         import torch
         if not isinstance(problem, SylvesterProblem):
@@ -629,6 +631,16 @@ class DeviceAdi:
                     f"{config.strategy.value}: direct inner solves are not on the GPU hot path")
         self.problem, self.config, self.shifts = problem, config, shift_sequence
         self.device = device
+        if engine == "auto":
+            # Both sides HBM-bound and large (config 5: 512 / 262 MB blocks): the
+            # multi-kernel delayed-Gram engine -- stand-alone banded SpMM and the
+            # basis sweeps through a TMA ring, one slab per side -- beats the
+            # persistent kernel, whose in-kernel SpMM sub-phase shares the block's
+            # shared memory with the sweeps (config 5: 39.4 s vs 44.2 s).  Smaller
+            # blocks are bound by per-step latency: one persistent launch per solve
+            # (config 3: 16.4 s vs 17.9 s; config 2: 0.07 s vs 0.36 s).
+            big = min(problem.n, problem.m) * problem.r * 16 >= AUTO_RING_BLOCK_BYTES
+            engine = "rowpart" if (big and solver == "gmres" and problem.r <= 8) else "persistent"
         self.engine = engine
         self.solver = solver
         # the outer loop in native code (sad_adi_run) for the persistent GMRES
@@ -669,9 +681,11 @@ class DeviceAdi:
             frac_a = float(sm_split)
         sm_a = max(1, min(nsm - 1, int(round(nsm * frac_a)))) if concurrent else 0
         sm_b = max(1, nsm - sm_a) if concurrent else 0
-        if row_ranks > 1:
+        if row_ranks > 1 or engine == "rowpart":
             # each side row-partitioned over `row_ranks` slabs, all ranks in this
-            # process on one device (rowpart.py; the one-GPU test vehicle)
+            # process on one device (rowpart.py; the one-GPU test vehicle).
+            # engine="rowpart" with one slab = the multi-kernel delayed-Gram engine
+            # with the ring sweeps on the whole operator
             from .rowpart import RowPartitionedGmres
             self.concurrent = False
             self._pool = None
@@ -918,7 +932,7 @@ def _seq_len(seq):
 
 
 def _run_device(problem, config, shifts, restart, flexible, device, concurrent,
-                keep_on_device, engine="persistent", solver="gmres"):
+                keep_on_device, engine="auto", solver="gmres"):
     t0 = time.perf_counter()
     eng = DeviceAdi(problem, config, shifts, restart=restart, flexible=flexible,
                     device=device, concurrent=concurrent, engine=engine, solver=solver)

@@ -162,6 +162,17 @@ class _Comm:
         return self.handle.h
 
 
+class _OpRef:
+    """A single-GPU DeviceOperator standing in for the one slab of a P = 1 group."""
+
+    def __init__(self, dop):
+        self.dop = dop
+
+    @property
+    def h(self):
+        return self.dop.handle
+
+
 class RowPartitionedGmres:
     """Jacobi-GMRES(m)/FGMRES(m) on a row-partitioned operator (see module doc)."""
 
@@ -174,7 +185,7 @@ class RowPartitionedGmres:
             raise NotImplementedError("direct inner solves are outside the GPU hot path")
         if precond_kind not in _KIND:
             raise ValueError(f"preconditioner {precond_kind!r} is not available on the GPU path")
-        if mass is not None:
+        if mass is not None and int(nranks) != 1:
             raise NotImplementedError("a non-identity mass matrix is not row-partitioned "
                                       "(generalised pencils run A || B, BASELINE config 3)")
         if orth not in ("dcgs2", "cgs2"):
@@ -187,6 +198,14 @@ class RowPartitionedGmres:
         self.device = device
         self.mass = None
         self._ctx = _lib.context(device)
+        self._base_dm = None
+        if mass is not None:
+            # one slab: the whole generalised pencil, assembled per shift by the
+            # single-GPU operator (sad_op_create); DeviceAdi reads .mass for M z / C^T y
+            from .device import DeviceMatrix
+            adj = (side == "B")
+            self._base_dm = base if isinstance(base, DeviceMatrix) else DeviceMatrix(base, adj, device)
+            self.mass = mass if isinstance(mass, DeviceMatrix) else DeviceMatrix(mass, adj, device)
         csr = as_csr(base)
         if side == "B":
             csr = as_csr(csr.T.tocsr())
@@ -235,12 +254,18 @@ class RowPartitionedGmres:
             s = np.conj(shift) if self.side == "B" else shift
             lib = _lib.load()
             ops = []
-            for slab in self._slabs:
-                h = ctypes.c_void_p()
-                _lib.check(lib.sad_local_op_create(self._ctx, slab.h, s.real, s.imag,
-                                                   _KIND[self.precond_kind], ctypes.byref(h)),
-                           self._ctx)
-                ops.append(_Handle(h, "sad_op_destroy"))
+            if self.mass is not None:
+                from .device import DeviceOperator
+                dop = DeviceOperator(self._base_dm, self.mass, shift, adjoint=(self.side == "B"),
+                                     precond_kind=self.precond_kind)
+                ops.append(_OpRef(dop))
+            else:
+                for slab in self._slabs:
+                    h = ctypes.c_void_p()
+                    _lib.check(lib.sad_local_op_create(self._ctx, slab.h, s.real, s.imag,
+                                                       _KIND[self.precond_kind], ctypes.byref(h)),
+                               self._ctx)
+                    ops.append(_Handle(h, "sad_op_destroy"))
             import torch
             stream = torch.cuda.current_stream(torch.device("cuda", self.device))
             _lib.check(lib.sad_dist_op_setup(self.comm.h, self.nl, _ptrs([o.h for o in ops]),

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--concurrent", action="store_true", help="A and B solves overlapped")
     ap.add_argument("--phase-a", default="auto", choices=["auto", "tma", "direct"])
     ap.add_argument("--profile", action="store_true", help="instrumented pass (GB/s per kernel)")
+    ap.add_argument("--engine", default="persistent", choices=["persistent", "multi", "rowpart"])
     args = ap.parse_args()
     warnings.simplefilter("ignore")
     spec = cfgs.CONFIGS[args.config]
@@ -44,7 +45,7 @@ def main():
     t0 = time.perf_counter()
     eng = pb.DeviceAdi(prob, cfg, seq, restart=spec.restart, flexible=spec.flexible,
                        concurrent=False if args.sequential else (True if args.concurrent else "auto"),
-                       phase_a=args.phase_a)
+                       phase_a=args.phase_a, engine=args.engine)
     eng.warm()
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
