@@ -209,7 +209,17 @@ def make_sharded(problem, config, shifts, *, restart=30, flexible=False, device=
             continue
         base, mass = (problem.A, problem.M) if side == "A" else (problem.B, problem.C)
         kind = config.precond_kind_A if side == "A" else config.precond_kind_B
-        if len(ranks) == 1 and not force_rowpart:
+        from .adi import AUTO_RING_BLOCK_BYTES
+        big = ((problem.n if side == "A" else problem.m) * problem.r * 16 >= AUTO_RING_BLOCK_BYTES
+               and problem.r <= 8)
+        if len(ranks) == 1 and big and not force_rowpart:
+            # a large side on one GPU: the ring multi-kernel engine on one slab
+            # (DeviceAdi's engine="auto" rule; config 5 at 2 GPUs)
+            s = RowPartitionedGmres(side, base, mass, "iterative", kind, nranks=1, comm="local",
+                                    **kw)
+            solvers[side] = s
+            slabs[side] = (0, s.n)
+        elif len(ranks) == 1 and not force_rowpart:
             # a side on one GPU: the persistent single-GPU engine (also takes a
             # mass matrix, config 3 at 2 GPUs = A || B)
             s = GpuGmresBinding(side, base, mass, "iterative", kind, engine="persistent", **kw)
