@@ -224,6 +224,11 @@ int band_values(sad_ctx* ctx, const BandPlan* p, const VT* vals_dev, VT** out) {
   k_band_values<VT><<<blocks, 256>>>(p->nent, p->perm, vals_dev, *out);
   COUNT_LAUNCH(1);
   CKL(ctx);
+  // Plans are built on first use, possibly from a solve on a non-blocking stream
+  // (the concurrent A / B solves of DeviceAdi): the values must be complete before
+  // any stream reads them, so the legacy-stream kernel is waited for here (once
+  // per operator and plan class).
+  CK(ctx, cudaStreamSynchronize(cudaStreamLegacy));
   return SAD_OK;
 }
 
