@@ -74,8 +74,9 @@ static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
     attr = true;
   }
-  static size_t nb_smem = 0;
-  static int nb = 0;
+  // per host thread: the A- and B-side solves may launch from two threads
+  static thread_local size_t nb_smem = 0;
+  static thread_local int nb = 0;
   if (nb_smem != smem) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads + 32, smem);
     nb_smem = smem;
