@@ -1472,7 +1472,12 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     if (!e) return -1;
     return std::string(e) == "tma" ? 0 : 1;
   }();
-  const int sweep_direct = sweep_env >= 0 ? sweep_env : ((32 % ws->R) != 0 ? 1 : 0);
+  // (round 2, with one synchronisation per group in the ring sweep: on blocks of
+  // 32 MB and more the ring wins for R = 3 too -- config 3's A side 294 -> 282 us of
+  // phase-A work per step, its B side, 23.5 MB, stays with the direct loads)
+  const bool small_block = (size_t)ws->n * R * ws->esz < ((size_t)32 << 20);
+  const int sweep_direct =
+      sweep_env >= 0 ? sweep_env : (((32 % ws->R) != 0 && small_block) ? 1 : 0);
   // Banded plan for the SpMM sub-phase (large slabs): the stages share the ring
   // region; two blocks per SM must still fit, with at least two stages
   const BandPlan* bp = nullptr;
