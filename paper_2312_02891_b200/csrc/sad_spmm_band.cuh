@@ -57,9 +57,21 @@ struct BandCfg {
 // run 8 or 16 warps per SM on dependent shared-memory loads, so the instruction-
 // level parallelism is what keeps them ahead of the copies): 4 when a tile holds
 // four passes of the block, else 2 (config 4, 256-row tiles: U = 2 0.537 ms, 4 0.509 ms)
-template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U>
+// PAIR: a real fp64 block with an even number of columns processed as R pairs
+// (XT = double2, 16-byte lanes: half the instructions per byte -- the 8-byte-lane
+// kernel is instruction-bound, config 4's Arnoldi SpMM 0.96 ms vs 0.52 ms).  Every
+// product is then COMPONENTWISE: real matrix values and a real Jacobi diagonal
+// (a.dinv points to doubles) times a pair, a real shift, the two columns' own
+// scales S -- the same real operations as the unpaired kernel, bit for bit.
+__device__ __forceinline__ double2 pscal(double2 s, double2 v) {
+  return make_double2(s.x == 0.0 ? 0.0 : s.x * v.x, s.y == 0.0 ? 0.0 : s.y * v.y);
+}
+
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, BandCfg cfg) {
+  static_assert(!PAIR || (sizeof(XT) == 16 && sizeof(VT) == 8), "pairs: double2 lanes, real values");
   constexpr int GPW = 32 / R;
+  constexpr unsigned DS = PAIR ? 8u : (unsigned)sizeof(XT);   // bytes per Jacobi row
   const int TR = a.band_tr;
   constexpr unsigned RB = R * sizeof(XT);
   extern __shared__ __align__(128) unsigned char smem_b[];
@@ -136,11 +148,11 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
         len = (unsigned)(((s1 + 15ull) & ~15ull) - src);
         dst = 16u + (unsigned)m.ro[lane] * RB - (unsigned)(s0 - src);
         if (PRE) {
-          const unsigned long long d0 = reinterpret_cast<unsigned long long>(a.dinv) + (unsigned long long)m.xs[lane] * sizeof(XT);
-          const unsigned long long d1 = d0 + (unsigned long long)m.xl[lane] * sizeof(XT);
+          const unsigned long long d0 = reinterpret_cast<unsigned long long>(a.dinv) + (unsigned long long)m.xs[lane] * DS;
+          const unsigned long long d1 = d0 + (unsigned long long)m.xl[lane] * DS;
           dsrc = d0 & ~15ull;
           dlen = (unsigned)(((d1 + 15ull) & ~15ull) - dsrc);
-          ddst = cfg.offD + 16u + (unsigned)m.ro[lane] * (unsigned)sizeof(XT) - (unsigned)(d0 - dsrc);
+          ddst = cfg.offD + 16u + (unsigned)m.ro[lane] * DS - (unsigned)(d0 - dsrc);
         }
       } else if (lane == 30) {
         src = reinterpret_cast<unsigned long long>(a.band_idx + m.eoff);
@@ -172,13 +184,29 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
   const int grp = lane / R, c = lane - grp * R;
   const bool lane_ok = grp < GPW;
   double scale = 1.0;
-  if (MODE == SPMM_ARNOLDI) scale = lane_ok ? a.st.S[jcur * R + c] : 0.0;
+  double2 scale2 = make_double2(1.0, 1.0);
+  if (MODE == SPMM_ARNOLDI) {
+    if (PAIR) {
+      if (lane_ok) scale2 = make_double2(a.st.S[jcur * 2 * R + 2 * c], a.st.S[jcur * 2 * R + 2 * c + 1]);
+    } else {
+      scale = lane_ok ? a.st.S[jcur * R + c] : 0.0;
+    }
+  }
+  // x_l scaled by the Jacobi row l; the result scaled per column
+  auto dmul = [&](const unsigned char* dbase, int l, XT v) -> XT {
+    if constexpr (PAIR) return mul(reinterpret_cast<const double*>(dbase)[l], v);
+    else return mul(reinterpret_cast<const XT*>(dbase)[l], v);
+  };
+  auto colscale = [&](XT v) -> XT {
+    if constexpr (PAIR) return pscal(scale2, v);
+    else return sscal(scale, v);
+  };
   for (long long k = 0; k < K; ++k) {
     const int st = (int)(k % S);
     mbar_wait(full + st, (unsigned)((k / S) & 1));
     const unsigned char* base = smem_b + (size_t)st * cfg.SB;
     const XT* xs = reinterpret_cast<const XT*>(base + 16);
-    const XT* ds = reinterpret_cast<const XT*>(base + cfg.offD + 16);
+    const unsigned char* ds = base + cfg.offD + 16;
     const unsigned short* si = reinterpret_cast<const unsigned short*>(base + cfg.offI);
     const VT* sv = reinterpret_cast<const VT*>(base + cfg.offV);
     const int W = s_W[st], self = s_self[st];
@@ -203,7 +231,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
             const int e = t * TR + lr[u];
             const int l = si[e];
             XT xv = xs[l * R + c];
-            if (PRE) xv = mul(ds[l], xv);
+            if (PRE) xv = dmul(ds, l, xv);
             acc[u] = fma_(sv[e], xv, acc[u]);
           }
         }
@@ -215,11 +243,14 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
           if (SIGMA || (MODE == SPMM_ARNOLDI && zout)) {
             const int ls = self + lr[u];
             XT xi = xs[ls * R + c];
-            if (PRE) xi = mul(ds[ls], xi);
-            if (SIGMA) vres = fma_(from_c<XT>(a.sigma), xi, vres);
-            if (MODE == SPMM_ARNOLDI && zout) zout[idx] = sscal(scale, xi);
+            if (PRE) xi = dmul(ds, ls, xi);
+            if (SIGMA) {
+              if constexpr (PAIR) vres = fma_(a.sigma.x, xi, vres);
+              else vres = fma_(from_c<XT>(a.sigma), xi, vres);
+            }
+            if (MODE == SPMM_ARNOLDI && zout) zout[idx] = colscale(xi);
           }
-          if (MODE == SPMM_ARNOLDI) vres = sscal(scale, vres);
+          if (MODE == SPMM_ARNOLDI) vres = colscale(vres);
           if (MODE == SPMM_RESID || MODE == SPMM_RESID_CYCLE) vres = sub(a.b[idx], vres);
           y[idx] = vres;
         }

@@ -3,6 +3,7 @@
 //   0: fp64 apply/residual   1: complex128 apply/residual
 //   2: fp64 Arnoldi/cycle    3: complex128 Arnoldi/cycle
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "sad_spmm_launch.cuh"
@@ -30,10 +31,10 @@ static size_t al128(size_t b) { return (b + 127) & ~size_t(127); }
 
 // Banded plan: stage layout and pipeline depth for this block type; false when
 // two stages do not fit (the CSR kernel runs instead)
-template <typename XT, typename VT, int R, bool PRE>
+template <typename XT, typename VT, int R, bool PRE, bool PAIR = false>
 static bool band_config(int xcap, int wmax, int tr, BandCfg& cfg, size_t& smem) {
   const size_t xb = al128(32 + (size_t)xcap * R * sizeof(XT));
-  const size_t db = PRE ? al128(32 + (size_t)xcap * sizeof(XT)) : 0;
+  const size_t db = PRE ? al128(32 + (size_t)xcap * (PAIR ? 8 : sizeof(XT))) : 0;
   const size_t ib = al128((size_t)wmax * tr * 2);
   const size_t vb = al128((size_t)wmax * tr * sizeof(VT));
   const size_t sb = xb + db + ib + vb;
@@ -49,7 +50,7 @@ static bool band_config(int xcap, int wmax, int tr, BandCfg& cfg, size_t& smem) 
   return true;
 }
 
-template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U>
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U, bool PAIR = false>
 static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s);
 
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
@@ -59,7 +60,7 @@ static bool launch_band(const SpmmArgs<XT>& a, cudaStream_t s) {
   return launch_band_u<XT, VT, R, MODE, PRE, SIGMA, 2>(a, s);
 }
 
-template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U>
+template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U, bool PAIR>
 static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s) {
   // TMA sources must be 16-byte aligned up to the parity rule of the plan
   const XT* xsrc = a.x;
@@ -67,8 +68,8 @@ static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s) {
   if (MODE == SPMM_ARNOLDI && ((size_t)a.stride * sizeof(XT)) % 16) return false;
   BandCfg cfg{};
   size_t smem = 0;
-  if (!band_config<XT, VT, R, PRE>(a.band_xcap, a.band_wmax, a.band_tr, cfg, smem)) return false;
-  auto kern = k_spmm_band<XT, VT, R, MODE, PRE, SIGMA, U>;
+  if (!band_config<XT, VT, R, PRE, PAIR>(a.band_xcap, a.band_wmax, a.band_tr, cfg, smem)) return false;
+  auto kern = k_spmm_band<XT, VT, R, MODE, PRE, SIGMA, U, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
@@ -160,9 +161,59 @@ static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, i
   return true;
 }
 
+#if SAD_SPMM_PART == 2
+// Arnoldi-mode SpMM of a real block with an even number of columns through the
+// banded kernel's PAIR mode (16-byte lanes); false: not applicable, the caller
+// runs the per-column kernels
+template <int RP, bool PRE, bool SIGMA>
+static bool pair_arnoldi_u(const SpmmArgs<double2>& z, cudaStream_t s) {
+  if (z.band_tr >= 4 * kWarps * (32 / RP))
+    return launch_band_u<double2, double, RP, SPMM_ARNOLDI, PRE, SIGMA, 4, true>(z, s);
+  return launch_band_u<double2, double, RP, SPMM_ARNOLDI, PRE, SIGMA, 2, true>(z, s);
+}
+template <int RP>
+static bool pair_arnoldi_r(const SpmmArgs<double2>& z, bool pre, bool sigma, cudaStream_t s) {
+  if (pre) return sigma ? pair_arnoldi_u<RP, true, true>(z, s) : pair_arnoldi_u<RP, true, false>(z, s);
+  return sigma ? pair_arnoldi_u<RP, false, true>(z, s) : pair_arnoldi_u<RP, false, false>(z, s);
+}
+static bool pair_arnoldi(const SpmmArgs<double>& a, int R, bool pre, bool sigma, cudaStream_t s) {
+  if (R % 2 || a.sigma.y != 0.0 || !a.band_meta || a.row0 != 0 || (a.stride & 1)) return false;
+  static const bool off = [] {
+    const char* e = getenv("SAD_SPMM_PAIRS");
+    return e && *e && atoi(e) == 0;
+  }();
+  if (off) return false;
+  SpmmArgs<double2> z{};
+  z.n = a.n; z.rowptr = a.rowptr; z.colidx = a.colidx; z.vals = a.vals;
+  z.x = reinterpret_cast<const double2*>(a.x);
+  z.y = reinterpret_cast<double2*>(a.y);
+  z.b = reinterpret_cast<const double2*>(a.b);
+  z.dinv = reinterpret_cast<const double2*>(a.dinv);      // doubles: read as such in PAIR mode
+  z.zout = reinterpret_cast<double2*>(a.zout);
+  z.sigma = a.sigma;
+  z.stride = a.stride / 2;
+  z.row0 = 0;
+  z.band_meta = a.band_meta; z.band_idx = a.band_idx; z.band_val = a.band_val;
+  z.band_xcap = a.band_xcap; z.band_wmax = a.band_wmax; z.band_tr = a.band_tr;
+  z.st = a.st;
+  switch (R / 2) {
+    case 1: return pair_arnoldi_r<1>(z, pre, sigma, s);
+    case 2: return pair_arnoldi_r<2>(z, pre, sigma, s);
+    case 3: return pair_arnoldi_r<3>(z, pre, sigma, s);
+    case 4: return pair_arnoldi_r<4>(z, pre, sigma, s);
+  }
+  return false;
+}
+#endif
+
 template <typename XT, int MODE>
 int launch_spmm(const SpmmArgs<XT>& a, int R, bool vc, bool pre, bool sigma, int nsm,
                 cudaStream_t s, int grid_cap) {
+#if SAD_SPMM_PART == 2
+  if constexpr (std::is_same<XT, double>::value && MODE == SPMM_ARNOLDI) {
+    if (pair_arnoldi(a, R, pre, sigma, s)) return 0;
+  }
+#endif
   if constexpr (std::is_same<XT, double>::value && (MODE == SPMM_APPLY || MODE == SPMM_RESID)) {
     if (spmm_pairs(a, R, pre, sigma, nsm, s, MODE)) return 0;
   }
