@@ -875,6 +875,10 @@ def run_ours_c4(args, dist):
                          "dram_gbs": traffic / (spmm_ms * 1e-3) / 1e9 if traffic else None,
                          "dram_frac": traffic / (spmm_ms * 1e-3) / 1e9 / peak if traffic else None,
                          "band_plan": band,
+                         "note": "frac = SURVEY 8d's algorithmic (CSR) bytes / time / peak; the banded "
+                                 "plan moves fewer bytes than that formula (10 B per nonzero, no row "
+                                 "offsets), so frac can pass 1.0 -- dram_frac (ncu DRAM traffic / time / "
+                                 "peak) is the device's own rate" if band else None,
                          "traffic_source": tr_ent and (f"profiles/traffic.json[c4_spmm]: "
                                                        f"{tr_ent['note']}"),
                          "peak_kind": peak_kind, "algorithmic_bytes_per_launch": spmm_b,

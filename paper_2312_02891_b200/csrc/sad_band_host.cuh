@@ -19,11 +19,14 @@ constexpr int kBandXMax = 1400;      // local rows per tile the plan accepts
 struct BandPlan {
   long long n = 0, ntiles = 0, nent = 0, nnz = 0;
   int xcap = 0, wmax = 0, tr = 0;      // tr: rows per tile
+  int xstride = 0;                     // local rows reserved per tile in the Jacobi-row copies (even)
   BandMeta* meta = nullptr;            // device
-  unsigned short* idx = nullptr;       // device
+  unsigned short* idx = nullptr;       // device: local row of every padded slot
   int* perm = nullptr;                 // device: CSR position of every padded slot (-1 = padding)
-  double* pval_base = nullptr;         // device: values of the matrix itself (operators with
-                                       // identity mass share them; the shift is in the epilogue)
+  int* lrow = nullptr;                 // device [ntiles * xstride]: x row of every local row (-1 unused)
+  unsigned char* seg_base = nullptr;   // device: values + indices segments of the matrix itself
+                                       // (operators with identity mass share them; the shift is
+                                       // in the epilogue)
 };
 
 // the plans of one pattern (a matrix side, or a merged base + mass pattern whose
@@ -47,7 +50,8 @@ void band_free(sad_ctx* ctx, BandPlan* p) {
   ctx_free(ctx, p->meta);
   ctx_free(ctx, p->idx);
   ctx_free(ctx, p->perm);
-  ctx_free(ctx, p->pval_base);
+  ctx_free(ctx, p->lrow);
+  ctx_free(ctx, p->seg_base);
   delete p;
 }
 
@@ -103,6 +107,7 @@ void band_tile_ranges(long long n, const int* rp, const int* ci, long long t, in
     pos += len;
   }
   out.rows_total = (int)pos + 1;
+  m.xrows = out.rows_total;
 }
 
 inline int band_local(const BandMeta& m, int col) {
@@ -147,14 +152,19 @@ BandPlan* band_build_tr(sad_ctx* ctx, long long n, const std::vector<int>& rp, c
   }
   if (nent > nnz + nnz / 2 + 64 * kBandRows) return nullptr;   // too much padding
   if (stage_limit && (size_t)xcap * 72 + (size_t)wmax * TR * 10 > stage_limit) return nullptr;
+  const int xstride = (xcap + 1) & ~1;
   std::vector<unsigned short> idx((size_t)nent);
   std::vector<int> perm((size_t)nent);
+  std::vector<int> lrow((size_t)ntiles * xstride, -1);
   std::vector<BandMeta> meta(ntiles);
   std::atomic<bool> bad{false};
   par([&](long long t0, long long t1) {
     for (long long t = t0; t < t1; ++t) {
       const BandMeta& m = info[t].m;
       meta[t] = m;
+      for (int q = 0; q < m.nr; ++q)
+        for (int k = 0; k < (int)m.xl[q]; ++k)
+          lrow[(size_t)t * xstride + m.ro[q] + k] = m.xs[q] + k;
       const long long r0 = t * kBandRows;
       for (int lr = 0; lr < kBandRows; ++lr) {
         const long long i = r0 + lr;
@@ -183,9 +193,12 @@ BandPlan* band_build_tr(sad_ctx* ctx, long long n, const std::vector<int>& rp, c
   p->xcap = xcap;
   p->wmax = wmax;
   p->tr = TR;
+  p->xstride = xstride;
   if (ctx_malloc(ctx, (void**)&p->meta, (size_t)ntiles * sizeof(BandMeta)) != cudaSuccess ||
       ctx_malloc(ctx, (void**)&p->idx, (size_t)nent * 2 + 64) != cudaSuccess ||
       ctx_malloc(ctx, (void**)&p->perm, (size_t)nent * 4) != cudaSuccess ||
+      ctx_malloc(ctx, (void**)&p->lrow, lrow.size() * 4) != cudaSuccess ||
+      cudaMemcpy(p->lrow, lrow.data(), lrow.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->meta, meta.data(), (size_t)ntiles * sizeof(BandMeta), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->idx, idx.data(), (size_t)nent * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->perm, perm.data(), (size_t)nent * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -216,18 +229,31 @@ BandPlan* band_build(sad_ctx* ctx, long long n, const std::vector<int>& rp, cons
   return band_build_tr(ctx, n, rp, ci, 64, 0);
 }
 
-// padded values of a plan from CSR values on the device
+// values + indices segments of a plan from CSR values on the device
 template <typename VT>
-int band_values(sad_ctx* ctx, const BandPlan* p, const VT* vals_dev, VT** out) {
-  CK(ctx, ctx_malloc(ctx, (void**)out, (size_t)p->nent * sizeof(VT) + 64));
-  const int blocks = (int)std::min<long long>((p->nent + 255) / 256, (long long)ctx->nsm * 32);
-  k_band_values<VT><<<blocks, 256>>>(p->nent, p->perm, vals_dev, *out);
+int band_segments(sad_ctx* ctx, const BandPlan* p, const VT* vals_dev, unsigned char** out) {
+  CK(ctx, ctx_malloc(ctx, (void**)out, (size_t)p->nent * (sizeof(VT) + 2) + 64));
+  const int blocks = (int)std::min<long long>(p->ntiles, (long long)ctx->nsm * 16);
+  k_band_segments<VT><<<blocks, 256>>>(p->ntiles, p->tr, p->meta, p->idx, p->perm, vals_dev, *out);
   COUNT_LAUNCH(1);
   CKL(ctx);
   // Plans are built on first use, possibly from a solve on a non-blocking stream
-  // (the concurrent A / B solves of DeviceAdi): the values must be complete before
+  // (the concurrent A / B solves of DeviceAdi): the segments must be complete before
   // any stream reads them, so the legacy-stream kernel is waited for here (once
   // per operator and plan class).
+  CK(ctx, cudaStreamSynchronize(cudaStreamLegacy));
+  return SAD_OK;
+}
+
+// the Jacobi rows of every tile in local row order (per operator: D depends on the shift)
+template <typename DT>
+int band_dinv_rows(sad_ctx* ctx, const BandPlan* p, const DT* dinv_dev, DT** out) {
+  const long long count = p->ntiles * (long long)p->xstride;
+  CK(ctx, ctx_malloc(ctx, (void**)out, (size_t)count * sizeof(DT) + 64));
+  const int blocks = (int)std::min<long long>((count + 255) / 256, (long long)ctx->nsm * 32);
+  k_band_dinv<DT><<<blocks, 256>>>(count, p->lrow, dinv_dev, *out);
+  COUNT_LAUNCH(1);
+  CKL(ctx);
   CK(ctx, cudaStreamSynchronize(cudaStreamLegacy));
   return SAD_OK;
 }

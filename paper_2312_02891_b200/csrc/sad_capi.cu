@@ -120,8 +120,11 @@ struct sad_op {
   int adjoint = 0;
   BandSet* bset = nullptr;
   const BandPlan* band[2] = {nullptr, nullptr};
-  const void* band_val[2] = {nullptr, nullptr};
-  void* own_band_val[2] = {nullptr, nullptr};
+  const unsigned char* band_seg[2] = {nullptr, nullptr};
+  unsigned char* own_band_seg[2] = {nullptr, nullptr};
+  // the tiles' Jacobi rows in the plan's layout, [class][0 real / 1 complex], built when a
+  // block of that type first runs the Jacobi prologue
+  void* band_dinv[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   bool band_tried[2] = {false, false};
   bool band_ok = false;               // SAD_SPMM_BAND / size rule, read when the operator is created
   bool vals_complex = false;
@@ -635,8 +638,11 @@ extern "C" int sad_op_destroy(sad_op* op) {
   ctx_free(op->ctx, op->own_rowptr);
   ctx_free(op->ctx, op->own_colidx);
   ctx_free(op->ctx, op->own_vals);
-  ctx_free(op->ctx, op->own_band_val[0]);
-  ctx_free(op->ctx, op->own_band_val[1]);
+  for (int cl = 0; cl < 2; ++cl) {
+    ctx_free(op->ctx, op->own_band_seg[cl]);
+    ctx_free(op->ctx, op->band_dinv[cl][0]);
+    ctx_free(op->ctx, op->band_dinv[cl][1]);
+  }
   ctx_free(op->ctx, op->dinv_c);   // dinv_r lives in the same allocation
   delete op;
   return SAD_OK;
@@ -664,7 +670,7 @@ static const BandPlan* op_band(sad_op* op, int cls) {
     if (p && !op->mass_uid) {
       // identity mass: the operators of every shift share the matrix's values
       const DevCsr& bd = op->adjoint ? bm->dt : bm->d;
-      if (band_values<double>(ctx, p, bd.vals, &p->pval_base) != SAD_OK) {
+      if (band_segments<double>(ctx, p, bd.vals, &p->seg_base) != SAD_OK) {
         band_free(ctx, p);
         p = nullptr;
       }
@@ -674,20 +680,40 @@ static const BandPlan* op_band(sad_op* op, int cls) {
   const BandPlan* p = bs->plan[cls];
   if (!p || p->nnz != op->nnz) return nullptr;
   if (!op->mass_uid) {
-    op->band_val[cls] = p->pval_base;
+    op->band_seg[cls] = p->seg_base;
   } else {
     const int rc = op->vals_complex
-        ? band_values<double2>(ctx, p, (const double2*)op->own_vals, (double2**)&op->own_band_val[cls])
-        : band_values<double>(ctx, p, (const double*)op->own_vals, (double**)&op->own_band_val[cls]);
+        ? band_segments<double2>(ctx, p, (const double2*)op->own_vals, &op->own_band_seg[cls])
+        : band_segments<double>(ctx, p, (const double*)op->own_vals, &op->own_band_seg[cls]);
     if (rc != SAD_OK) {
-      ctx_free(ctx, op->own_band_val[cls]);
-      op->own_band_val[cls] = nullptr;
+      ctx_free(ctx, op->own_band_seg[cls]);
+      op->own_band_seg[cls] = nullptr;
       return nullptr;
     }
-    op->band_val[cls] = op->own_band_val[cls];
+    op->band_seg[cls] = op->own_band_seg[cls];
   }
   op->band[cls] = p;
   return p;
+}
+
+// The tiles' Jacobi rows for blocks of the given type (built on first use; nullptr on failure)
+static const void* op_band_dinv(sad_op* op, int cls, bool cplx) {
+  const BandPlan* p = op->band[cls];
+  if (!p) return nullptr;
+  void*& slot = op->band_dinv[cls][cplx ? 1 : 0];
+  if (!slot) {
+    sad_csr* bm = const_cast<sad_csr*>(op->base_csr);
+    std::lock_guard<std::mutex> lk(bm->band_mu);
+    if (!slot) {
+      const int rc = cplx ? band_dinv_rows<double2>(op->ctx, p, op->dinv_c, (double2**)&slot)
+                          : band_dinv_rows<double>(op->ctx, p, op->dinv_r, (double**)&slot);
+      if (rc != SAD_OK) {
+        ctx_free(op->ctx, slot);
+        slot = nullptr;
+      }
+    }
+  }
+  return slot;
 }
 
 // info[7]: plan present (0/1), tiles, padded entries, nonzeros, local x rows per
@@ -723,9 +749,12 @@ template <typename XT>
 static void op_band_args(sad_op* op, SpmmArgs<XT>& a) {
   const BandPlan* p = op_band(op, 0);
   if (!p) return;
+  const void* dv = op_band_dinv(op, 0, sizeof(XT) == 16);
+  if (!dv) return;
   a.band_meta = p->meta;
-  a.band_idx = p->idx;
-  a.band_val = op->band_val[0];
+  a.band_seg = op->band_seg[0];
+  a.band_dinv = dv;
+  a.band_xstride = p->xstride;
   a.band_xcap = p->xcap;
   a.band_wmax = p->wmax;
   a.band_tr = p->tr;
@@ -1481,6 +1510,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   // Banded plan for the SpMM sub-phase (large slabs): the stages share the ring
   // region; two blocks per SM must still fit, with at least two stages
   const BandPlan* bp = nullptr;
+  const void* bdinv = nullptr;
   BandCfg bcfg{};
   static const int band_p_env = [] {
     const char* e = getenv("SAD_BAND_PERSISTENT");
@@ -1497,9 +1527,8 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
       auto al128 = [](size_t b) { return (b + 127) & ~size_t(127); };
       const size_t xb = al128(32 + (size_t)p->xcap * R * ws->esz);
       const size_t db = al128(32 + (size_t)p->xcap * ws->esz);
-      const size_t ib = al128((size_t)p->wmax * p->tr * 2);
-      const size_t vb = al128((size_t)p->wmax * p->tr * vsz);
-      const size_t sb = xb + db + ib + vb;
+      const size_t vb = al128((size_t)p->wmax * p->tr * (vsz + 2));   // values + indices
+      const size_t sb = xb + db + vb;
       const size_t other = sums;
       // per block: two blocks stay within the 196 KB carve-out (SAD_BAND_CAP_KB: A/B runs)
       static const size_t cap_env = [] {
@@ -1514,13 +1543,14 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
         return e && *e ? atoi(e) : 0;
       }();
       if (s_env > 0) S = std::min(S, s_env);
-      if (S >= 2) {
+      const void* dv = S >= 2 ? op_band_dinv(op, 1, ws->dtype == SAD_C128) : nullptr;
+      if (S >= 2 && dv) {
         bp = p;
+        bdinv = dv;
         bcfg.S = S;
         bcfg.SB = (unsigned)sb;
         bcfg.offD = (unsigned)xb;
-        bcfg.offI = (unsigned)(xb + db);
-        bcfg.offV = (unsigned)(xb + db + ib);
+        bcfg.offV = (unsigned)(xb + db);
         ring_bytes = std::max(ring_bytes, (size_t)S * sb + recs);
       }
     }
@@ -1546,8 +1576,9 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     PArgs<double> a = make_pargs<double>(ws, op, rhs, x);
     if (bp) {
       a.band_meta = bp->meta;
-      a.band_idx = bp->idx;
-      a.band_val = op->band_val[1];
+      a.band_seg = op->band_seg[1];
+      a.band_dinv = bdinv;
+      a.band_xstride = bp->xstride;
       a.band_tr = bp->tr;
       a.band_cfg = bcfg;
     }
@@ -1565,8 +1596,9 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
     if (bp) {
       a.band_meta = bp->meta;
-      a.band_idx = bp->idx;
-      a.band_val = op->band_val[1];
+      a.band_seg = op->band_seg[1];
+      a.band_dinv = bdinv;
+      a.band_xstride = bp->xstride;
       a.band_tr = bp->tr;
       a.band_cfg = bcfg;
     }

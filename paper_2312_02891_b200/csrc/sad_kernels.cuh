@@ -410,8 +410,9 @@ struct SpmmArgs {
   // banded plan (sad_spmm_band.cuh; null = the CSR kernels): tile records, 16-bit
   // local row indices and values in the padded slot-major layout
   const void* band_meta;
-  const unsigned short* band_idx;
-  const void* band_val;
+  const unsigned char* band_seg;      // per tile: values, then 16-bit local row indices
+  const void* band_dinv;              // per tile: the Jacobi rows in local row order (PRE)
+  int band_xstride;                   // local rows reserved per tile in band_dinv
   int band_xcap, band_wmax, band_tr;   // local x rows / padded row length (max), rows per tile
   GState st;
 };

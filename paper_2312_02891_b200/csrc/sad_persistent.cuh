@@ -97,8 +97,9 @@ struct PArgs {
   // banded plan for sub-phase A1 (sad_spmm_band.cuh; null: the CSR tiles): rows per
   // block are a multiple of band_tr, the stages live in the ring region
   const void* band_meta;
-  const unsigned short* band_idx;
-  const void* band_val;
+  const unsigned char* band_seg;   // per tile: values, then 16-bit local row indices
+  const void* band_dinv;           // per tile: the Jacobi rows in local row order
+  int band_xstride;
   int band_tr;
   BandCfg band_cfg;
   PState st;
@@ -571,7 +572,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             const int TR = a.band_tr, S1 = a.band_cfg.S;
             constexpr unsigned RB = R * sizeof(XT);
             const BandMeta* metas = reinterpret_cast<const BandMeta*>(a.band_meta) + r0 / TR;
-            const VT* bvals = reinterpret_cast<const VT*>(a.band_val);
             const long long ntile = r1 > r0 ? (r1 - r0 + TR - 1) / TR : 0;
             BandMeta(*s_bmeta)[32] =
                 reinterpret_cast<BandMeta(*)[32]>(smem_c + (size_t)S1 * a.band_cfg.SB);
@@ -587,31 +587,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               const BandMeta& m = s_bmeta[(int)((t >> 5) & 1)][(int)(t & 31)];
               const int q = (int)((ringb + t) % S1);
               const unsigned nent = (unsigned)m.W * TR;
-              unsigned long long src = 0, dsrc = 0;
-              unsigned len = 0, dlen = 0, dst = 0, ddst = 0;
+              unsigned long long src = 0;
+              unsigned len = 0, dst = 0;
               if (lane < m.nr) {
                 const unsigned long long s0 = reinterpret_cast<unsigned long long>(vj) + (unsigned long long)m.xs[lane] * RB;
                 const unsigned long long s1 = s0 + (unsigned long long)m.xl[lane] * RB;
                 src = s0 & ~15ull;
                 len = (unsigned)(((s1 + 15ull) & ~15ull) - src);
                 dst = 16u + (unsigned)m.ro[lane] * RB - (unsigned)(s0 - src);
-                if (PRE) {
-                  const unsigned long long d0 = reinterpret_cast<unsigned long long>(a.dinv) + (unsigned long long)m.xs[lane] * sizeof(XT);
-                  const unsigned long long d1 = d0 + (unsigned long long)m.xl[lane] * sizeof(XT);
-                  dsrc = d0 & ~15ull;
-                  dlen = (unsigned)(((d1 + 15ull) & ~15ull) - dsrc);
-                  ddst = a.band_cfg.offD + 16u + (unsigned)m.ro[lane] * (unsigned)sizeof(XT) - (unsigned)(d0 - dsrc);
-                }
               } else if (lane == 30) {
-                src = reinterpret_cast<unsigned long long>(a.band_idx + m.eoff);
-                len = nent * 2u;
-                dst = a.band_cfg.offI;
+                // the tile's Jacobi rows in local row order (one copy per tile)
+                const long long tile = r0 / TR + t;
+                src = reinterpret_cast<unsigned long long>(a.band_dinv) +
+                      (unsigned long long)tile * (unsigned long long)a.band_xstride * sizeof(XT);
+                len = ((unsigned)m.xrows * (unsigned)sizeof(XT) + 15u) & ~15u;
+                dst = a.band_cfg.offD + 16u;
               } else if (lane == 31) {
-                src = reinterpret_cast<unsigned long long>(bvals + m.eoff);
-                len = nent * (unsigned)sizeof(VT);
+                // values then indices of the tile, one segment
+                src = reinterpret_cast<unsigned long long>(a.band_seg) +
+                      (unsigned long long)m.eoff * (unsigned long long)(sizeof(VT) + 2);
+                len = nent * (unsigned)(sizeof(VT) + 2);
                 dst = a.band_cfg.offV;
               }
-              unsigned bytes = len + dlen;
+              unsigned bytes = len;
 #pragma unroll
               for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
               unsigned char* sb = smem_c + (size_t)q * a.band_cfg.SB;
@@ -622,7 +620,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               }
               __syncwarp();
               if (len) bulk_g2s(sb + dst, reinterpret_cast<const void*>(src), len, s_fullb + q);
-              if (PRE && dlen) bulk_g2s(sb + ddst, reinterpret_cast<const void*>(dsrc), dlen, s_fullb + q);
             };
             // warp 0 produces (runs up to S1 tiles ahead, waiting on the stage's
             // "empty" barrier), warps 1..7 consume: no block-wide synchronisation
@@ -653,9 +650,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
                 const unsigned char* sb = smem_c + (size_t)q * a.band_cfg.SB;
                 const XT* xs = reinterpret_cast<const XT*>(sb + 16);
                 const XT* ds = reinterpret_cast<const XT*>(sb + a.band_cfg.offD + 16);
-                const unsigned short* si = reinterpret_cast<const unsigned short*>(sb + a.band_cfg.offI);
-                const VT* sv = reinterpret_cast<const VT*>(sb + a.band_cfg.offV);
                 const int W = s_bW[q], self = s_bself[q];
+                const VT* sv = reinterpret_cast<const VT*>(sb + a.band_cfg.offV);
+                const unsigned short* si = reinterpret_cast<const unsigned short*>(sv + (size_t)W * TR);
                 const long long row0 = r0 + t * TR;
                 if (lane_ok) {
                   constexpr int UB = 2;

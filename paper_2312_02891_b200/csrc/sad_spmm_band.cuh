@@ -13,9 +13,11 @@
 //   * the tile's nonzeros in a slot-major padded layout [W][kBandRows] with the
 //     column replaced by the 16-bit LOCAL row index into that buffer.
 // The kernel is then pure streaming: a producer warp issues, per tile, one
-// cp.async.bulk (1-D TMA) per x range, one for the indices and one for the
-// values (and one per range of the Jacobi diagonal), S tiles ahead, completing
-// on an mbarrier; consumer warps read everything from shared memory with no
+// cp.async.bulk (1-D TMA) per x range, ONE for the tile's values + indices
+// (stored back to back in one segment) and ONE for the tile's Jacobi rows (a
+// per-operator copy of D^-1 in the tile's local row order) -- the kernel is
+// bound by the number of copies per tile, not by their bytes -- S tiles ahead,
+// completing on an mbarrier; consumer warps read everything from shared memory with no
 // global load on their critical path, no row-length predicates, and write y.
 // Per row the products are summed in the CSR (increasing column) order, padded
 // slots add v = 0 times the row's own x entry.
@@ -42,14 +44,14 @@ struct __align__(16) BandMeta {      // 64 bytes per tile
   int xs[kBandMaxRanges];            // first x row of range q
   unsigned short xl[kBandMaxRanges]; // rows in range q
   unsigned short ro[kBandMaxRanges]; // local row of range q (ro == xs mod 2, one spare row between ranges)
-  int pad;
+  int xrows;                         // local rows in use (the tile's Jacobi rows)
 };
 static_assert(sizeof(BandMeta) == 64, "BandMeta is one 64-byte record");
 
 struct BandCfg {
   int S;                  // pipeline stages
   unsigned SB;            // bytes per stage
-  unsigned offD, offI, offV;   // dinv rows, indices, values inside a stage (x rows at 0)
+  unsigned offD, offV;    // Jacobi rows, values + indices segment inside a stage (x rows at 0)
 };
 
 
@@ -67,8 +69,18 @@ __device__ __forceinline__ double2 pscal(double2 s, double2 v) {
   return make_double2(s.x == 0.0 ? 0.0 : s.x * v.x, s.y == 0.0 ? 0.0 : s.y * v.y);
 }
 
+// U encodes the consumer shape: U = 2: 8 consumer warps, two rows per lane group in
+// flight, two blocks per SM for small stages; U = 4: SIXTEEN consumer warps with two
+// rows each (tiles of 256 rows and other one-block-per-SM stages: the consumers are
+// bound by dependent shared-memory loads, and with the Jacobi prologue 8 warps per
+// SM fell behind the copies -- config 4's Arnoldi SpMM 0.87 ms vs 0.49 ms plain).
+template <int U> __host__ __device__ constexpr int band_consumer_warps() { return U >= 4 ? 16 : 8; }
+
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA, int U, bool PAIR = false>
-__global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, BandCfg cfg) {
+__global__ void __launch_bounds__((band_consumer_warps<U>() + 1) * 32, U >= 4 ? 1 : 2)
+k_spmm_band(SpmmArgs<XT> a, BandCfg cfg) {
+  constexpr int NCW = band_consumer_warps<U>();   // consumer warps; warp NCW produces
+  constexpr int UR = 2;                           // rows per lane group in flight
   static_assert(!PAIR || (sizeof(XT) == 16 && sizeof(VT) == 8), "pairs: double2 lanes, real values");
   constexpr int GPW = 32 / R;
   constexpr unsigned DS = PAIR ? 8u : (unsigned)sizeof(XT);   // bytes per Jacobi row
@@ -87,7 +99,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
   if (threadIdx.x == 0) {
     for (int q = 0; q < S; ++q) {
       mbar_init(full + q, 1);
-      mbar_init(empty + q, kWarps);
+      mbar_init(empty + q, NCW);
     }
     fence_mbar_init();
   }
@@ -104,7 +116,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
   __syncthreads();
   const BandMeta* metas = reinterpret_cast<const BandMeta*>(a.band_meta);
 
-  if (warp == kWarps) {
+  if (warp == NCW) {
     // ---------------- producer ----------------
     // Tile records are fetched 32 at a time, one per lane, a batch ahead of their
     // use, into shared memory.  Per tile every copy has its own lane: lane q < nr
@@ -113,7 +125,6 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
     // cp.async.bulk instruction issues all of them; lane 0 only waits for the
     // stage to be free and arms the barrier with the byte total.
     __shared__ __align__(16) BandMeta s_meta[2][32];
-    const VT* vals = reinterpret_cast<const VT*>(a.band_val);
     auto fetch = [&](long long kk, int buf) {
       if (kk < K) {
         const int4* src = reinterpret_cast<const int4*>(metas + (blockIdx.x + kk * G));
@@ -137,9 +148,9 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
       const int st = (int)(k % S);
       const int nr = m.nr;
       const unsigned nent = (unsigned)m.W * TR;
-      unsigned long long src = 0, dsrc = 0;
-      unsigned len = 0, dlen = 0, dst = 0, ddst = 0;
-      // widened, 16-byte aligned copies: source and destination are congruent
+      unsigned long long src = 0;
+      unsigned len = 0, dst = 0;
+      // x ranges: widened, 16-byte aligned copies: source and destination are congruent
       // mod 16 (ro == xs mod 2, 16-aligned bases), spare rows absorb the slack
       if (lane < nr) {
         const unsigned long long s0 = reinterpret_cast<unsigned long long>(x) + (unsigned long long)m.xs[lane] * RB;
@@ -147,23 +158,24 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
         src = s0 & ~15ull;
         len = (unsigned)(((s1 + 15ull) & ~15ull) - src);
         dst = 16u + (unsigned)m.ro[lane] * RB - (unsigned)(s0 - src);
-        if (PRE) {
-          const unsigned long long d0 = reinterpret_cast<unsigned long long>(a.dinv) + (unsigned long long)m.xs[lane] * DS;
-          const unsigned long long d1 = d0 + (unsigned long long)m.xl[lane] * DS;
-          dsrc = d0 & ~15ull;
-          dlen = (unsigned)(((d1 + 15ull) & ~15ull) - dsrc);
-          ddst = cfg.offD + 16u + (unsigned)m.ro[lane] * DS - (unsigned)(d0 - dsrc);
-        }
       } else if (lane == 30) {
-        src = reinterpret_cast<unsigned long long>(a.band_idx + m.eoff);
-        len = nent * 2u;
-        dst = cfg.offI;
+        if (PRE) {
+          // the tile's Jacobi rows, already in local row order (16-byte aligned: the
+          // per-tile stride is even)
+          const long long tile = blockIdx.x + k * G;
+          src = reinterpret_cast<unsigned long long>(a.band_dinv) +
+                (unsigned long long)tile * (unsigned long long)a.band_xstride * DS;
+          len = ((unsigned)m.xrows * DS + 15u) & ~15u;
+          dst = cfg.offD + 16u;
+        }
       } else if (lane == 31) {
-        src = reinterpret_cast<unsigned long long>(vals + m.eoff);
-        len = nent * (unsigned)sizeof(VT);
+        // values then indices of the tile, one segment
+        src = reinterpret_cast<unsigned long long>(a.band_seg) +
+              (unsigned long long)m.eoff * (unsigned long long)(sizeof(VT) + 2);
+        len = nent * (unsigned)(sizeof(VT) + 2);
         dst = cfg.offV;
       }
-      unsigned bytes = len + dlen;
+      unsigned bytes = len;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
       unsigned char* base = smem_b + (size_t)st * cfg.SB;
@@ -175,7 +187,6 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
       }
       __syncwarp();
       if (len) bulk_g2s(base + dst, reinterpret_cast<const void*>(src), len, full + st);
-      if (PRE && dlen) bulk_g2s(base + ddst, reinterpret_cast<const void*>(dsrc), dlen, full + st);
     }
     return;
   }
@@ -207,27 +218,27 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
     const unsigned char* base = smem_b + (size_t)st * cfg.SB;
     const XT* xs = reinterpret_cast<const XT*>(base + 16);
     const unsigned char* ds = base + cfg.offD + 16;
-    const unsigned short* si = reinterpret_cast<const unsigned short*>(base + cfg.offI);
-    const VT* sv = reinterpret_cast<const VT*>(base + cfg.offV);
     const int W = s_W[st], self = s_self[st];
+    const VT* sv = reinterpret_cast<const VT*>(base + cfg.offV);
+    const unsigned short* si = reinterpret_cast<const unsigned short*>(sv + (size_t)W * TR);
     const long long r0 = (blockIdx.x + k * G) * (long long)TR;
     if (lane_ok) {
-      for (int rb = 0; rb < TR; rb += kWarps * GPW * U) {
-        int lr[U];
-        bool ok[U];
-        XT acc[U];
+      for (int rb = 0; rb < TR; rb += NCW * GPW * UR) {
+        int lr[UR];
+        bool ok[UR];
+        XT acc[UR];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          lr[u] = rb + (u * kWarps + warp) * GPW + grp;
+        for (int u = 0; u < UR; ++u) {
+          lr[u] = rb + (u * NCW + warp) * GPW + grp;
           ok[u] = lr[u] < TR && r0 + lr[u] < a.n;
           if (!ok[u]) lr[u] = 0;
           acc[u] = zero<XT>();
         }
-        if (!ok[0] && !ok[U - 1]) continue;
+        if (!ok[0] && !ok[UR - 1]) continue;
 #pragma unroll 4
         for (int t = 0; t < W; ++t) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
+          for (int u = 0; u < UR; ++u) {
             const int e = t * TR + lr[u];
             const int l = si[e];
             XT xv = xs[l * R + c];
@@ -236,7 +247,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
           }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < UR; ++u) {
           if (!ok[u]) continue;
           const long long idx = (r0 + lr[u]) * R + c;
           XT vres = acc[u];
@@ -261,14 +272,36 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_spmm_band(SpmmArgs<XT> a, 
   }
 }
 
-// values of a padded plan from the operator's CSR values: pval[e] = vals[perm[e]] (0 for padding)
+// The values + indices segment of every tile from the operator's CSR values:
+// tile t at byte eoff * (sizeof(VT) + 2): [W * TR values][W * TR 16-bit local rows]
+// (values 0 and the row's own local index for padding).  One block per tile.
 template <typename VT>
-__global__ void k_band_values(long long nent, const int* __restrict__ perm, const VT* __restrict__ vals,
-                              VT* __restrict__ out) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nent;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int p = perm[e];
-    out[e] = p >= 0 ? vals[p] : zero<VT>();
+__global__ void k_band_segments(long long ntiles, int TR, const BandMeta* __restrict__ meta,
+                                const unsigned short* __restrict__ idx, const int* __restrict__ perm,
+                                const VT* __restrict__ vals, unsigned char* __restrict__ seg) {
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const unsigned eoff = meta[t].eoff;
+    const int nent = (int)meta[t].W * TR;
+    unsigned char* base = seg + (size_t)eoff * (sizeof(VT) + 2);
+    VT* v = reinterpret_cast<VT*>(base);
+    unsigned short* ix = reinterpret_cast<unsigned short*>(base + (size_t)nent * sizeof(VT));
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+      const int p = perm[eoff + e];
+      v[e] = p >= 0 ? vals[p] : zero<VT>();
+      ix[e] = idx[eoff + e];
+    }
+  }
+}
+
+// The Jacobi rows of every tile in its local row order: out[t * xstride + l] =
+// dinv[lrow[t * xstride + l]] (0 for unused local rows)
+template <typename DT>
+__global__ void k_band_dinv(long long count, const int* __restrict__ lrow, const DT* __restrict__ dinv,
+                            DT* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = lrow[i];
+    out[i] = g >= 0 ? dinv[g] : zero<DT>();
   }
 }
 

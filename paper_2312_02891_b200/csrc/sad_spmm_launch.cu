@@ -32,20 +32,18 @@ static size_t al128(size_t b) { return (b + 127) & ~size_t(127); }
 // Banded plan: stage layout and pipeline depth for this block type; false when
 // two stages do not fit (the CSR kernel runs instead)
 template <typename XT, typename VT, int R, bool PRE, bool PAIR = false>
-static bool band_config(int xcap, int wmax, int tr, BandCfg& cfg, size_t& smem) {
+static bool band_config(int xcap, int wmax, int tr, bool one_block, BandCfg& cfg, size_t& smem) {
   const size_t xb = al128(32 + (size_t)xcap * R * sizeof(XT));
   const size_t db = PRE ? al128(32 + (size_t)xcap * (PAIR ? 8 : sizeof(XT))) : 0;
-  const size_t ib = al128((size_t)wmax * tr * 2);
-  const size_t vb = al128((size_t)wmax * tr * sizeof(VT));
-  const size_t sb = xb + db + ib + vb;
-  int S = (int)std::min<size_t>(6, (110 * 1024) / sb);         // two blocks per SM
-  if (S < 3) S = (int)std::min<size_t>(6, (212 * 1024) / sb);  // one block per SM
+  const size_t vb = al128((size_t)wmax * tr * (sizeof(VT) + 2));   // values + indices
+  const size_t sb = xb + db + vb;
+  int S = one_block ? 0 : (int)std::min<size_t>(6, (110 * 1024) / sb);   // two blocks per SM
+  if (S < 3) S = (int)std::min<size_t>(6, (212 * 1024) / sb);            // one block per SM
   if (S < 2) return false;
   cfg.S = S;
   cfg.SB = (unsigned)sb;
   cfg.offD = (unsigned)xb;
-  cfg.offI = (unsigned)(xb + db);
-  cfg.offV = (unsigned)(xb + db + ib);
+  cfg.offV = (unsigned)(xb + db);
   smem = (size_t)S * sb;
   return true;
 }
@@ -56,7 +54,10 @@ static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s);
 template <typename XT, typename VT, int R, int MODE, bool PRE, bool SIGMA>
 static bool launch_band(const SpmmArgs<XT>& a, cudaStream_t s) {
   if (!a.band_meta || a.row0 != 0) return false;
-  if (a.band_tr >= 4 * kWarps * (32 / R)) return launch_band_u<XT, VT, R, MODE, PRE, SIGMA, 4>(a, s);
+  // 16 consumer warps (U = 4, one block per SM) when a tile holds two rows per lane group
+  // of 16 warps (config 4: 256-row tiles); tiles of 16 warps x ONE row are slower than 8
+  // warps x two rows (config 5, 128-row tiles: 516 vs 449 us)
+  if (a.band_tr >= 2 * 16 * (32 / R)) return launch_band_u<XT, VT, R, MODE, PRE, SIGMA, 4>(a, s);
   return launch_band_u<XT, VT, R, MODE, PRE, SIGMA, 2>(a, s);
 }
 
@@ -68,7 +69,7 @@ static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s) {
   if (MODE == SPMM_ARNOLDI && ((size_t)a.stride * sizeof(XT)) % 16) return false;
   BandCfg cfg{};
   size_t smem = 0;
-  if (!band_config<XT, VT, R, PRE, PAIR>(a.band_xcap, a.band_wmax, a.band_tr, cfg, smem)) return false;
+  if (!band_config<XT, VT, R, PRE, PAIR>(a.band_xcap, a.band_wmax, a.band_tr, U >= 4, cfg, smem)) return false;
   auto kern = k_spmm_band<XT, VT, R, MODE, PRE, SIGMA, U, PAIR>;
   static bool attr = false;
   if (!attr) {
@@ -79,13 +80,13 @@ static bool launch_band_u(const SpmmArgs<XT>& a, cudaStream_t s) {
   static thread_local size_t nb_smem = 0;
   static thread_local int nb = 0;
   if (nb_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads + 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, (band_consumer_warps<U>() + 1) * 32, smem);
     nb_smem = smem;
   }
   if (nb < 1) return false;
   const long long tiles = (a.n + a.band_tr - 1) / a.band_tr;
   const int g = (int)std::max(1LL, std::min(tiles, (long long)nb * g_spmm_bulk_sms));
-  kern<<<g, kThreads + 32, smem, s>>>(a, cfg);
+  kern<<<g, (band_consumer_warps<U>() + 1) * 32, smem, s>>>(a, cfg);
   count_launches(1);
   return true;
 }
@@ -154,7 +155,8 @@ static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, i
   z.b = reinterpret_cast<const double2*>(a.b);
   z.sigma = a.sigma;
   z.row0 = a.row0;
-  z.band_meta = a.band_meta; z.band_idx = a.band_idx; z.band_val = a.band_val;
+  z.band_meta = a.band_meta; z.band_seg = a.band_seg; z.band_dinv = a.band_dinv;
+  z.band_xstride = a.band_xstride;
   z.band_xcap = a.band_xcap; z.band_wmax = a.band_wmax; z.band_tr = a.band_tr;
   if (mode == SPMM_APPLY) launch_spmm<double2, SPMM_APPLY>(z, R / 2, false, false, sigma, nsm, s);
   else launch_spmm<double2, SPMM_RESID>(z, R / 2, false, false, sigma, nsm, s);
@@ -167,7 +169,7 @@ static bool spmm_pairs(const SpmmArgs<double>& a, int R, bool pre, bool sigma, i
 // runs the per-column kernels
 template <int RP, bool PRE, bool SIGMA>
 static bool pair_arnoldi_u(const SpmmArgs<double2>& z, cudaStream_t s) {
-  if (z.band_tr >= 4 * kWarps * (32 / RP))
+  if (z.band_tr >= 2 * 16 * (32 / RP))
     return launch_band_u<double2, double, RP, SPMM_ARNOLDI, PRE, SIGMA, 4, true>(z, s);
   return launch_band_u<double2, double, RP, SPMM_ARNOLDI, PRE, SIGMA, 2, true>(z, s);
 }
@@ -193,7 +195,8 @@ static bool pair_arnoldi(const SpmmArgs<double>& a, int R, bool pre, bool sigma,
   z.sigma = a.sigma;
   z.stride = a.stride / 2;
   z.row0 = 0;
-  z.band_meta = a.band_meta; z.band_idx = a.band_idx; z.band_val = a.band_val;
+  z.band_meta = a.band_meta; z.band_seg = a.band_seg; z.band_dinv = a.band_dinv;
+  z.band_xstride = a.band_xstride;
   z.band_xcap = a.band_xcap; z.band_wmax = a.band_wmax; z.band_tr = a.band_tr;
   z.st = a.st;
   switch (R / 2) {
