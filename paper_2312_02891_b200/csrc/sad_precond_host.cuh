@@ -189,9 +189,9 @@ struct TriFactor {
   // schedules per lane-group count 32/R (built on demand)
   struct Sched { int* order = nullptr; int ntasks = 0; };
   std::map<int, Sched> sched;
-  int* ready = nullptr;
-  int ready_r = 0;
-  int epoch = 0;
+  void* cells = nullptr;       // 16-byte {value, epoch} cells of the solved elements
+  size_t cells_cap = 0;        // cells allocated
+  long long epoch = 0;
   unsigned* counter = nullptr;
 };
 
@@ -216,7 +216,7 @@ void tri_free(sad_ctx* ctx, TriFactor& f) {
   ctx_free(ctx, f.colidx);
   ctx_free(ctx, f.vals);
   ctx_free(ctx, f.diag);
-  ctx_free(ctx, f.ready);
+  ctx_free(ctx, f.cells);
   ctx_free(ctx, f.counter);
   for (auto& kv : f.sched) ctx_free(ctx, kv.second.order);
   f = TriFactor();
@@ -302,18 +302,15 @@ int tri_solve(sad_ctx* ctx, TriFactor& f, int r, int dtype, const void* b, void*
   TriFactor::Sched* sc = nullptr;
   int rc = tri_sched(ctx, f, 32 / r, &sc);
   if (rc) return rc;
-  if (f.ready_r < r) {
-    // flags start below any epoch; a wider block needs a longer flag array
+  const size_t need = (size_t)f.n * r * (dtype == SAD_C128 ? 2 : 1);
+  if (f.cells_cap < need) {
+    // tags start below any epoch; a wider (or complex) block needs more cells
     CK(ctx, cudaStreamSynchronize(s));
-    ctx_free(ctx, f.ready);
-    f.ready = nullptr;
-    CK(ctx, ctx_malloc(ctx, (void**)&f.ready, (size_t)f.n * r * sizeof(int)));
-    CK(ctx, cudaMemsetAsync(f.ready, 0, (size_t)f.n * r * sizeof(int), s));
-    f.ready_r = r;
-    f.epoch = 0;
-  }
-  if (f.epoch == INT32_MAX) {
-    CK(ctx, cudaMemsetAsync(f.ready, 0, (size_t)f.n * f.ready_r * sizeof(int), s));
+    ctx_free(ctx, f.cells);
+    f.cells = nullptr;
+    CK(ctx, ctx_malloc(ctx, &f.cells, need * 16));
+    CK(ctx, cudaMemsetAsync(f.cells, 0, need * 16, s));
+    f.cells_cap = need;
     f.epoch = 0;
   }
   TriArgs a{};
@@ -324,7 +321,7 @@ int tri_solve(sad_ctx* ctx, TriFactor& f, int r, int dtype, const void* b, void*
   a.diag = f.diag;
   a.order = sc->order;
   a.ntasks = sc->ntasks;
-  a.ready = f.ready;
+  a.cells = f.cells;
   a.epoch = ++f.epoch;
   a.counter = f.counter;
   a.b = b;
