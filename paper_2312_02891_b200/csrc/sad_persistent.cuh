@@ -141,47 +141,74 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 
-// Arrive at the grid barrier.  Returns true in exactly one block (the last to
-// arrive), which must then do the reduction and call bar_release().
-__device__ __forceinline__ bool bar_arrive(const PState& st, unsigned& gen_seen) {
+// Grid barrier.  The arrival counter is zeroed by the host before every launch
+// and only ever grows: barrier number k (0-based, counted by every block in
+// `narr`) is complete when it reads (k + 1) * gridDim.x, so nothing has to be
+// reset between barriers and no block has to look up the current generation
+// before it arrives (one L2 round trip less per arrival than a counter + flag
+// read pair).  Two uses:
+//  * bar_arrive / bar_release / bar_wait: the last block to arrive does a serial
+//    finisher and then bumps the generation word the others poll (`gen` is the
+//    block's own count of those releases on top of the value at kernel start);
+//  * bar_sync: nobody has anything to do before the release, so the waiting
+//    blocks poll the arrival counter itself -- the last arrival IS the release.
+__device__ __forceinline__ bool bar_arrive(const PState& st, unsigned& narr) {
   __shared__ unsigned s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    gen_seen = ld_relaxed(st.bar_gen);
     const unsigned t = atom_add_acq_rel(st.bar_count, 1u);
-    s_last = (t == gridDim.x - 1) ? 1u : 0u;
+    s_last = (t + 1u == (narr + 1u) * gridDim.x) ? 1u : 0u;
   }
+  ++narr;
   __syncthreads();
   return s_last != 0;
 }
 
-__device__ __forceinline__ void bar_release(const PState& st) {
+__device__ __forceinline__ void bar_release(const PState& st, unsigned& gen) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    *reinterpret_cast<volatile unsigned*>(st.bar_count) = 0u;
-    red_add_release(st.bar_gen, 1u);
-  }
+  if (threadIdx.x == 0) red_add_release(st.bar_gen, 1u);
+  ++gen;
   __syncthreads();
 }
 
-// Non-last blocks wait for the release; spin with a 20 s safety timeout
-// (a hang would otherwise wedge the GPU).
-__device__ __forceinline__ void bar_wait(const PState& st, unsigned gen_seen) {
-  if (threadIdx.x == 0) {
-    unsigned long long t0 = 0;
-    unsigned spins = 0;
-    while (ld_acquire(st.bar_gen) == gen_seen) {
-      if (++spins > 32) __nanosleep(32);
-      if ((spins & 4095u) == 0) {
-        const unsigned long long t = gtimer();
-        if (t0 == 0) t0 = t;
-        else if (t - t0 > 20000000000ull) {
-          atomicExch(st.err, 1);
-          __trap();
-        }
+// spin with a 20 s safety timeout (a hang would otherwise wedge the GPU)
+template <typename Done>
+__device__ __forceinline__ void bar_spin(const PState& st, Done done) {
+  unsigned long long t0 = 0;
+  unsigned spins = 0;
+  while (!done()) {
+    if (++spins > 32) __nanosleep(32);
+    if ((spins & 4095u) == 0) {
+      const unsigned long long t = gtimer();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) {
+        atomicExch(st.err, 1);
+        __trap();
       }
     }
   }
+}
+
+// Non-last blocks wait for the finisher's release.
+__device__ __forceinline__ void bar_wait(const PState& st, unsigned& gen) {
+  if (threadIdx.x == 0) {
+    const unsigned seen = gen;
+    bar_spin(st, [&] { return ld_acquire(st.bar_gen) != seen; });
+  }
+  ++gen;
+  __syncthreads();
+}
+
+// Barrier without a finisher.
+__device__ __forceinline__ void bar_sync(const PState& st, unsigned& narr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned target = (narr + 1u) * gridDim.x;
+    const unsigned t = atom_add_acq_rel(st.bar_count, 1u);
+    if (t + 1u != target)
+      bar_spin(st, [&] { return (int)(ld_acquire(st.bar_count) - target) >= 0; });
+  }
+  ++narr;
   __syncthreads();
 }
 
@@ -281,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
   const int pT = a.pT;
   double2* partT = reinterpret_cast<double2*>(gs.part);
   auto put = [&](int o, double2 v) { partT[(size_t)o * pT + blockIdx.x] = v; };
-  unsigned gen = 0;
+  unsigned gen = ld_relaxed(st.bar_gen);   // before this block's first arrival: no release yet
+  unsigned narr = 0;
   const bool timing = (blockIdx.x == 0 && threadIdx.x == 0);   // counters kept by block 0
   const bool prof = a.prof != 0;                                  // phase timers (profiling)
   unsigned long long tphase = 0;
@@ -393,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
       for (int w = 0; w < kWarps; ++w) t += s_w2[w][threadIdx.x];
       put(threadIdx.x, make_double2(t, 0.0));
     }
-    if (bar_arrive(st, gen)) {
+    if (bar_arrive(st, narr)) {
       reduce_partials_small(partT, pT, gridDim.x, R, st.red);
       __syncthreads();
       __shared__ double s_n2[8];
@@ -418,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         *gs.any_active = any;
         *gs.j = 0;
       }
-      bar_release(st);
+      bar_release(st, gen);
     } else {
       bar_wait(st, gen);
     }
@@ -985,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           put(2 * J * R + threadIdx.x, make_double2(t, 0.0));
         }
         if (timing && prof) t_acc[4] += (double)(gtimer() - tphase);
-        if (bar_arrive(st, gen)) {
+        if (bar_arrive(st, narr)) {
           const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
           const int nout = 2 * J * R + R;
           // smem: reduced sums | S | h1 | new Gram column | active flags
@@ -1065,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           // step's bookkeeping off the critical path.  Its global writes (Gram
           // column, ||w_pre||^2, rotated Hessenberg column) are read by later
           // finishers only, which run after this block's next arrive (release).
-          bar_release(st);
+          bar_release(st, gen);
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
             const int ii = o / R, cc = o - ii * R;
             double2* Gc = st.G + (size_t)cc * (m + 1) * (m + 1);
@@ -1222,8 +1250,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         // the last block and the release.  Block 0 alone writes the global
         // state; the other blocks keep what the next step needs (j, S_{j+1},
         // whether the cycle goes on) in shared memory.
-        if (bar_arrive(st, gen)) bar_release(st);
-        else bar_wait(st, gen);
+        bar_sync(st, narr);
         if (a.dbg_delay_ns > 0 && blockIdx.x == gridDim.x - 1 && gridDim.x > 1) {
           // race stress (tests): block 0 runs ahead and rewrites the global
           // Givens state before this block's finisher runs
@@ -1332,8 +1359,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
               }
             }
             // everyone waits for block 0's back substitution
-            if (bar_arrive(st, gen)) bar_release(st);
-            else bar_wait(st, gen);
+            bar_sync(st, narr);
           }
           if (prof && w0 && threadIdx.x == 0) atomicAdd(st.stats + 11, (double)(gtimer() - tfin));
           if (threadIdx.x == 0) s_any = any_now;
@@ -1371,11 +1397,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         }
       if (timing) acc_bytes += (double)(jx + 2) * (double)a.stride * sizeof(XT) +
                                (FLEX ? 0.0 : (double)n * sizeof(XT));
-      if (bar_arrive(st, gen)) {
-        bar_release(st);
-      } else {
-        bar_wait(st, gen);
-      }
+      bar_sync(st, narr);
     }
     if (timing && prof) { unsigned long long t = gtimer(); t_acc[2] += (double)(t - tphase); tphase = t; }
     // phase R: V_0 = b - Op x, ||.||^2 -> restart decision
@@ -1407,7 +1429,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         for (int wq = 0; wq < kWarps; ++wq) t += s_w2[wq][threadIdx.x];
         put(threadIdx.x, make_double2(t, 0.0));
       }
-      if (bar_arrive(st, gen)) {
+      if (bar_arrive(st, narr)) {
         reduce_partials_small(partT, pT, gridDim.x, R, st.red);
         __syncthreads();
         if (threadIdx.x < R) {
@@ -1428,7 +1450,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           *gs.any_active = any;
           *gs.j = 0;
         }
-        bar_release(st);
+        bar_release(st, gen);
       } else {
         bar_wait(st, gen);
       }
