@@ -79,18 +79,21 @@ __device__ __forceinline__ double2 tdiv(double2 a, double2 b) {
 __device__ __forceinline__ double tneg(double a) { return -a; }
 __device__ __forceinline__ double2 tneg(double2 a) { return make_double2(-a.x, -a.y); }
 
+// One cell is read and written as a single .b128 access (single-copy atomic:
+// value and tag can never be seen torn).
 struct __align__(16) TriCell { double v; long long tag; };
 
 __device__ __forceinline__ TriCell ld_cell(const TriCell* p) {
   TriCell c;
   unsigned long long lo, hi;
-  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+  asm volatile("{\n\t.reg .b128 q;\n\tld.relaxed.gpu.global.b128 q, [%2];\n\tmov.b128 {%0, %1}, q;\n\t}"
+               : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
   c.v = __longlong_as_double((long long)lo);
   c.tag = (long long)hi;
   return c;
 }
 __device__ __forceinline__ void st_cell(TriCell* p, double v, long long tag) {
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p),
+  asm volatile("{\n\t.reg .b128 q;\n\tmov.b128 q, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], q;\n\t}" ::"l"(p),
                "l"((unsigned long long)__double_as_longlong(v)), "l"((unsigned long long)tag)
                : "memory");
 }
