@@ -141,6 +141,14 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Grid barrier.  The arrival counter is zeroed by the host before every launch
 // and only ever grows: barrier number k (0-based, counted by every block in
 // `narr`) is complete when it reads (k + 1) * gridDim.x, so nothing has to be
@@ -248,6 +256,35 @@ static __device__ void reduce_partials_T(const double2* partT, int pT, int nbloc
       for (int s = 16; s > 0; s >>= 1) acc[q] = add(acc[q], shfl_down(acc[q], s));
       if (lane == 0 && o0 + q < nout) out[o0 + q] = acc[q];
     }
+  }
+}
+
+// The same reduction spread over the grid (large J * R * blocks: one block can
+// only pull ~100 GB/s out of L2, config 3's 249 x 296 partials took it 16 us per
+// Arnoldi step): after a barrier that makes every block's partials visible,
+// output o is summed by warp (o / nblocks) of block (o % nblocks) -- lane l adds
+// blocks l, l+32, ... in order, then a fixed shuffle tree -- and written to
+// red[o]; the finisher then reads nout values instead of nout * nblocks.
+static __device__ void reduce_partials_dist(const double2* partT, int pT, int nblocks, int nout,
+                                            double2* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int KB = 5;    // 160 blocks per load round
+  for (int o = blockIdx.x + warp * nblocks; o < nout; o += kWarps * nblocks) {
+    const double2* p = partT + (size_t)o * pT;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int b0 = 0; b0 < nblocks; b0 += 32 * KB) {
+      double2 v[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int b = b0 + k * 32 + lane;
+        v[k] = b < nblocks ? __ldcg(p + b) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int k = 0; k < KB; ++k) acc = add(acc, v[k]);
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) acc = add(acc, shfl_down(acc, sh));
+    if (lane == 0) red[o] = acc;
   }
 }
 
@@ -1013,9 +1050,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
           put(2 * J * R + threadIdx.x, make_double2(t, 0.0));
         }
         if (timing && prof) t_acc[4] += (double)(gtimer() - tphase);
+        const int nout = 2 * J * R + R;
+        // >= 512 KB of partials: reduce them on the whole grid first
+        const bool dist_red = (long long)nout * gridDim.x >= 32768 && gridDim.x > 1;
+        if (dist_red) {
+          bar_sync(st, narr);
+          reduce_partials_dist(partT, pT, gridDim.x, nout, st.red);
+        }
         if (bar_arrive(st, narr)) {
           const unsigned long long tfin = (prof && threadIdx.x == 0) ? gtimer() : 0ull;
-          const int nout = 2 * J * R + R;
           // smem: reduced sums | S | h1 | new Gram column | active flags
           double2* s_red = reinterpret_cast<double2*>(smem_p);
           double2* s_h1 = s_red + nout;
@@ -1037,12 +1080,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
             s_csr[cc * j + ii] = ldcg1(gs.cs + (size_t)cc * m + ii);
           }
           if (gsm) {
+            // asynchronous 16-byte copies (L2 -> shared memory, no register in
+            // between): a load + store loop waits for every element at its store,
+            // one L2 round trip each, 19 per thread on config 3 at j = 40
             for (int o = threadIdx.x; o < R * j * j; o += kThreads) {
               const int cc = o / (j * j), rem = o - cc * j * j, ii = rem / j, l = rem - ii * j;
-              s_G[o] = ldcg2(st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1) + l);
+              cp_async16(s_G + o, st.G + (size_t)cc * (m + 1) * (m + 1) + (size_t)ii * (m + 1) + l);
             }
           }
-          reduce_partials_T(partT, pT, gridDim.x, nout, s_red);
+          if (dist_red) {
+            for (int o = threadIdx.x; o < nout; o += kThreads) s_red[o] = ldcg2(st.red + o);
+          } else {
+            reduce_partials_T(partT, pT, gridDim.x, nout, s_red);
+          }
+          cp_async_wait_all();
           __syncthreads();
           // new Gram column G[:, j] and h1 = S h_raw
           for (int o = threadIdx.x; o < J * R; o += kThreads) {
