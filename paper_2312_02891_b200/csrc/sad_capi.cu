@@ -1567,6 +1567,10 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   const size_t csr_budget = (direct && ws->resident_csr && csr_off + 4096 <= per_block_cap)
                                 ? per_block_cap - csr_off : 0;
   if (csr_budget) smem = csr_off + csr_budget;
+  static const int dist_red_env = [] {
+    const char* e = getenv("SAD_DIST_RED_MIN");
+    return e && *e ? atoi(e) : 8192;
+  }();
   static const int ring_c_env = [] {
     const char* e = getenv("SAD_RING_C");
     return e && *e ? atoi(e) : 2;
@@ -1591,6 +1595,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.csr_budget = (int)csr_budget;
     a.sweep_direct = sweep_direct;
     a.ring_c = ring_c_env;
+    a.dist_red_min = dist_red_env;
     e = coop_dispatch_d(a, ws, op, s, smem);
   } else {
     PArgs<double2> a = make_pargs<double2>(ws, op, rhs, x);
@@ -1611,6 +1616,7 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.csr_budget = (int)csr_budget;
     a.sweep_direct = sweep_direct;
     a.ring_c = ring_c_env;
+    a.dist_red_min = dist_red_env;
     e = coop_dispatch_z(a, ws, op, s, smem);
   }
   if (e != cudaSuccess)

@@ -91,6 +91,7 @@ struct PArgs {
   int csr_off;           // dynamic-smem byte offset of the resident CSR slab
   int csr_budget;        // bytes available there (0 = CSR read from global)
   int sweep_direct;      // large slabs: basis sweep by basis block with direct loads (no TMA ring)
+  int dist_red_min;      // finisher A: partials (outputs x blocks) from which the grid reduces them (SAD_DIST_RED_MIN)
   int ring_c;            // large slabs: phase C through the TMA ring (SAD_RING_C: 0 off, 1 only with
                          // the TMA-ring phase-A sweep, 2 = default: always)
   int dbg_delay_ns;      // tests: the last block idles this long after every phase-C release
@@ -1051,8 +1052,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gmres_persistent(PArgs<XT> a) {
         }
         if (timing && prof) t_acc[4] += (double)(gtimer() - tphase);
         const int nout = 2 * J * R + R;
-        // >= 512 KB of partials: reduce them on the whole grid first
-        const bool dist_red = (long long)nout * gridDim.x >= 32768 && gridDim.x > 1;
+        // many partials: reduce them on the whole grid first
+        const bool dist_red = (long long)nout * gridDim.x >= a.dist_red_min && gridDim.x > 1;
         if (dist_red) {
           bar_sync(st, narr);
           reduce_partials_dist(partT, pT, gridDim.x, nout, st.red);
