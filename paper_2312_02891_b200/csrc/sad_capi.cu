@@ -1477,12 +1477,22 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   // direct phase A stages the block's rows of w and v_j in shared memory: an
   // upper bound of the rows per block (the launcher's grid is at least
   // min(n R / (threads * min elems per thread), SMs) blocks)
+  // Sized for `bps` blocks per SM: a direct-path block stays within 110 KB, so two
+  // are resident per SM and the launcher's grid reaches 2 * SMs blocks -- sizing
+  // the rows for one block per SM left no room for the resident CSR slab (config
+  // 2's B side on its 22 SMs: 44 blocks of 614 rows, SpMM sub-phase 13 us from L2
+  // against 2.5 us from shared memory).  If the occupancy turns out lower the
+  // launcher refuses (rows per block > direct_rows) and the sizing is redone for
+  // one block per SM.
+  int bps = 2;
+resize:
+  const size_t slots = (size_t)sms * bps;
   const size_t rows_cap = std::max<size_t>(
       ((size_t)kThreads * std::max(ws->min_elems_per_thread, 1) + R - 1) / R,
-      ((size_t)ws->n + sms - 1) / sms);
+      ((size_t)ws->n + slots - 1) / slots);
   const size_t stage_rows_bytes = 2 * rows_cap * R * ws->esz;
   bool direct = ws->direct_a >= 0 ? ws->direct_a != 0
-                                  : (size_t)ws->n <= 2 * tile_rows * (size_t)sms;
+                                  : (size_t)ws->n <= 2 * tile_rows * slots;
   if (direct && stage_rows_bytes > 96 * 1024) direct = false;   // rows do not fit: TMA ring
   const size_t stage = direct ? 0 : ((tile_rows * R * ws->esz + 32 + 127) & ~size_t(127));
   // s_blk [2(m+1)R] + the ring sweep's per-warp sums (two parity buffers)
@@ -1618,6 +1628,10 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
     a.ring_c = ring_c_env;
     a.dist_red_min = dist_red_env;
     e = coop_dispatch_z(a, ws, op, s, smem);
+  }
+  if (e == cudaErrorInvalidConfiguration && direct && bps == 2) {
+    bps = 1;
+    goto resize;
   }
   if (e != cudaSuccess)
     return set_err(ctx, SAD_ECUDA, "cooperative GMRES launch failed: %s", cudaGetErrorString(e));
