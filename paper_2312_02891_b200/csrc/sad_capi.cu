@@ -1484,7 +1484,9 @@ static int persistent_run(sad_gmres* ws, sad_op* op, const void* rhs, void* x, c
   // against 2.5 us from shared memory).  If the occupancy turns out lower the
   // launcher refuses (rows per block > direct_rows) and the sizing is redone for
   // one block per SM.
+  // SAD_DIRECT_BPS=1: size for one block per SM from the start (A/B runs, tests)
   int bps = 2;
+  if (const char* e = getenv("SAD_DIRECT_BPS")) bps = atoi(e) == 1 ? 1 : 2;
 resize:
   const size_t slots = (size_t)sms * bps;
   const size_t rows_cap = std::max<size_t>(
@@ -1577,10 +1579,9 @@ resize:
   const size_t csr_budget = (direct && ws->resident_csr && csr_off + 4096 <= per_block_cap)
                                 ? per_block_cap - csr_off : 0;
   if (csr_budget) smem = csr_off + csr_budget;
-  static const int dist_red_env = [] {
-    const char* e = getenv("SAD_DIST_RED_MIN");
-    return e && *e ? atoi(e) : 8192;
-  }();
+  // (read per launch: the tests switch it inside one process)
+  const char* dist_red_s = getenv("SAD_DIST_RED_MIN");
+  const int dist_red_env = dist_red_s && *dist_red_s ? atoi(dist_red_s) : 8192;
   static const int ring_c_env = [] {
     const char* e = getenv("SAD_RING_C");
     return e && *e ? atoi(e) : 2;

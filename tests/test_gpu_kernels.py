@@ -242,6 +242,34 @@ def test_gmres_c2_complex_matches_oracle(engine):
         assert np.all(got.converged)
 
 
+@pytest.mark.parametrize("max_sms", [0, 22])
+@pytest.mark.parametrize("red_min", ["8192", "1", "1000000000"])
+def test_persistent_direct_path_sizing_and_grid_reduction(monkeypatch, max_sms, red_min):
+    """The small-slab (direct) phase A sized for two blocks per SM (default) and
+    for one (SAD_DIRECT_BPS=1), on all SMs and on config 2's B-side share of 22,
+    with finisher A's reduction on the whole grid always / by the default rule /
+    never (SAD_DIST_RED_MIN): the same iteration counts as the oracle's run, and
+    solutions equal to 1e-10 across the variants."""
+    from paper_2312_02891_b200 import GpuGmresBinding
+    monkeypatch.setenv("SAD_DIST_RED_MIN", red_min)
+    _, B, _, _, _, g = cfgs.build_problem("c2")
+    pairs, _ = cfgs.CONFIGS["c2"].load_shift_pairs()
+    alpha = pairs[0][0]
+    delta = 1e-9 * np.linalg.norm(g)
+    want = orc.Binding("B", B, None, solver="fgmres", restart=30, orth="dcgs2").solve(alpha, g, delta)
+    sols = []
+    for bps in ("2", "1"):
+        monkeypatch.setenv("SAD_DIRECT_BPS", bps)
+        gb = GpuGmresBinding("B", B, None, precond_kind="jacobi", restart=30, flexible=True,
+                             engine="persistent", phase_a="direct", max_sms=max_sms)
+        got = gb.solve(alpha, g, delta)
+        assert np.all(got.converged)
+        assert np.all(np.abs(got.iterations - want.iterations) <= 2)
+        sols.append(got.solution)
+    assert np.linalg.norm(sols[0] - sols[1]) <= 1e-10 * np.linalg.norm(sols[1])
+    assert np.linalg.norm(sols[0] - want.solution) <= 1e-7 * np.linalg.norm(want.solution)
+
+
 @pytest.mark.parametrize("engine", [e for e, _ in ENGINES])
 def test_gmres_fixed_steps_match_oracle(rng, engine):
     """Fixed-step mode (config 4 path): the true residual after 40 steps

@@ -25,7 +25,7 @@ for split in SPLITS:
     for _ in range(2):
         eng.run()
     ts = []
-    for _ in range(5):
+    for _ in range(int(os.environ.get("REPS", "5"))):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         _, rep, _ = eng.run()
@@ -33,5 +33,5 @@ for split in SPLITS:
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts.sort()
-    print(f"split={split}: median {ts[2]:.1f} ms (inner {rep.sum_inner_A}/{rep.sum_inner_B})", flush=True)
+    print(f"split={split}: min {ts[0]:.1f} median {ts[len(ts) // 2]:.1f} ms (inner {rep.sum_inner_A}/{rep.sum_inner_B})", flush=True)
     del eng
